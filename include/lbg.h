@@ -1,0 +1,167 @@
+/*
+ * lbg.h — C-ABI of the B200-native Lindblad propagation engine (liblbg.so).
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (arxiv/paper_2603_18052 "lindbench", /root/reference/proj). Each entry point
+ * names the reference interface it replaces (file:line, relative to proj/).
+ * Plain pointers and sizes only; no C++ or torch types cross this boundary.
+ *
+ * Conventions:
+ *  - complex128 matrices are row-major; "AoS" = interleaved (re, im) doubles
+ *    exactly like lb::MatrixAoS (include/lb/complex_matrix.hpp:15-31); "SoA" =
+ *    split re / im planes like lb::MatrixSoA (complex_matrix.hpp:35-45).
+ *  - vec(rho) is row-major: rho[i][j] -> slot i*d + j (complex_matrix.hpp:78-81).
+ *  - Functions suffixed _dev take DEVICE pointers, are stream-ordered and
+ *    asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream)
+ *    on the caller's current device. Everything else takes HOST pointers and is
+ *    synchronous.
+ *  - Status codes map 1:1 onto the reference's exception classes; no C++
+ *    exception crosses the ABI. lbg_last_error() returns the calling thread's
+ *    last message.
+ */
+#ifndef LBG_H
+#define LBG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LBG_OK 0
+#define LBG_EINVAL 1   /* std::invalid_argument (propagate.cpp:14-28, lindblad.cpp:25-33, expm.cpp:110-112) */
+#define LBG_ERUNTIME 2 /* std::runtime_error (expm.cpp:40-41,120-121; propagate.cpp:65) */
+#define LBG_ECUDA 3    /* CUDA launch / runtime failure (no reference counterpart) */
+
+/* kernel selection for the batched shared-P stepper (0 = automatic) */
+#define LBG_ALGO_AUTO 0
+#define LBG_ALGO_CHAIN 1   /* K2: one warp, one trajectory, latency-bound (config 0) */
+#define LBG_ALGO_DFMA9 2   /* K1a: n == 9, P in the constant bank, DFMA (config 1) */
+#define LBG_ALGO_SMEM 3    /* K1b: n <= 84, P resident in shared memory, DMMA (config 2) */
+#define LBG_ALGO_TILED 4   /* K1c: any n, P streamed from L2, persistent DMMA tiles (config 3) */
+
+const char* lbg_last_error(void);
+const char* lbg_version(void);
+
+/* ------------------------------------------------------------------------
+ * Raw step kernels — exact signatures of the reference's hot-loop pointers.
+ * Replace lb::StepSoAFn (include/lb/kernels.hpp:23-24) and lb::StepAoSFn
+ * (kernels.hpp:22; cplx* == interleaved double[2]). out[i] = sum_j P[i,j] v[j].
+ * Host pointers; each call uploads P and v, runs one step on the GPU and
+ * downloads `out` (compat shim for parity, not for speed). void return like
+ * the reference; a CUDA failure aborts the process with a message (fail loud).
+ * ------------------------------------------------------------------------ */
+void lbg_step_soa(const double* p_re, const double* p_im, const double* v_re,
+                  const double* v_im, double* out_re, double* out_im, size_t n);
+void lbg_step_aos(const double* p, const double* v, double* out, size_t n);
+
+/* ------------------------------------------------------------------------
+ * Model assembly and propagator (device).
+ * lbg_build_lindbladian_dev: replaces lb::build_lindbladian (lindblad.hpp:34,
+ *   lindblad.cpp:37-59): L = -i(H(x)I - I(x)H^T) + sum_k [L_k(x)conj(L_k)
+ *   - 1/2 L_k^dag L_k (x) I - 1/2 I (x) (L_k^dag L_k)^T], one thread per element.
+ *   h: d*d AoS, ops: n_ops*d*d AoS, out: d^2*d^2 AoS (all device).
+ *   Hermiticity of H is checked on the host side (lbg_build_lindbladian).
+ * lbg_expm_dev: replaces lb::expm (expm.hpp:31, expm.cpp:109-134):
+ *   P = exp(a*dt) for an n x n AoS matrix, by scaling and squaring around a
+ *   degree-16 Taylor polynomial in Paterson-Stockmeyer form (6 DMMA matmuls,
+ *   no solve; truncation <= 2^-54 relative for ||a dt||_1 <= 0.79 after
+ *   scaling). `work` must hold 6*n*n complex (device).
+ * ------------------------------------------------------------------------ */
+int lbg_build_lindbladian(size_t d, const double* h, size_t n_ops, const double* ops,
+                          double* out);
+int lbg_build_lindbladian_dev(size_t d, const double* h, size_t n_ops, const double* ops,
+                              double* out, void* stream);
+int lbg_expm(const double* a, size_t n, double dt, double* out);
+int lbg_expm_dev(const double* a, size_t n, double dt, double* out, double* work,
+                 void* stream);
+size_t lbg_expm_workspace(size_t n); /* bytes */
+
+/* ------------------------------------------------------------------------
+ * Batched shared-P propagation: replaces lb::evolve (propagate.hpp:33-34,
+ * propagate.cpp:75-109) over `batch` independent trajectories.
+ * P: n x n AoS (n = d^2). X: batch x n complex, trajectory b's vec(rho_b) at
+ * X[b*n ...]; SoA planes (x_re, x_im) or one AoS array. Updated in place after
+ * `steps` steps. `algo` = LBG_ALGO_*. `work` (device) must hold
+ * lbg_evolve_workspace(n, batch, algo) bytes (may be NULL when that is 0).
+ * ------------------------------------------------------------------------ */
+size_t lbg_evolve_workspace(size_t n, int64_t batch, int algo);
+int lbg_evolve_shared_p_soa_dev(const double* p, size_t n, double* x_re, double* x_im,
+                                int64_t batch, int64_t steps, int algo, void* work,
+                                void* stream);
+int lbg_evolve_shared_p_aos_dev(const double* p, size_t n, double* x, int64_t batch,
+                                int64_t steps, int algo, void* work, void* stream);
+/* host-buffer variant (end-to-end: H2D, steps, D2H; synchronous). rho0/out are
+ * batch x d x d AoS density matrices; rho0 is validated like propagate.cpp:79. */
+int lbg_evolve_shared_p(const double* p, size_t d, const double* rho0, int64_t batch,
+                        int64_t steps, double* out, int algo);
+
+/* ------------------------------------------------------------------------
+ * Per-trajectory propagators (config 4, "robustness atlas"): for trajectory b
+ *   H_b = h0 + delta[b] * hd + scale[b] * hs,   L_k fixed,
+ *   L_b = build_lindbladian(H_b, L_k),  P_b = exp(L_b dt),
+ *   rho_b <- P_b^steps rho0      (fused on the GPU: assembly K5, expm K4,
+ *                                  P_b-resident stepping K3; P_b never leaves the chip)
+ * Outputs: pops[b*d + i] = Re rho_b[i][i]; ens_sum (d*d AoS) += sum_b rho_b.
+ * Replaces, per trajectory, the make_model + build_lindbladian + expm + step
+ * sequence of lb::grape_chain (propagate.cpp:130-160). Device pointers.
+ * ------------------------------------------------------------------------ */
+size_t lbg_sweep_workspace(size_t d, int64_t batch);
+int lbg_evolve_sweep_dev(size_t d, const double* h0, const double* hd, const double* hs,
+                         size_t n_ops, const double* ops, const double* delta,
+                         const double* scale, double dt, const double* rho0, int64_t batch,
+                         int64_t steps, double* pops, double* ens_sum, void* work,
+                         void* stream);
+
+/* ------------------------------------------------------------------------
+ * Batched invariant check: replaces lb::check_state (validate.hpp:22,
+ * validate.cpp:10-30) over a batch. x: batch x d x d AoS (device).
+ * Writes the max over the batch of |Tr rho - 1| and max|rho_ij - conj rho_ji|,
+ * and the min Re rho_ii, into out3[0..2] (device).
+ * ------------------------------------------------------------------------ */
+int lbg_check_state_batched_dev(const double* x, size_t d, int64_t batch, double* out3,
+                                void* stream);
+
+/* ------------------------------------------------------------------------
+ * Ensemble reduction across ranks (config 4): in-place sum of `count` doubles
+ * over the communicator `comm` (an ncclComm_t). The only collective of the
+ * engine. Returns LBG_ECUDA if NCCL is unavailable.
+ * ------------------------------------------------------------------------ */
+int lbg_allreduce_sum_dev(double* buf, size_t count, void* comm, void* stream);
+/* NCCL communicator plumbing (libnccl.so.2 is dlopen'ed on first use).
+ * Rank 0 calls lbg_nccl_unique_id (128 bytes), the caller broadcasts the bytes
+ * out of band (e.g. torch.distributed), then every rank calls
+ * lbg_nccl_comm_init on its own device. */
+int lbg_nccl_unique_id(void* id128);
+int lbg_nccl_comm_init(void** comm, int nranks, const void* id128, int rank);
+int lbg_nccl_comm_destroy(void* comm);
+
+/* ------------------------------------------------------------------------
+ * Host-side inputs (BASELINE.json configs). The
+ * reference has no multi-transmon models, Ginibre states or sweeps; these are
+ * built with the reference's primitives' arithmetic (kron, i-k-j matmul,
+ * lindblad.cpp:76-80 lowering operator). cfg in 0..4.
+ * ------------------------------------------------------------------------ */
+int lbg_config_dims(int cfg, size_t* d, size_t* n_ops);
+int lbg_config_model(int cfg, double delta, double s, double* h, double* ops);
+/* config 4: H(delta, s) = h0 + delta*hd + s*hs (each 9x9 AoS) */
+int lbg_config_sweep_terms(double* h0, double* hd, double* hs);
+/* counter-based uniform in (0,1) keyed on (seed, cfg, trajectory, k) */
+double lbg_uniform(uint64_t seed, uint32_t cfg, uint64_t traj, uint64_t k);
+/* Ginibre rho0 (G with N(0,1) re/im by explicit Box-Muller, rho = GG^dag/tr)
+ * for global trajectories [first, first+count): out is count x d x d AoS */
+int lbg_ginibre_batch(uint64_t seed, uint32_t cfg, uint64_t first, int64_t count, size_t d,
+                      double* out, int threads);
+int lbg_sweep_params_batch(uint64_t seed, uint64_t first, int64_t count, double* delta,
+                           double* scale);
+
+/* Number of kernels this thread launched since the last reset (evidence for
+ * bench.py's gpu_launches). */
+int64_t lbg_launch_count(void);
+void lbg_reset_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LBG_H */

@@ -1,0 +1,239 @@
+"""ctypes bindings for the CPU checkers (TEST INFRASTRUCTURE ONLY).
+
+- ``Oracle``: oracle/liblbo.so, the plain-C restatement of the reference path
+  (oracle/lbo.c; each function cites the reference file:line it follows).
+- ``Reference``: oracle/_ref/libref.so, the unmodified reference library
+  compiled from /root/reference/proj/src by oracle/Makefile, driven through
+  its own C++ API by oracle/ref_driver.cpp.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+``--impl reference`` legs may import this module, and only as the checker or
+the CPU baseline. The product path (paper_2603_18052_b200) never does.
+Complex matrices are numpy complex128, row-major (interleaved re/im in memory,
+like lb::MatrixAoS).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_dp = C.POINTER(C.c_double)
+
+
+def _ptr(a: np.ndarray):
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(_dp)
+
+
+class _Report(C.Structure):
+    _fields_ = [("trace_error", C.c_double), ("hermiticity_error", C.c_double),
+                ("min_diagonal", C.c_double), ("passed", C.c_int)]
+
+
+class Oracle:
+    """The C restatement (oracle/lbo.c)."""
+
+    def __init__(self, path: str | None = None):
+        path = path or os.path.join(HERE, "liblbo.so")
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} missing: run `make -C oracle`")
+        L = self.lib = C.CDLL(path)
+        sz = C.c_size_t
+        L.lbo_kron.argtypes = [_dp, sz, sz, _dp, sz, sz, _dp]
+        L.lbo_matmul.argtypes = [_dp, sz, sz, _dp, sz, _dp]
+        L.lbo_one_norm.argtypes = [_dp, sz, sz]
+        L.lbo_one_norm.restype = C.c_double
+        L.lbo_build_lindbladian.argtypes = [sz, _dp, sz, _dp, _dp]
+        L.lbo_expm.argtypes = [_dp, sz, C.c_double, _dp]
+        L.lbo_step_soa.argtypes = [_dp] * 6 + [sz]
+        L.lbo_step_aos.argtypes = [_dp, _dp, _dp, sz]
+        L.lbo_evolve.argtypes = [_dp, sz, _dp, sz, _dp]
+        L.lbo_check_state.argtypes = [_dp, sz, C.c_double]
+        L.lbo_check_state.restype = _Report
+        L.lbo_config_dim.argtypes = [C.c_int]
+        L.lbo_config_dim.restype = sz
+        L.lbo_config_nops.argtypes = [C.c_int]
+        L.lbo_config_nops.restype = sz
+        L.lbo_config_model.argtypes = [C.c_int, C.c_double, C.c_double, _dp, _dp]
+        L.lbo_uniform.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64]
+        L.lbo_uniform.restype = C.c_double
+        L.lbo_ginibre_rho.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, sz, _dp]
+        L.lbo_sweep_params.argtypes = [C.c_uint64, C.c_uint64, _dp, _dp]
+
+    def kron(self, a, b):
+        a = np.ascontiguousarray(a, np.complex128)
+        b = np.ascontiguousarray(b, np.complex128)
+        out = np.zeros((a.shape[0] * b.shape[0], a.shape[1] * b.shape[1]), np.complex128)
+        self.lib.lbo_kron(_ptr(a), a.shape[0], a.shape[1], _ptr(b), b.shape[0], b.shape[1], _ptr(out))
+        return out
+
+    def matmul(self, a, b):
+        a = np.ascontiguousarray(a, np.complex128)
+        b = np.ascontiguousarray(b, np.complex128)
+        out = np.zeros((a.shape[0], b.shape[1]), np.complex128)
+        self.lib.lbo_matmul(_ptr(a), a.shape[0], a.shape[1], _ptr(b), b.shape[1], _ptr(out))
+        return out
+
+    def one_norm(self, a):
+        a = np.ascontiguousarray(a, np.complex128)
+        return self.lib.lbo_one_norm(_ptr(a), a.shape[0], a.shape[1])
+
+    def build_lindbladian(self, h, ops):
+        h = np.ascontiguousarray(h, np.complex128)
+        d = h.shape[0]
+        ops = np.ascontiguousarray(np.asarray(ops, np.complex128).reshape(-1, d, d))
+        out = np.zeros((d * d, d * d), np.complex128)
+        rc = self.lib.lbo_build_lindbladian(d, _ptr(h), ops.shape[0], _ptr(ops), _ptr(out))
+        if rc:
+            raise ValueError("lbo_build_lindbladian: invalid argument")
+        return out
+
+    def expm(self, a, dt):
+        a = np.ascontiguousarray(a, np.complex128)
+        out = np.zeros_like(a)
+        rc = self.lib.lbo_expm(_ptr(a), a.shape[0], dt, _ptr(out))
+        if rc == 1:
+            raise ValueError("lbo_expm: invalid argument")
+        if rc == 2:
+            raise RuntimeError("lbo_expm: runtime error")
+        return out
+
+    def step_soa(self, p, v):
+        p = np.asarray(p, np.complex128)
+        v = np.asarray(v, np.complex128)
+        n = v.shape[0]
+        pr, pi = np.ascontiguousarray(p.real), np.ascontiguousarray(p.imag)
+        vr, vi = np.ascontiguousarray(v.real), np.ascontiguousarray(v.imag)
+        orr, oi = np.zeros(n), np.zeros(n)
+        self.lib.lbo_step_soa(_ptr(pr), _ptr(pi), _ptr(vr), _ptr(vi), _ptr(orr), _ptr(oi), n)
+        return orr + 1j * oi
+
+    def evolve(self, p, rho0, steps):
+        p = np.ascontiguousarray(p, np.complex128)
+        rho0 = np.ascontiguousarray(rho0, np.complex128)
+        out = np.zeros_like(rho0)
+        rc = self.lib.lbo_evolve(_ptr(p), rho0.shape[0], _ptr(rho0), steps, _ptr(out))
+        if rc:
+            raise ValueError("lbo_evolve: initial state fails physical-state checks")
+        return out
+
+    def check_state(self, rho, tol=1e-8):
+        rho = np.ascontiguousarray(rho, np.complex128)
+        r = self.lib.lbo_check_state(_ptr(rho), rho.shape[0], tol)
+        return dict(trace_error=r.trace_error, hermiticity_error=r.hermiticity_error,
+                    min_diagonal=r.min_diagonal, passed=bool(r.passed))
+
+    def config_model(self, cfg, delta=0.0, s=1.0):
+        d = self.lib.lbo_config_dim(cfg)
+        k = self.lib.lbo_config_nops(cfg)
+        h = np.zeros((d, d), np.complex128)
+        ops = np.zeros((k, d, d), np.complex128)
+        self.lib.lbo_config_model(cfg, delta, s, _ptr(h), _ptr(ops))
+        return h, ops
+
+    def uniform(self, seed, cfg, traj, k):
+        return self.lib.lbo_uniform(seed, cfg, traj, k)
+
+    def ginibre_rho(self, seed, cfg, traj, d):
+        out = np.zeros((d, d), np.complex128)
+        self.lib.lbo_ginibre_rho(seed, cfg, traj, d, _ptr(out))
+        return out
+
+    def sweep_params(self, seed, traj):
+        a, b = C.c_double(), C.c_double()
+        self.lib.lbo_sweep_params(seed, traj, C.byref(a), C.byref(b))
+        return a.value, b.value
+
+
+class Reference:
+    """The reference library itself (oracle/_ref/libref.so)."""
+
+    def __init__(self, path: str | None = None):
+        path = path or os.path.join(HERE, "_ref", "libref.so")
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} missing: run `make -C oracle` where /root/reference exists")
+        L = self.lib = C.CDLL(path)
+        sz = C.c_size_t
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_config_model.argtypes = [C.c_int, C.c_double, C.c_double, _dp, _dp]
+        L.ref_build_lindbladian.argtypes = [sz, _dp, sz, _dp, _dp]
+        L.ref_expm.argtypes = [_dp, sz, C.c_double, _dp]
+        L.ref_config_propagator.argtypes = [C.c_int, C.c_double, C.c_double, _dp]
+        L.ref_step_soa.argtypes = [C.c_char_p] + [_dp] * 6 + [sz]
+        L.ref_evolve_batch.argtypes = [_dp, sz, _dp, C.c_int64, sz, _dp, C.c_int, _dp]
+        L.ref_sweep_batch.argtypes = [_dp, _dp, C.c_int64, sz, _dp, _dp, C.c_int, _dp]
+        L.ref_check_state.argtypes = [_dp, sz, C.c_double, _dp, _dp, _dp]
+
+    def _rc(self, rc, what):
+        if rc == 1:
+            raise ValueError(f"{what}: {self.lib.ref_last_error().decode()}")
+        if rc:
+            raise RuntimeError(f"{what}: {self.lib.ref_last_error().decode()}")
+
+    def hardware_threads(self):
+        return self.lib.ref_hardware_threads()
+
+    def config_model(self, cfg, delta=0.0, s=1.0):
+        d = {0: 3, 1: 3, 2: 9, 3: 27, 4: 9}[cfg]
+        k = {0: 2, 1: 2, 2: 4, 3: 6, 4: 4}[cfg]
+        h = np.zeros((d, d), np.complex128)
+        ops = np.zeros((k, d, d), np.complex128)
+        self._rc(self.lib.ref_config_model(cfg, delta, s, _ptr(h), _ptr(ops)), "config_model")
+        return h, ops
+
+    def build_lindbladian(self, h, ops):
+        h = np.ascontiguousarray(h, np.complex128)
+        d = h.shape[0]
+        ops = np.ascontiguousarray(np.asarray(ops, np.complex128).reshape(-1, d, d))
+        out = np.zeros((d * d, d * d), np.complex128)
+        self._rc(self.lib.ref_build_lindbladian(d, _ptr(h), ops.shape[0], _ptr(ops), _ptr(out)),
+                 "build_lindbladian")
+        return out
+
+    def expm(self, a, dt):
+        a = np.ascontiguousarray(a, np.complex128)
+        out = np.zeros_like(a)
+        self._rc(self.lib.ref_expm(_ptr(a), a.shape[0], dt, _ptr(out)), "expm")
+        return out
+
+    def config_propagator(self, cfg, delta=0.0, s=1.0):
+        d = {0: 3, 1: 3, 2: 9, 3: 27, 4: 9}[cfg]
+        out = np.zeros((d * d, d * d), np.complex128)
+        self._rc(self.lib.ref_config_propagator(cfg, delta, s, _ptr(out)), "config_propagator")
+        return out
+
+    def step_soa(self, p, v, profile="native-fast"):
+        p = np.asarray(p, np.complex128)
+        v = np.asarray(v, np.complex128)
+        n = v.shape[0]
+        pr, pi = np.ascontiguousarray(p.real), np.ascontiguousarray(p.imag)
+        vr, vi = np.ascontiguousarray(v.real), np.ascontiguousarray(v.imag)
+        orr, oi = np.zeros(n), np.zeros(n)
+        self._rc(self.lib.ref_step_soa(profile.encode(), _ptr(pr), _ptr(pi), _ptr(vr), _ptr(vi),
+                                       _ptr(orr), _ptr(oi), n), "step_soa")
+        return orr + 1j * oi
+
+    def evolve_batch(self, p, rho0, steps, threads=1):
+        """rho0: (B, d, d) complex. Returns (out, seconds)."""
+        p = np.ascontiguousarray(p, np.complex128)
+        rho0 = np.ascontiguousarray(rho0, np.complex128)
+        out = np.zeros_like(rho0)
+        secs = C.c_double()
+        self._rc(self.lib.ref_evolve_batch(_ptr(p), rho0.shape[1], _ptr(rho0), rho0.shape[0], steps,
+                                           _ptr(out), threads, C.byref(secs)), "evolve_batch")
+        return out, secs.value
+
+    def sweep_batch(self, deltas, scales, steps=500, threads=1):
+        """Config 4 through the reference. Returns (pops (B,9), ens_sum (9,9), seconds)."""
+        deltas = np.ascontiguousarray(deltas, np.float64)
+        scales = np.ascontiguousarray(scales, np.float64)
+        B = deltas.shape[0]
+        pops = np.zeros((B, 9))
+        ens = np.zeros((9, 9), np.complex128)
+        secs = C.c_double()
+        self._rc(self.lib.ref_sweep_batch(_ptr(deltas), _ptr(scales), B, steps, _ptr(pops), _ptr(ens),
+                                          threads, C.byref(secs)), "sweep_batch")
+        return pops, ens, secs.value

@@ -1,0 +1,276 @@
+"""B200-native Lindblad propagation engine — Python mirror of the C-ABI.
+
+The product is ``liblbg.so`` (hand-written sm_100a CUDA kernels + the C-ABI in
+``include/lbg.h``). This module binds it with ctypes and mirrors the
+reference's operator interface for the hot path (lindbench, /root/reference):
+
+    build_lindbladian(h, ops)        lb::build_lindbladian  (lindblad.cpp:37-59)   -> GPU K5
+    expm(a, dt)                      lb::expm               (expm.cpp:109-134)      -> GPU K4
+    step_soa / step_aos              lb::StepSoAFn/StepAoSFn (kernels.hpp:22-24)    -> GPU shim
+    evolve(p, rho0, n_steps)         lb::evolve             (propagate.cpp:75-109)  -> GPU K1/K2
+    evolve_batch(p, rho0s, n_steps)  batched evolve over trajectories               -> GPU K1/K2
+    evolve_sweep_dev(...)            per-trajectory build+expm+steps (config 4)     -> GPU K3-K5
+    check_state(rho)                 lb::check_state        (validate.cpp:10-30)
+
+Errors map like the reference: ValueError <- std::invalid_argument,
+RuntimeError <- std::runtime_error. There is no CPU fallback: if the
+extension is missing or no GPU is present, calls raise.
+
+torch is used only as device-memory/stream plumbing for the ``*_dev`` entry
+points (tensors' data pointers are passed through the C-ABI).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+__all__ = [
+    "lib", "LbgError", "ALGO", "config_dims", "config_model", "config_sweep_terms",
+    "ginibre_batch", "sweep_params", "build_lindbladian", "expm", "step_soa", "step_aos",
+    "evolve", "evolve_batch", "evolve_batch_dev", "evolve_workspace", "evolve_sweep_dev",
+    "sweep_workspace", "check_state", "check_state_batched_dev", "launch_count",
+    "reset_launch_count", "SEED",
+]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liblbg.so")
+SEED = 42  # lb::kDefaultSeed (proj/include/lb/random.hpp:10)
+
+ALGO = {"auto": 0, "chain": 1, "dfma9": 2, "smem": 3, "tiled": 4}
+
+_dp = C.POINTER(C.c_double)
+_sz = C.c_size_t
+_lib = None
+
+
+class LbgError(RuntimeError):
+    """CUDA / launch failure inside liblbg (LBG_ECUDA)."""
+
+
+def lib() -> C.CDLL:
+    """Load liblbg.so (built in-tree by paper_2603_18052_b200.build). Fails loudly."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2603_18052_b200.build`")
+    L = C.CDLL(LIB_PATH)
+    vp = C.c_void_p
+    L.lbg_last_error.restype = C.c_char_p
+    L.lbg_version.restype = C.c_char_p
+    L.lbg_launch_count.restype = C.c_int64
+    L.lbg_step_soa.argtypes = [_dp] * 6 + [_sz]
+    L.lbg_step_soa.restype = None
+    L.lbg_step_aos.argtypes = [_dp, _dp, _dp, _sz]
+    L.lbg_step_aos.restype = None
+    L.lbg_build_lindbladian.argtypes = [_sz, _dp, _sz, _dp, _dp]
+    L.lbg_build_lindbladian_dev.argtypes = [_sz, vp, _sz, vp, vp, vp]
+    L.lbg_expm.argtypes = [_dp, _sz, C.c_double, _dp]
+    L.lbg_expm_dev.argtypes = [vp, _sz, C.c_double, vp, vp, vp]
+    L.lbg_expm_workspace.argtypes = [_sz]
+    L.lbg_expm_workspace.restype = _sz
+    L.lbg_evolve_workspace.argtypes = [_sz, C.c_int64, C.c_int]
+    L.lbg_evolve_workspace.restype = _sz
+    L.lbg_evolve_shared_p_soa_dev.argtypes = [vp, _sz, vp, vp, C.c_int64, C.c_int64, C.c_int, vp, vp]
+    L.lbg_evolve_shared_p_aos_dev.argtypes = [vp, _sz, vp, C.c_int64, C.c_int64, C.c_int, vp, vp]
+    L.lbg_evolve_shared_p.argtypes = [_dp, _sz, _dp, C.c_int64, C.c_int64, _dp, C.c_int]
+    L.lbg_sweep_workspace.argtypes = [_sz, C.c_int64]
+    L.lbg_sweep_workspace.restype = _sz
+    L.lbg_evolve_sweep_dev.argtypes = [_sz, vp, vp, vp, _sz, vp, vp, vp, C.c_double, vp, C.c_int64,
+                                       C.c_int64, vp, vp, vp, vp]
+    L.lbg_check_state_batched_dev.argtypes = [vp, _sz, C.c_int64, vp, vp]
+    L.lbg_allreduce_sum_dev.argtypes = [vp, _sz, vp, vp]
+    L.lbg_nccl_unique_id.argtypes = [vp]
+    L.lbg_nccl_comm_init.argtypes = [C.POINTER(vp), C.c_int, vp, C.c_int]
+    L.lbg_nccl_comm_destroy.argtypes = [vp]
+    L.lbg_config_dims.argtypes = [C.c_int, C.POINTER(_sz), C.POINTER(_sz)]
+    L.lbg_config_model.argtypes = [C.c_int, C.c_double, C.c_double, _dp, _dp]
+    L.lbg_config_sweep_terms.argtypes = [_dp, _dp, _dp]
+    L.lbg_uniform.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64]
+    L.lbg_uniform.restype = C.c_double
+    L.lbg_ginibre_batch.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_int64, _sz, _dp, C.c_int]
+    L.lbg_sweep_params_batch.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, _dp, _dp]
+    _lib = L
+    return L
+
+
+def _check(rc: int, what: str) -> None:
+    if rc == 0:
+        return
+    msg = f"{what}: {lib().lbg_last_error().decode()}"
+    if rc == 1:
+        raise ValueError(msg)
+    if rc == 2:
+        raise RuntimeError(msg)
+    raise LbgError(msg)
+
+
+def _p(a: np.ndarray):
+    assert a.flags["C_CONTIGUOUS"], "arrays must be C-contiguous"
+    return a.ctypes.data_as(_dp)
+
+
+def _c128(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.complex128)
+
+
+def _tp(t):
+    """device pointer of a torch tensor (or None)."""
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _sp(stream):
+    if stream is None:
+        return None
+    return C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def launch_count() -> int:
+    return int(lib().lbg_launch_count())
+
+
+def reset_launch_count() -> None:
+    lib().lbg_reset_launch_count()
+
+
+# ---------------------------------------------------------------- configs ---
+def config_dims(cfg: int) -> tuple[int, int]:
+    d, k = _sz(), _sz()
+    _check(lib().lbg_config_dims(cfg, C.byref(d), C.byref(k)), "config_dims")
+    return d.value, k.value
+
+
+def config_model(cfg: int, delta: float = 0.0, s: float = 1.0):
+    """(H, L_k) of BASELINE.json config `cfg`."""
+    d, k = config_dims(cfg)
+    h = np.zeros((d, d), np.complex128)
+    ops = np.zeros((k, d, d), np.complex128)
+    _check(lib().lbg_config_model(cfg, delta, s, _p(h), _p(ops)), "config_model")
+    return h, ops
+
+
+def config_sweep_terms():
+    """Config 4: H(delta, s) = h0 + delta*hd + s*hs."""
+    h0, hd, hs = (np.zeros((9, 9), np.complex128) for _ in range(3))
+    _check(lib().lbg_config_sweep_terms(_p(h0), _p(hd), _p(hs)), "config_sweep_terms")
+    return h0, hd, hs
+
+
+def ginibre_batch(cfg: int, first: int, count: int, d: int, seed: int = SEED, threads: int | None = None):
+    out = np.empty((count, d, d), np.complex128)
+    threads = threads or os.cpu_count() or 1
+    _check(lib().lbg_ginibre_batch(seed, cfg, first, count, d, _p(out), threads), "ginibre_batch")
+    return out
+
+
+def sweep_params(first: int, count: int, seed: int = SEED):
+    delta, scale = np.empty(count), np.empty(count)
+    _check(lib().lbg_sweep_params_batch(seed, first, count, _p(delta), _p(scale)), "sweep_params")
+    return delta, scale
+
+
+# ------------------------------------------------------ host (synchronous) ---
+def build_lindbladian(h, ops):
+    """Vectorised generator L (d^2 x d^2), assembled on the GPU (K5)."""
+    h = _c128(h)
+    d = h.shape[0]
+    if h.ndim != 2 or h.shape[1] != d:
+        raise ValueError("make_model: Hamiltonian must be square")
+    ops = _c128(np.asarray(ops, np.complex128).reshape(-1, d, d)) if len(ops) else np.zeros((0, d, d), np.complex128)
+    out = np.zeros((d * d, d * d), np.complex128)
+    _check(lib().lbg_build_lindbladian(d, _p(h), ops.shape[0], _p(ops), _p(out)), "build_lindbladian")
+    return out
+
+
+def expm(a, dt: float):
+    """P = exp(a*dt) on the GPU (K4: Taylor-16 / Paterson-Stockmeyer on DMMA)."""
+    a = _c128(a)
+    if a.ndim != 2 or a.shape[0] != a.shape[1]:
+        raise ValueError("expm: matrix must be square")
+    out = np.zeros_like(a)
+    _check(lib().lbg_expm(_p(a), a.shape[0], float(dt), _p(out)), "expm")
+    return out
+
+
+def step_soa(p, v):
+    """One raw step through the lb::StepSoAFn-compatible shim."""
+    p, v = _c128(p), _c128(v)
+    n = v.shape[0]
+    pr, pi = np.ascontiguousarray(p.real), np.ascontiguousarray(p.imag)
+    vr, vi = np.ascontiguousarray(v.real), np.ascontiguousarray(v.imag)
+    orr, oi = np.zeros(n), np.zeros(n)
+    lib().lbg_step_soa(_p(pr), _p(pi), _p(vr), _p(vi), _p(orr), _p(oi), n)
+    return orr + 1j * oi
+
+
+def step_aos(p, v):
+    p, v = _c128(p), _c128(v)
+    out = np.zeros_like(v)
+    lib().lbg_step_aos(_p(p), _p(v), _p(out), v.shape[0])
+    return out
+
+
+def evolve_batch(p, rho0, n_steps: int, algo: str = "auto"):
+    """rho0: (B, d, d) complex -> final states (B, d, d). Host buffers, end-to-end."""
+    p, rho0 = _c128(p), _c128(rho0)
+    if rho0.ndim != 3 or rho0.shape[1] != rho0.shape[2]:
+        raise ValueError("evolve: states must be (B, d, d)")
+    B, d = rho0.shape[0], rho0.shape[1]
+    if p.shape != (d * d, d * d):
+        raise ValueError("evolve: state dimension does not match propagator")
+    out = np.empty_like(rho0)
+    _check(lib().lbg_evolve_shared_p(_p(p), d, _p(rho0), B, int(n_steps), _p(out), ALGO[algo]), "evolve")
+    return out
+
+
+def evolve(p, rho0, n_steps: int, algo: str = "auto"):
+    """lb::evolve for one trajectory (propagate.cpp:75-109), on the GPU."""
+    rho0 = _c128(rho0)
+    if rho0.ndim != 2 or rho0.shape[0] != rho0.shape[1]:
+        raise ValueError("evolve: state must be square")
+    return evolve_batch(p, rho0[None], n_steps, algo)[0]
+
+
+def check_state(rho, tol: float = 1e-8) -> dict:
+    """validate.cpp:10-30 on the host (a d x d density matrix)."""
+    rho = _c128(rho)
+    if rho.ndim != 2 or rho.shape[0] != rho.shape[1]:
+        raise ValueError("check_state: state must be square")
+    tr = np.trace(rho)
+    herm = float(np.abs(rho - rho.conj().T).max()) if rho.size else 0.0
+    mind = float(np.real(np.diag(rho)).min()) if rho.size else 0.0
+    te = float(abs(tr - 1.0))
+    return dict(trace_error=te, hermiticity_error=herm, min_diagonal=mind,
+                passed=te <= tol and herm <= tol and mind >= -tol)
+
+
+# -------------------------------------------------- device (stream-ordered) ---
+def evolve_workspace(n: int, batch: int, algo: str = "auto") -> int:
+    return int(lib().lbg_evolve_workspace(n, batch, ALGO[algo]))
+
+
+def evolve_batch_dev(p, x, n_steps: int, algo: str = "auto", work=None, stream=None):
+    """In-place on device tensors: p (n, n) complex128, x (B, n) complex128."""
+    n = p.shape[0]
+    B = x.shape[0]
+    _check(lib().lbg_evolve_shared_p_aos_dev(_tp(p), n, _tp(x), B, int(n_steps), ALGO[algo], _tp(work),
+                                             _sp(stream)), "evolve_shared_p_aos_dev")
+
+
+def sweep_workspace(d: int, batch: int) -> int:
+    return int(lib().lbg_sweep_workspace(d, batch))
+
+
+def evolve_sweep_dev(h0, hd, hs, ops, delta, scale, dt, rho0, n_steps, pops, ens_sum, work, stream=None):
+    """Config-4 sweep on device tensors (see include/lbg.h lbg_evolve_sweep_dev)."""
+    d = h0.shape[0]
+    _check(lib().lbg_evolve_sweep_dev(d, _tp(h0), _tp(hd), _tp(hs), ops.shape[0], _tp(ops), _tp(delta),
+                                      _tp(scale), float(dt), _tp(rho0), delta.shape[0], int(n_steps),
+                                      _tp(pops), _tp(ens_sum), _tp(work), _sp(stream)), "evolve_sweep_dev")
+
+
+def check_state_batched_dev(x, d: int, out3, stream=None):
+    _check(lib().lbg_check_state_batched_dev(_tp(x), d, x.shape[0], _tp(out3), _sp(stream)),
+           "check_state_batched_dev")

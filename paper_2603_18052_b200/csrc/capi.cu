@@ -1,0 +1,337 @@
+// capi.cu — the extern "C" boundary (include/lbg.h). Validates arguments
+// exactly where the reference throws (propagate.cpp:14-28,77-80; lindblad.cpp:25-33;
+// expm.cpp:110-121), picks the kernel regime, and maps C++ exceptions to
+// LBG_* status codes (no exception crosses the ABI).
+#include <dlfcn.h>
+
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/lbg.h"
+#include "internal.hpp"
+
+namespace lbg {
+
+namespace {
+thread_local std::string g_err;
+thread_local int64_t g_launches = 0;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return LBG_OK;
+  } catch (const lbg::invalid_argument& e) {
+    g_err = e.what();
+    return LBG_EINVAL;
+  } catch (const lbg::cuda_error& e) {
+    g_err = e.what();
+    return LBG_ECUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return LBG_ERUNTIME;
+  }
+}
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+// RAII device buffer for the host-pointer entry points
+struct DevBuf {
+  void* p = nullptr;
+  explicit DevBuf(size_t bytes) {
+    if (bytes) check_cuda(cudaMalloc(&p, bytes), "cudaMalloc");
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+// reference is_hermitian (lindblad.cpp:13-20): relative 1e-12 on max |h|
+bool is_hermitian(const double* h, size_t d) {
+  double worst = 0.0, scale = 0.0;
+  for (size_t i = 0; i < d; ++i)
+    for (size_t j = 0; j < d; ++j) {
+      const std::complex<double> a(h[2 * (i * d + j)], h[2 * (i * d + j) + 1]);
+      const std::complex<double> b(h[2 * (j * d + i)], h[2 * (j * d + i) + 1]);
+      worst = std::max(worst, std::abs(a - std::conj(b)));
+      scale = std::max(scale, std::abs(a));
+    }
+  return scale == 0.0 ? worst == 0.0 : worst <= 1e-12 * scale;
+}
+
+int choose_algo(size_t n, int64_t batch, int algo) {
+  if (algo != LBG_ALGO_AUTO) return algo;
+  if (chain_supported(n) && batch <= 512) return LBG_ALGO_CHAIN;
+  if (n == 9) return LBG_ALGO_DFMA9;
+  if (smem_supported(n)) return LBG_ALGO_SMEM;
+  return LBG_ALGO_TILED;
+}
+
+void evolve_dev(const double* p, size_t n, double* x_re, double* x_im, double* x_aos, int64_t batch,
+                int64_t steps, int algo, void* work, cudaStream_t s, Layout layout) {
+  if (n == 0) throw invalid_argument("evolve: propagator must be non-empty");
+  if (batch < 0 || steps < 0) throw invalid_argument("evolve: negative batch or steps");
+  if (!p) throw invalid_argument("evolve: null propagator");
+  if (batch == 0 || steps == 0) return;
+  if (layout == Layout::soa && (!x_re || !x_im)) throw invalid_argument("evolve: null state");
+  if (layout == Layout::aos && !x_aos) throw invalid_argument("evolve: null state");
+  switch (choose_algo(n, batch, algo)) {
+    case LBG_ALGO_CHAIN:
+      if (!chain_supported(n)) throw invalid_argument("evolve: chain kernel needs n <= 16");
+      return launch_chain(p, n, x_re, x_im, x_aos, batch, steps, layout, s);
+    case LBG_ALGO_DFMA9:
+      if (n != 9) throw invalid_argument("evolve: dfma9 kernel needs n == 9");
+      return launch_dfma9(nullptr, p, x_re, x_im, x_aos, batch, steps, layout, s);
+    case LBG_ALGO_SMEM:
+      if (!smem_supported(n)) throw invalid_argument("evolve: smem kernel needs n <= 84");
+      return launch_smem(p, n, x_re, x_im, x_aos, batch, steps, layout, s);
+    case LBG_ALGO_TILED:
+      return launch_tiled_evolve(p, n, x_re, x_im, x_aos, batch, steps, layout, work, s);
+    default:
+      throw invalid_argument("evolve: unknown algo");
+  }
+}
+
+// ---- NCCL through dlopen (no link-time dependency) ----
+struct Nccl {
+  void* h = nullptr;
+  int (*get_unique_id)(void*) = nullptr;
+  int (*comm_init_rank)(void**, int, const void*, int) = nullptr;  // id passed by value: 128 B
+  int (*comm_destroy)(void*) = nullptr;
+  int (*all_reduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  const char* (*error_string)(int) = nullptr;
+};
+typedef struct { char internal[128]; } NcclUniqueId;
+typedef int (*CommInitRankFn)(void**, int, NcclUniqueId, int);
+
+Nccl& nccl() {
+  static Nccl n = [] {
+    Nccl x;
+    x.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!x.h) return x;
+    x.get_unique_id = reinterpret_cast<int (*)(void*)>(dlsym(x.h, "ncclGetUniqueId"));
+    x.comm_destroy = reinterpret_cast<int (*)(void*)>(dlsym(x.h, "ncclCommDestroy"));
+    x.all_reduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t)>(
+        dlsym(x.h, "ncclAllReduce"));
+    x.error_string = reinterpret_cast<const char* (*)(int)>(dlsym(x.h, "ncclGetErrorString"));
+    return x;
+  }();
+  if (!n.h) throw cuda_error("libnccl.so.2 not loadable");
+  return n;
+}
+void nccl_check(int rc, const char* what) {
+  if (rc != 0)
+    throw cuda_error(std::string(what) + ": " + (nccl().error_string ? nccl().error_string(rc) : "nccl error"));
+}
+
+}  // namespace
+
+void note_launch(int n) { g_launches += n; }
+
+}  // namespace lbg
+
+using namespace lbg;
+
+extern "C" {
+
+const char* lbg_last_error(void) { return g_err.c_str(); }
+const char* lbg_version(void) { return "lbg 0.1 (sm_100a)"; }
+int64_t lbg_launch_count(void) { return g_launches; }
+void lbg_reset_launch_count(void) { g_launches = 0; }
+
+// ---- raw step shims (kernels.hpp:22-24) ----
+void lbg_step_soa(const double* p_re, const double* p_im, const double* v_re, const double* v_im,
+                  double* out_re, double* out_im, size_t n) {
+  const int rc = guarded([&] {
+    std::vector<double> p(2 * n * n), v(2 * n), o(2 * n);
+    for (size_t e = 0; e < n * n; ++e) {
+      p[2 * e] = p_re[e];
+      p[2 * e + 1] = p_im[e];
+    }
+    for (size_t e = 0; e < n; ++e) {
+      v[2 * e] = v_re[e];
+      v[2 * e + 1] = v_im[e];
+    }
+    DevBuf dp(p.size() * 8), dv(v.size() * 8), dout(o.size() * 8);
+    check_cuda(cudaMemcpy(dp.p, p.data(), p.size() * 8, cudaMemcpyHostToDevice), "H2D");
+    check_cuda(cudaMemcpy(dv.p, v.data(), v.size() * 8, cudaMemcpyHostToDevice), "H2D");
+    launch_step_once(dp.as<double>(), dv.as<double>(), dout.as<double>(), n, nullptr);
+    check_cuda(cudaMemcpy(o.data(), dout.p, o.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+    for (size_t e = 0; e < n; ++e) {
+      out_re[e] = o[2 * e];
+      out_im[e] = o[2 * e + 1];
+    }
+  });
+  if (rc != LBG_OK) {
+    std::fprintf(stderr, "lbg_step_soa: %s\n", g_err.c_str());
+    std::abort();
+  }
+}
+
+void lbg_step_aos(const double* p, const double* v, double* out, size_t n) {
+  const int rc = guarded([&] {
+    DevBuf dp(2 * n * n * 8), dv(2 * n * 8), dout(2 * n * 8);
+    check_cuda(cudaMemcpy(dp.p, p, 2 * n * n * 8, cudaMemcpyHostToDevice), "H2D");
+    check_cuda(cudaMemcpy(dv.p, v, 2 * n * 8, cudaMemcpyHostToDevice), "H2D");
+    launch_step_once(dp.as<double>(), dv.as<double>(), dout.as<double>(), n, nullptr);
+    check_cuda(cudaMemcpy(out, dout.p, 2 * n * 8, cudaMemcpyDeviceToHost), "D2H");
+  });
+  if (rc != LBG_OK) {
+    std::fprintf(stderr, "lbg_step_aos: %s\n", g_err.c_str());
+    std::abort();
+  }
+}
+
+// ---- model assembly / propagator ----
+int lbg_build_lindbladian_dev(size_t d, const double* h, size_t n_ops, const double* ops,
+                              double* out, void* stream) {
+  return guarded([&] {
+    if (d == 0) throw invalid_argument("build_lindbladian: dimension must be positive");
+    if (!h || !out || (n_ops && !ops)) throw invalid_argument("build_lindbladian: null pointer");
+    launch_build_lindbladian(d, h, n_ops, ops, out, as_stream(stream));
+  });
+}
+
+int lbg_build_lindbladian(size_t d, const double* h, size_t n_ops, const double* ops, double* out) {
+  return guarded([&] {
+    if (d == 0) throw invalid_argument("make_model: dimension must be positive");
+    if (!is_hermitian(h, d)) throw invalid_argument("make_model: Hamiltonian is not Hermitian within 1e-12");
+    const size_t n = d * d;
+    DevBuf dh(2 * d * d * 8), dops(2 * n_ops * d * d * 8), dout(2 * n * n * 8);
+    check_cuda(cudaMemcpy(dh.p, h, 2 * d * d * 8, cudaMemcpyHostToDevice), "H2D");
+    if (n_ops) check_cuda(cudaMemcpy(dops.p, ops, 2 * n_ops * d * d * 8, cudaMemcpyHostToDevice), "H2D");
+    launch_build_lindbladian(d, dh.as<double>(), n_ops, dops.as<double>(), dout.as<double>(), nullptr);
+    check_cuda(cudaMemcpy(out, dout.p, 2 * n * n * 8, cudaMemcpyDeviceToHost), "D2H");
+  });
+}
+
+size_t lbg_expm_workspace(size_t n) { return 6 * n * n * 16; }
+
+int lbg_expm_dev(const double* a, size_t n, double dt, double* out, double* work, void* stream) {
+  return guarded([&] {
+    if (n == 0) throw invalid_argument("expm: matrix must be square and non-empty");
+    if (!std::isfinite(dt)) throw invalid_argument("expm: dt must be finite");
+    if (!a || !out || !work) throw invalid_argument("expm: null pointer");
+    expm_dev(a, n, dt, out, work, as_stream(stream));
+  });
+}
+
+int lbg_expm(const double* a, size_t n, double dt, double* out) {
+  return guarded([&] {
+    if (n == 0) throw invalid_argument("expm: matrix must be square and non-empty");
+    if (!std::isfinite(dt)) throw invalid_argument("expm: dt must be finite");
+    for (size_t e = 0; e < 2 * n * n; ++e)
+      if (!std::isfinite(a[e])) throw invalid_argument("expm: non-finite entries in input");
+    DevBuf da(2 * n * n * 8), dout(2 * n * n * 8), dw(lbg_expm_workspace(n));
+    check_cuda(cudaMemcpy(da.p, a, 2 * n * n * 8, cudaMemcpyHostToDevice), "H2D");
+    expm_dev(da.as<double>(), n, dt, dout.as<double>(), dw.as<double>(), nullptr);
+    check_cuda(cudaMemcpy(out, dout.p, 2 * n * n * 8, cudaMemcpyDeviceToHost), "D2H");
+  });
+}
+
+// ---- batched shared-P propagation ----
+size_t lbg_evolve_workspace(size_t n, int64_t batch, int algo) {
+  if (n == 0 || batch <= 0) return 0;
+  return choose_algo(n, batch, algo) == LBG_ALGO_TILED ? tiled_workspace(n, batch) : 0;
+}
+
+int lbg_evolve_shared_p_soa_dev(const double* p, size_t n, double* x_re, double* x_im,
+                                int64_t batch, int64_t steps, int algo, void* work, void* stream) {
+  return guarded([&] {
+    evolve_dev(p, n, x_re, x_im, nullptr, batch, steps, algo, work, as_stream(stream), Layout::soa);
+  });
+}
+
+int lbg_evolve_shared_p_aos_dev(const double* p, size_t n, double* x, int64_t batch, int64_t steps,
+                                int algo, void* work, void* stream) {
+  return guarded([&] {
+    evolve_dev(p, n, nullptr, nullptr, x, batch, steps, algo, work, as_stream(stream), Layout::aos);
+  });
+}
+
+int lbg_evolve_shared_p(const double* p, size_t d, const double* rho0, int64_t batch, int64_t steps,
+                        double* out, int algo) {
+  return guarded([&] {
+    if (d == 0) throw invalid_argument("evolve: state dimension must be positive");
+    if (batch < 0 || steps < 0) throw invalid_argument("evolve: negative batch or steps");
+    const size_t n = d * d;
+    const size_t xbytes = size_t(batch) * n * 16;
+    DevBuf dp(n * n * 16), dx(xbytes), dchk(3 * 8), dw(lbg_evolve_workspace(n, batch, algo));
+    check_cuda(cudaMemcpy(dp.p, p, n * n * 16, cudaMemcpyHostToDevice), "H2D P");
+    check_cuda(cudaMemcpy(dx.p, rho0, xbytes, cudaMemcpyHostToDevice), "H2D rho0");
+    // propagate.cpp:79 — every rho0 must pass check_state at 1e-8
+    launch_check_state(dx.as<double>(), d, batch, dchk.as<double>(), nullptr);
+    double chk[3];
+    check_cuda(cudaMemcpy(chk, dchk.p, sizeof chk, cudaMemcpyDeviceToHost), "D2H check");
+    if (batch > 0 && !(chk[0] <= 1e-8 && chk[1] <= 1e-8 && chk[2] >= -1e-8))
+      throw invalid_argument("evolve: initial state fails physical-state checks");
+    evolve_dev(dp.as<double>(), n, nullptr, nullptr, dx.as<double>(), batch, steps, algo, dw.p, nullptr,
+               Layout::aos);
+    check_cuda(cudaMemcpy(out, dx.p, xbytes, cudaMemcpyDeviceToHost), "D2H rho");
+  });
+}
+
+// ---- per-trajectory sweep (config 4) ----
+size_t lbg_sweep_workspace(size_t d, int64_t batch) { return sweep_workspace(d, batch); }
+
+int lbg_evolve_sweep_dev(size_t d, const double* h0, const double* hd, const double* hs, size_t n_ops,
+                         const double* ops, const double* delta, const double* scale, double dt,
+                         const double* rho0, int64_t batch, int64_t steps, double* pops,
+                         double* ens_sum, void* work, void* stream) {
+  return guarded([&] {
+    if (d == 0) throw invalid_argument("sweep: dimension must be positive");
+    if (batch < 0 || steps < 0) throw invalid_argument("sweep: negative batch or steps");
+    if (!std::isfinite(dt)) throw invalid_argument("sweep: dt must be finite");
+    if (!h0 || !hd || !hs || !delta || !scale || !rho0 || !pops || !ens_sum || (n_ops && !ops))
+      throw invalid_argument("sweep: null pointer");
+    launch_sweep(d, h0, hd, hs, n_ops, ops, delta, scale, dt, rho0, batch, steps, pops, ens_sum, work,
+                 as_stream(stream));
+  });
+}
+
+int lbg_check_state_batched_dev(const double* x, size_t d, int64_t batch, double* out3, void* stream) {
+  return guarded([&] {
+    if (d == 0 || batch < 0 || !out3) throw invalid_argument("check_state: bad arguments");
+    launch_check_state(x, d, batch, out3, as_stream(stream));
+  });
+}
+
+// ---- NCCL ----
+int lbg_nccl_unique_id(void* id128) {
+  return guarded([&] { nccl_check(nccl().get_unique_id(id128), "ncclGetUniqueId"); });
+}
+
+int lbg_nccl_comm_init(void** comm, int nranks, const void* id128, int rank) {
+  return guarded([&] {
+    auto fn = reinterpret_cast<CommInitRankFn>(dlsym(nccl().h, "ncclCommInitRank"));
+    if (!fn) throw cuda_error("ncclCommInitRank missing");
+    NcclUniqueId id;
+    std::memcpy(id.internal, id128, 128);
+    nccl_check(fn(comm, nranks, id, rank), "ncclCommInitRank");
+  });
+}
+
+int lbg_nccl_comm_destroy(void* comm) {
+  return guarded([&] { nccl_check(nccl().comm_destroy(comm), "ncclCommDestroy"); });
+}
+
+int lbg_allreduce_sum_dev(double* buf, size_t count, void* comm, void* stream) {
+  return guarded([&] {
+    if (!comm) throw invalid_argument("allreduce: null communicator");
+    // ncclFloat64 = 8, ncclSum = 0 (nccl.h)
+    nccl_check(nccl().all_reduce(buf, buf, count, 8, 0, comm, as_stream(stream)), "ncclAllReduce");
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,67 @@
+// common.cuh — shared device helpers for the sm_100a kernels.
+//
+// FP64 on sm_100a: tcgen05 has no f64 kind (ptxas rejects .kind::f64), so the
+// FP64 tensor path is mma.sync ...f64 -> SASS DMMA.8x8x4 (measured 37.0 TF/s,
+// profiles/r01_fp64_peaks.json; DFMA 34.1 TF/s).
+//
+// Complex GEMM on DMMA uses the exact real form of a complex product
+// (no padding of the arithmetic, 4 real FMAs per complex MAC = 8 flops):
+//   A'(2M x 2K):  A'[2i+a][2j+b] = a==b ? Re A_ij : (a==0 ? -Im A_ij : Im A_ij)
+//   B'(2K x N):   B'[2j+b][n]    = b==0 ? Re B_jn : Im B_jn
+//   C'(2M x N):   C'[2i+a][n]    = a==0 ? Re C_in : Im C_in
+// With interleaved (AoS) complex storage B' and C' are the SAME bytes as B and
+// C, so only the A fragment needs the sign/selection trick.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace lbg {
+
+// ---- m8n8k4 f64 fragments (PTX ISA, mma.m8n8k4 .f64 layout) --------------
+//   A (8x4 row): lane holds A[lane>>2][lane&3]
+//   B (4x8 col): lane holds B[lane&3][lane>>2]
+//   C (8x8):     lane holds C[lane>>2][2*(lane&3) + {0,1}]
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// Per-lane constants of the real-form A fragment for complex storage.
+struct AFragLane {
+  int di;      // complex row offset within the m8 tile: lane >> 3        (0..3)
+  int dj;      // complex col offset within the k4 step: (lane & 3) >> 1 (0..1)
+  int comp;    // which double of the complex: ((lane >> 2) ^ lane) & 1
+  double sgn;  // -1 for (row re, col im), else +1
+  __device__ __forceinline__ AFragLane(int lane) {
+    di = lane >> 3;
+    dj = (lane & 3) >> 1;
+    comp = ((lane >> 2) ^ lane) & 1;
+    sgn = (((lane >> 2) & 1) == 0 && (lane & 1) == 1) ? -1.0 : 1.0;
+  }
+};
+
+// cp.async 16-byte copy global->shared, zero-filling when !pred.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int sz = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// Pair the two lanes of a C fragment that hold Re/Im of the same complex
+// row (lane and lane^4), so each lane ends with one full complex value:
+// lane with a==0 gets column 2t, lane with a==1 gets column 2t+1.
+__device__ __forceinline__ double2 pair_complex(const double (&c)[2], int lane, int& col_off) {
+  const int a = (lane >> 2) & 1;
+  const double send = a ? c[0] : c[1];
+  const double recv = __shfl_xor_sync(0xffffffffu, send, 4);
+  col_off = 2 * (lane & 3) + a;
+  return a ? make_double2(recv, c[1]) : make_double2(c[0], recv);
+}
+
+}  // namespace lbg

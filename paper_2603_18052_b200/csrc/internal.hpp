@@ -1,0 +1,78 @@
+// internal.hpp — host-side launchers shared between the kernel translation
+// units and the C-ABI layer (capi.cu). Not part of the public boundary.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace lbg {
+
+// error types mirror the reference's exception classes (mapped to LBG_* codes)
+struct invalid_argument : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct runtime_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct cuda_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void note_launch(int n = 1);  // launch counter (capi.cu)
+
+inline void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw cuda_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define LBG_CHECK_LAUNCH(what)                  \
+  do {                                          \
+    ::lbg::note_launch();                       \
+    ::lbg::check_cuda(cudaGetLastError(), what); \
+  } while (0)
+
+enum class Layout { soa, aos };
+
+// K1a — n == 9, P in the constant bank (kernel parameter), DFMA (k_dfma9.cu)
+void launch_dfma9(const double* p_aos_host_or_null, const double* p_dev, double* x_re,
+                  double* x_im, double* x_aos, int64_t batch, int64_t steps, Layout layout,
+                  cudaStream_t s);
+// K2 — one warp per trajectory chain, latency-bound (k_chain.cu)
+bool chain_supported(std::size_t n);
+void launch_chain(const double* p_dev, std::size_t n, double* x_re, double* x_im, double* x_aos,
+                  int64_t batch, int64_t steps, Layout layout, cudaStream_t s);
+// K1b — n <= 84, P resident in shared memory, DMMA (k_smem.cu)
+bool smem_supported(std::size_t n);
+void launch_smem(const double* p_dev, std::size_t n, double* x_re, double* x_im, double* x_aos,
+                 int64_t batch, int64_t steps, Layout layout, cudaStream_t s);
+// K1c — any n, persistent DMMA tiles streamed from L2 (k_tiled.cu)
+std::size_t tiled_workspace(std::size_t n, int64_t batch);
+void launch_tiled_evolve(const double* p_dev, std::size_t n, double* x_re, double* x_im,
+                         double* x_aos, int64_t batch, int64_t steps, Layout layout, void* work,
+                         cudaStream_t s);
+// plain batched complex GEMM C[b] = A[b] * B[b] (n x n, AoS), DMMA tiles;
+// strides in complex elements
+void launch_zgemm(const double* a, const double* b, double* c, int n, int batch,
+                  long long stride_a, long long stride_b, long long stride_c, cudaStream_t s);
+
+// model kernels (k_model.cu)
+void launch_build_lindbladian(std::size_t d, const double* h, std::size_t n_ops,
+                              const double* ops, double* out, cudaStream_t s);
+void expm_dev(const double* a, std::size_t n, double dt, double* out, double* work,
+              cudaStream_t s);
+void launch_check_state(const double* x, std::size_t d, int64_t batch, double* out3,
+                        cudaStream_t s);
+void launch_step_once(const double* p, const double* v, double* out, std::size_t n,
+                      cudaStream_t s);
+
+// K3/K4/K5 fused per-trajectory sweep (k_sweep.cu)
+std::size_t sweep_workspace(std::size_t d, int64_t batch);
+void launch_sweep(std::size_t d, const double* h0, const double* hd, const double* hs,
+                  std::size_t n_ops, const double* ops, const double* delta, const double* scale,
+                  double dt, const double* rho0, int64_t batch, int64_t steps, double* pops,
+                  double* ens_sum, void* work, cudaStream_t s);
+
+int sm_count();
+
+}  // namespace lbg

@@ -1,0 +1,111 @@
+// k_chain.cu — K2: latency kernel for few trajectories (config 0: d = 3, one
+// trajectory, 10^4 dependent steps).
+//
+// Regime: a single dependent chain of tiny matvecs has no throughput
+// roofline; the bound is the per-step latency (shared-memory round trip + the
+// FMA dependency depth). One warp owns one trajectory: lane r (r < 2n) owns
+// real-form output row r and keeps that row of the real-form P in registers
+// (2n doubles); each step every lane reads the current real vector from
+// shared memory as broadcast 128-bit loads, forms its dot product in four
+// interleaved FMA chains, writes its output element and __syncwarp()s.
+// Several warps per CTA run independent trajectories.
+//
+// Replaces evolve's step loop (proj/src/propagate.cpp:88-92) around
+// step_soa_kernel (proj/src/kernels_variants.cpp:26-41).
+#include "common.cuh"
+#include "internal.hpp"
+
+namespace lbg {
+
+namespace {
+
+constexpr int kWarps = 4;
+
+template <int N, Layout L>
+__global__ void __launch_bounds__(32 * kWarps) chain_kernel(const double2* __restrict__ p,
+                                                           double* __restrict__ x_re,
+                                                           double* __restrict__ x_im,
+                                                           double* __restrict__ x_aos,
+                                                           int64_t batch, int64_t steps) {
+  constexpr int R = 2 * N;  // real-form length
+  __shared__ __align__(16) double vbuf[kWarps][2][R + 2];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t t = blockIdx.x * (int64_t)kWarps + w;
+  if (t >= batch) return;  // whole warp exits together
+  const bool active = lane < R;
+  const int i = lane >> 1, a = lane & 1;
+  // real-form row r = 2i+a of P: coef[2j+b] = A'[2i+a][2j+b]
+  double coef[R];
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    const double2 z = active ? p[i * N + j] : make_double2(0.0, 0.0);
+    coef[2 * j] = a ? z.y : z.x;       // (a, b=0): re row -> Re, im row -> Im
+    coef[2 * j + 1] = a ? z.x : -z.y;  // (a, b=1): re row -> -Im, im row -> Re
+  }
+  double* v0 = vbuf[w][0];
+  double* v1 = vbuf[w][1];
+  if (active) {
+    if (L == Layout::soa)
+      v0[lane] = a ? x_im[t * N + i] : x_re[t * N + i];
+    else
+      v0[lane] = x_aos[t * R + lane];
+  }
+  __syncwarp();
+  for (int64_t s = 0; s < steps; ++s) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int k = 0; k < R; k += 2) {
+      const double2 vv = *reinterpret_cast<const double2*>(v0 + k);
+      acc[(k >> 1) & 3] = fma(coef[k], vv.x, acc[(k >> 1) & 3]);
+      acc[(k >> 1) & 3] = fma(coef[k + 1], vv.y, acc[(k >> 1) & 3]);
+    }
+    const double out = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    if (active) v1[lane] = out;
+    __syncwarp();
+    double* tmp = v0;
+    v0 = v1;
+    v1 = tmp;
+  }
+  if (active) {
+    if (L == Layout::soa) {
+      if (a)
+        x_im[t * N + i] = v0[lane];
+      else
+        x_re[t * N + i] = v0[lane];
+    } else {
+      x_aos[t * R + lane] = v0[lane];
+    }
+  }
+}
+
+template <int N>
+void launch_n(const double* p, double* x_re, double* x_im, double* x_aos, int64_t batch,
+              int64_t steps, Layout layout, cudaStream_t s) {
+  const unsigned blocks = static_cast<unsigned>((batch + kWarps - 1) / kWarps);
+  const double2* p2 = reinterpret_cast<const double2*>(p);
+  if (layout == Layout::soa)
+    chain_kernel<N, Layout::soa><<<blocks, 32 * kWarps, 0, s>>>(p2, x_re, x_im, nullptr, batch, steps);
+  else
+    chain_kernel<N, Layout::aos><<<blocks, 32 * kWarps, 0, s>>>(p2, nullptr, nullptr, x_aos, batch, steps);
+  LBG_CHECK_LAUNCH("chain_kernel");
+}
+
+}  // namespace
+
+bool chain_supported(std::size_t n) { return n >= 1 && n <= 16; }
+
+void launch_chain(const double* p_dev, std::size_t n, double* x_re, double* x_im, double* x_aos,
+                  int64_t batch, int64_t steps, Layout layout, cudaStream_t s) {
+  if (batch <= 0) return;
+  switch (n) {
+#define LBG_CASE(N) \
+  case N: return launch_n<N>(p_dev, x_re, x_im, x_aos, batch, steps, layout, s);
+    LBG_CASE(1) LBG_CASE(2) LBG_CASE(3) LBG_CASE(4) LBG_CASE(5) LBG_CASE(6) LBG_CASE(7)
+    LBG_CASE(8) LBG_CASE(9) LBG_CASE(10) LBG_CASE(11) LBG_CASE(12) LBG_CASE(13) LBG_CASE(14)
+    LBG_CASE(15) LBG_CASE(16)
+#undef LBG_CASE
+    default: throw invalid_argument("chain kernel supports n <= 16");
+  }
+}
+
+}  // namespace lbg

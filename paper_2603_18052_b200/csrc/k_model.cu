@@ -1,0 +1,268 @@
+// k_model.cu — model-side kernels: Kronecker assembly of the vectorised
+// Lindbladian (K5, single model), the GPU propagator P = exp(L dt) (K4,
+// single matrix), the batched invariant check (K6) and the single-step shim.
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.hpp"
+
+namespace lbg {
+
+namespace {
+
+// Complex arithmetic with explicit round-to-nearest intrinsics: no FMA
+// contraction, so the assembly reproduces the reference's std::complex
+// arithmetic bit for bit (tests/test_gpu_parity.py checks L exactly).
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)),
+                      __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) {
+  return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
+}
+__device__ __forceinline__ double2 csub(double2 a, double2 b) {
+  return make_double2(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y));
+}
+__device__ __forceinline__ double2 conjd(double2 a) { return make_double2(a.x, -a.y); }
+
+// (L_m^dag L_m)[i][j] accumulated like lb::matmul (complex_matrix.cpp:41-54):
+// ascending q from zero, re += ar*br - ai*bi, im += ar*bi + ai*br, a = conj(L[q][i]).
+__device__ __forceinline__ double2 ldl_entry(const double2* __restrict__ l, int d, int i, int j) {
+  double re = 0.0, im = 0.0;
+  for (int q = 0; q < d; ++q) {
+    const double2 a = conjd(l[q * d + i]);
+    const double2 b = l[q * d + j];
+    re = __dadd_rn(re, __dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)));
+    im = __dadd_rn(im, __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
+  }
+  return make_double2(re, im);
+}
+
+// K5: element (R = i*d + k, C = j*d + l) of
+//   L = -i (H (x) I - I (x) H^T) + sum_m [ L_m (x) conj L_m - 1/2 L_m^dag L_m (x) I
+//                                        - 1/2 I (x) (L_m^dag L_m)^T ]
+// in the reference's evaluation order (lindblad.cpp:46-57): kron entries are
+// a[i][j] * b[k][l] complex products, accumulated with add_scaled.
+__global__ void build_lindbladian_kernel(const double2* __restrict__ h,
+                                         const double2* __restrict__ ops, int n_ops, int d,
+                                         double2* __restrict__ out) {
+  const int n = d * d;
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= (long long)n * n) return;
+  const int R = int(e / n), Cc = int(e - (long long)R * n);
+  const int i = R / d, k = R - i * d, j = Cc / d, l = Cc - j * d;
+  const double2 one = make_double2(1.0, 0.0), zero = make_double2(0.0, 0.0);
+  const double2 dkl = (k == l) ? one : zero, dij = (i == j) ? one : zero;
+  // -i * (kron(H, I) - kron(I, H^T))
+  const double2 t1 = cmul(h[i * d + j], dkl);
+  const double2 t2 = cmul(dij, h[l * d + k]);
+  double2 acc = cmul(make_double2(0.0, -1.0), csub(t1, t2));
+  for (int m = 0; m < n_ops; ++m) {
+    const double2* lm = ops + (long long)m * d * d;
+    acc = cadd(acc, cmul(one, cmul(lm[i * d + j], conjd(lm[k * d + l]))));
+    const double2 a = (k == l) ? ldl_entry(lm, d, i, j) : zero;
+    acc = cadd(acc, cmul(make_double2(-0.5, 0.0), cmul(a, dkl)));
+    const double2 b = (i == j) ? ldl_entry(lm, d, l, k) : zero;
+    acc = cadd(acc, cmul(make_double2(-0.5, 0.0), cmul(dij, b)));
+  }
+  out[e] = acc;
+}
+
+// out = x + c0*I + c1*a1 + c2*a2 + c3*a3 + c4*a4   (any pointer may be null)
+__global__ void combo_kernel(double2* __restrict__ out, const double2* __restrict__ x,
+                             const double2* __restrict__ a1, const double2* __restrict__ a2,
+                             const double2* __restrict__ a3, const double2* __restrict__ a4,
+                             double c0, double c1, double c2, double c3, double c4, int n) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= (long long)n * n) return;
+  const int r = int(e / n), c = int(e - (long long)r * n);
+  double2 v = x ? x[e] : make_double2(0.0, 0.0);
+  if (r == c) v.x += c0;
+  if (a1) { v.x += c1 * a1[e].x; v.y += c1 * a1[e].y; }
+  if (a2) { v.x += c2 * a2[e].x; v.y += c2 * a2[e].y; }
+  if (a3) { v.x += c3 * a3[e].x; v.y += c3 * a3[e].y; }
+  if (a4) { v.x += c4 * a4[e].x; v.y += c4 * a4[e].y; }
+  out[e] = v;
+}
+
+__global__ void scale_kernel(double2* __restrict__ out, const double2* __restrict__ a, double s,
+                             long long count) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e < count) out[e] = make_double2(a[e].x * s, a[e].y * s);
+}
+
+// column sums of |a| (one thread per column) -> colsum[n]
+__global__ void colsum_kernel(const double2* __restrict__ a, int n, double* __restrict__ colsum) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  double s = 0.0;
+  for (int r = 0; r < n; ++r) s += hypot(a[(long long)r * n + c].x, a[(long long)r * n + c].y);
+  colsum[c] = s;
+}
+
+// order-preserving map of a double to uint64 for atomic min/max
+__device__ __forceinline__ unsigned long long okey(double v) {
+  const unsigned long long b = __double_as_longlong(v);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double ounkey(unsigned long long k) {
+  return __longlong_as_double((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k);
+}
+
+// K6: validate.cpp:10-30 per trajectory, reduced over the batch.
+__global__ void check_state_kernel(const double2* __restrict__ x, int d, long long batch,
+                                   unsigned long long* __restrict__ keys) {
+  const long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  double tr_err = 0.0, herm = 0.0, mind = 1e300;
+  if (b < batch) {
+    const double2* r = x + b * d * d;
+    double tre = 0.0, tim = 0.0;
+    mind = r[0].x;
+    for (int i = 0; i < d; ++i) {
+      tre += r[i * d + i].x;
+      tim += r[i * d + i].y;
+      mind = fmin(mind, r[i * d + i].x);
+      for (int j = 0; j < d; ++j) {
+        const double2 a = r[i * d + j], c = r[j * d + i];
+        herm = fmax(herm, hypot(a.x - c.x, a.y + c.y));
+      }
+    }
+    tr_err = hypot(tre - 1.0, tim);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    tr_err = fmax(tr_err, __shfl_xor_sync(0xffffffffu, tr_err, o));
+    herm = fmax(herm, __shfl_xor_sync(0xffffffffu, herm, o));
+    mind = fmin(mind, __shfl_xor_sync(0xffffffffu, mind, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&keys[0], okey(tr_err));
+    atomicMax(&keys[1], okey(herm));
+    atomicMin(&keys[2], okey(mind));
+  }
+}
+
+__global__ void check_state_finish(const unsigned long long* __restrict__ keys, double* out3) {
+  if (threadIdx.x < 3) out3[threadIdx.x] = ounkey(keys[threadIdx.x]);
+}
+__global__ void check_state_init(unsigned long long* keys) {
+  if (threadIdx.x < 2) keys[threadIdx.x] = okey(0.0);
+  if (threadIdx.x == 2) keys[2] = okey(1e300);
+}
+
+// one matvec out[i] = sum_j P[i][j] v[j] (the raw-pointer shim), ascending j
+__global__ void step_once_kernel(const double2* __restrict__ p, const double2* __restrict__ v,
+                                 double2* __restrict__ out, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double re = 0.0, im = 0.0;
+  for (int j = 0; j < n; ++j) {
+    const double2 a = p[(long long)i * n + j], b = v[j];
+    re = fma(a.x, b.x, re);
+    re = fma(-a.y, b.y, re);
+    im = fma(a.x, b.y, im);
+    im = fma(a.y, b.x, im);
+  }
+  out[i] = make_double2(re, im);
+}
+
+unsigned blocks_for(long long n, int t) { return unsigned((n + t - 1) / t); }
+
+}  // namespace
+
+void launch_build_lindbladian(size_t d, const double* h, size_t n_ops, const double* ops,
+                              double* out, cudaStream_t s) {
+  const long long nn = (long long)(d * d) * (long long)(d * d);
+  build_lindbladian_kernel<<<blocks_for(nn, 256), 256, 0, s>>>(
+      reinterpret_cast<const double2*>(h), reinterpret_cast<const double2*>(ops), int(n_ops),
+      int(d), reinterpret_cast<double2*>(out));
+  LBG_CHECK_LAUNCH("build_lindbladian_kernel");
+}
+
+// Taylor coefficients 1/k!, k = 0..16
+static double inv_fact(int k) {
+  double f = 1.0;
+  for (int i = 2; i <= k; ++i) f *= i;
+  return 1.0 / f;
+}
+
+// P = exp(a dt): scaling and squaring around a degree-16 Taylor polynomial in
+// Paterson-Stockmeyer form (s = 4): A2 = A A, A3 = A2 A, A4 = A2 A2,
+//   P = B0 + A4 (B1 + A4 (B2 + A4 (B3 + c16 A4))),  B_j = sum_{i<4} c_{4j+i} A^i.
+// 6 complex GEMMs on DMMA, no linear solve. Truncation error
+// sum_{k>16} x^k/k! <= 2^-54 for x = ||A||_1 <= kTheta16 = 0.79 (A = a dt 2^-s).
+// Replaces lb::expm (expm.cpp:109-134: Pade-13, 6 matmuls + LU solve).
+void expm_dev(const double* a, size_t n, double dt, double* out, double* work, cudaStream_t s) {
+  constexpr double kTheta16 = 0.79;
+  const long long nn = (long long)n * (long long)n;
+  double2* w = reinterpret_cast<double2*>(work);
+  double2 *A1 = w, *A2 = w + nn, *A3 = w + 2 * nn, *A4 = w + 3 * nn, *T = w + 4 * nn, *M = w + 5 * nn;
+  double2* P = reinterpret_cast<double2*>(out);
+  // ||a dt||_1 -> number of squarings (one host sync, like the reference's
+  // synchronous expm; the result steers the launch sequence)
+  double* colsum = reinterpret_cast<double*>(M);  // scratch
+  colsum_kernel<<<blocks_for((long long)n, 128), 128, 0, s>>>(reinterpret_cast<const double2*>(a), int(n), colsum);
+  LBG_CHECK_LAUNCH("colsum_kernel");
+  std::vector<double> cs(n);
+  check_cuda(cudaMemcpyAsync(cs.data(), colsum, sizeof(double) * n, cudaMemcpyDeviceToHost, s), "D2H norm");
+  check_cuda(cudaStreamSynchronize(s), "sync norm");
+  double nrm = 0.0;
+  for (double v : cs) nrm = std::max(nrm, v);
+  nrm *= std::fabs(dt);
+  if (!std::isfinite(nrm)) throw invalid_argument("expm: non-finite entries in input");
+  int sq = 0;
+  if (nrm > kTheta16) {
+    sq = int(std::ceil(std::log2(nrm / kTheta16)));
+    if (sq > 64) throw runtime_error("expm: norm of a*dt requires more than 64 squarings");
+  }
+  const double scale = dt * std::ldexp(1.0, -sq);
+  scale_kernel<<<blocks_for(nn, 256), 256, 0, s>>>(A1, reinterpret_cast<const double2*>(a), scale, nn);
+  LBG_CHECK_LAUNCH("scale_kernel");
+  const int ni = int(n);
+  launch_zgemm(reinterpret_cast<double*>(A1), reinterpret_cast<double*>(A1), reinterpret_cast<double*>(A2), ni, 1, 0, 0, 0, s);
+  launch_zgemm(reinterpret_cast<double*>(A2), reinterpret_cast<double*>(A1), reinterpret_cast<double*>(A3), ni, 1, 0, 0, 0, s);
+  launch_zgemm(reinterpret_cast<double*>(A2), reinterpret_cast<double*>(A2), reinterpret_cast<double*>(A4), ni, 1, 0, 0, 0, s);
+  double c[17];
+  for (int k = 0; k <= 16; ++k) c[k] = inv_fact(k);
+  const unsigned g = blocks_for(nn, 256);
+  // T = B3 + c16 A4
+  combo_kernel<<<g, 256, 0, s>>>(T, nullptr, A1, A2, A3, A4, c[12], c[13], c[14], c[15], c[16], ni);
+  LBG_CHECK_LAUNCH("combo_kernel");
+  for (int j = 2; j >= 0; --j) {
+    launch_zgemm(reinterpret_cast<double*>(A4), reinterpret_cast<double*>(T), reinterpret_cast<double*>(M), ni, 1, 0, 0, 0, s);
+    double2* dst = (j == 0 && sq == 0) ? P : T;
+    combo_kernel<<<g, 256, 0, s>>>(dst, M, A1, A2, A3, nullptr, c[4 * j], c[4 * j + 1], c[4 * j + 2], c[4 * j + 3], 0.0, ni);
+    LBG_CHECK_LAUNCH("combo_kernel");
+  }
+  // squarings: T holds the current value when sq > 0
+  double2* cur = T;
+  for (int i = 0; i < sq; ++i) {
+    double2* dst = (i == sq - 1) ? P : (cur == T ? M : T);
+    launch_zgemm(reinterpret_cast<double*>(cur), reinterpret_cast<double*>(cur), reinterpret_cast<double*>(dst), ni, 1, 0, 0, 0, s);
+    cur = dst;
+  }
+}
+
+void launch_check_state(const double* x, size_t d, int64_t batch, double* out3, cudaStream_t s) {
+  // keys live in the 3 doubles after out3's slot? use a small static device buffer per call
+  unsigned long long* keys = nullptr;
+  check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&keys), 3 * sizeof(unsigned long long), s), "malloc keys");
+  check_state_init<<<1, 32, 0, s>>>(keys);
+  LBG_CHECK_LAUNCH("check_state_init");
+  if (batch > 0) {
+    check_state_kernel<<<blocks_for(batch, 256), 256, 0, s>>>(reinterpret_cast<const double2*>(x), int(d), batch, keys);
+    LBG_CHECK_LAUNCH("check_state_kernel");
+  }
+  check_state_finish<<<1, 32, 0, s>>>(keys, out3);
+  LBG_CHECK_LAUNCH("check_state_finish");
+  check_cuda(cudaFreeAsync(keys, s), "free keys");
+}
+
+void launch_step_once(const double* p, const double* v, double* out, size_t n, cudaStream_t s) {
+  step_once_kernel<<<blocks_for((long long)n, 128), 128, 0, s>>>(
+      reinterpret_cast<const double2*>(p), reinterpret_cast<const double2*>(v),
+      reinterpret_cast<double2*>(out), int(n));
+  LBG_CHECK_LAUNCH("step_once_kernel");
+}
+
+}  // namespace lbg

@@ -1,0 +1,177 @@
+// k_smem.cu — K1b: shared-P batched propagation with P resident in shared
+// memory, FP64 tensor cores (DMMA) — config 2 (d = 9, n = 81, 4,096 trajectories).
+//
+// Each CTA owns 32 trajectories (four 8-wide MMA n-tiles) for ALL steps:
+//   - P (n x n complex, 110 KB padded) is staged once into shared memory;
+//   - the 32 state vectors live in shared memory in real form, ping-ponged;
+//   - per step the CTA computes V_next' (2n x 32) = P' (2n x 2n) * V' (2n x 32)
+//     as m8n8k4 DMMAs (real form of the complex product, common.cuh), 12 warps =
+//     3 row groups x 4 n-tiles (3 warps per SMSP, balanced), then __syncthreads().
+// HBM traffic is one read + one write of the state and one read of P per CTA;
+// the bound is the DMMA pipe (tile use at n=81: 162/168 rows x 162/164 k = 95.3%).
+// Shared-memory layouts are padded so every fragment load is conflict-free:
+//   P row stride SP = 2 (mod 8) complex, V row stride SV = 4 (mod 16) doubles.
+//
+// Replaces step_soa_kernel (proj/src/kernels_variants.cpp:26-41) inside
+// evolve (proj/src/propagate.cpp:85-92), batched over trajectories.
+#include "common.cuh"
+#include "internal.hpp"
+
+namespace lbg {
+
+namespace {
+
+constexpr int kTraj = 32;   // trajectories per CTA (4 n-tiles)
+constexpr int kWarps = 12;  // 3 row groups x 4 n-tiles
+constexpr int kMaxN = 84;
+
+struct SmemGeom {
+  int n, mt, kt, sp, sv;
+  size_t p_bytes, v_bytes, total;
+  __host__ __device__ SmemGeom(int n_) : n(n_) {
+    mt = (n + 3) / 4;      // m8 tiles over 2n real rows
+    kt = (n + 1) / 2;      // k4 steps over 2n real cols
+    sp = 2 * kt;           // complex cols incl. K padding
+    sp += (2 - (sp % 8) + 8) % 8;  // sp = 2 (mod 8)
+    sv = 4 * kt;           // doubles per trajectory row incl. K padding
+    sv += (4 - (sv % 16) + 16) % 16;  // sv = 4 (mod 16)
+    p_bytes = size_t(mt) * 4 * sp * 16;
+    v_bytes = size_t(kTraj) * sv * 8;
+    total = p_bytes + 2 * v_bytes;
+  }
+};
+
+template <int MG, Layout L>
+__global__ void __launch_bounds__(32 * kWarps, 1)
+    smem_kernel(const double2* __restrict__ p, int n, double* __restrict__ x_re,
+                double* __restrict__ x_im, double* __restrict__ x_aos, int64_t batch,
+                int64_t steps) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const SmemGeom g(n);
+  double2* ps = reinterpret_cast<double2*>(smem);
+  double* va = reinterpret_cast<double*>(smem + g.p_bytes);
+  double* vb = reinterpret_cast<double*>(smem + g.p_bytes + g.v_bytes);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t b0 = int64_t(blockIdx.x) * kTraj;
+
+  // ---- stage P (zero padded) and the CTA's 32 state vectors (real form) ----
+  const int prow = g.mt * 4;
+  for (int e = tid; e < prow * g.sp; e += blockDim.x) {
+    const int i = e / g.sp, j = e - i * g.sp;
+    ps[e] = (i < n && j < n) ? p[size_t(i) * n + j] : make_double2(0.0, 0.0);
+  }
+  for (int e = tid; e < kTraj * g.sv; e += blockDim.x) {
+    const int t = e / g.sv, r = e - t * g.sv;
+    const int64_t b = b0 + t;
+    double v = 0.0;
+    if (b < batch && r < 2 * n) {
+      if (L == Layout::soa)
+        v = (r & 1) ? x_im[b * n + (r >> 1)] : x_re[b * n + (r >> 1)];
+      else
+        v = x_aos[b * 2 * n + r];
+    }
+    va[e] = v;
+    vb[e] = 0.0;
+  }
+  __syncthreads();
+
+  const AFragLane af(lane);
+  const int mg = warp >> 2;  // row group 0..2
+  const int nt = warp & 3;   // n-tile 0..3
+  const int m_begin = mg * MG;
+  const int bn = nt * 8 + (lane >> 2);  // B fragment column (trajectory in CTA)
+  const int bk = lane & 3;              // B fragment k within the step
+
+  for (int64_t s = 0; s < steps; ++s) {
+    double acc[MG][2];
+#pragma unroll
+    for (int mi = 0; mi < MG; ++mi) acc[mi][0] = acc[mi][1] = 0.0;
+    const double* vrow = va + bn * g.sv + bk;
+#pragma unroll 2
+    for (int ks = 0; ks < g.kt; ++ks) {
+      const double bfrag = vrow[ks * 4];
+      const double* pcol = reinterpret_cast<const double*>(ps) + 2 * (ks * 2 + af.dj) + af.comp;
+#pragma unroll
+      for (int mi = 0; mi < MG; ++mi) {
+        const int mt = m_begin + mi;
+        if (mt < g.mt) {
+          const double afrag = af.sgn * pcol[size_t(mt * 4 + af.di) * 2 * g.sp];
+          dmma(acc[mi], afrag, bfrag);
+        }
+      }
+    }
+    // epilogue: complex-pair the fragments and write V_next (real form)
+#pragma unroll
+    for (int mi = 0; mi < MG; ++mi) {
+      const int mt = m_begin + mi;
+      if (mt < g.mt) {
+        int coff;
+        const double2 z = pair_complex(acc[mi], lane, coff);
+        const int i = mt * 4 + (lane >> 3);
+        const int t = nt * 8 + coff;
+        if (i < n) *reinterpret_cast<double2*>(vb + t * g.sv + 2 * i) = z;
+      }
+    }
+    __syncthreads();
+    double* tmp = va;
+    va = vb;
+    vb = tmp;
+  }
+
+  // ---- write the final states back ----
+  for (int e = tid; e < kTraj * 2 * n; e += blockDim.x) {
+    const int t = e / (2 * n), r = e - t * 2 * n;
+    const int64_t b = b0 + t;
+    if (b >= batch) continue;
+    const double v = va[t * g.sv + r];
+    if (L == Layout::soa) {
+      if (r & 1)
+        x_im[b * n + (r >> 1)] = v;
+      else
+        x_re[b * n + (r >> 1)] = v;
+    } else {
+      x_aos[b * 2 * n + r] = v;
+    }
+  }
+}
+
+template <int MG>
+void launch_mg(const double* p, int n, double* x_re, double* x_im, double* x_aos, int64_t batch,
+               int64_t steps, Layout layout, cudaStream_t s) {
+  const SmemGeom g(n);
+  const unsigned blocks = static_cast<unsigned>((batch + kTraj - 1) / kTraj);
+  const double2* p2 = reinterpret_cast<const double2*>(p);
+  if (layout == Layout::soa) {
+    auto k = smem_kernel<MG, Layout::soa>;
+    check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(g.total)),
+               "smem attr");
+    k<<<blocks, 32 * kWarps, g.total, s>>>(p2, n, x_re, x_im, nullptr, batch, steps);
+  } else {
+    auto k = smem_kernel<MG, Layout::aos>;
+    check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(g.total)),
+               "smem attr");
+    k<<<blocks, 32 * kWarps, g.total, s>>>(p2, n, nullptr, nullptr, x_aos, batch, steps);
+  }
+  LBG_CHECK_LAUNCH("smem_kernel");
+}
+
+}  // namespace
+
+bool smem_supported(std::size_t n) { return n >= 1 && n <= kMaxN; }
+
+void launch_smem(const double* p_dev, std::size_t n, double* x_re, double* x_im, double* x_aos,
+                 int64_t batch, int64_t steps, Layout layout, cudaStream_t s) {
+  if (batch <= 0) return;
+  if (!smem_supported(n)) throw invalid_argument("smem kernel supports n <= 84");
+  const int mt = (int(n) + 3) / 4;
+  const int mg = (mt + 2) / 3;
+  switch (mg) {
+#define LBG_CASE(M) \
+  case M: return launch_mg<M>(p_dev, int(n), x_re, x_im, x_aos, batch, steps, layout, s);
+    LBG_CASE(1) LBG_CASE(2) LBG_CASE(3) LBG_CASE(4) LBG_CASE(5) LBG_CASE(6) LBG_CASE(7)
+#undef LBG_CASE
+    default: throw invalid_argument("smem kernel: n too large");
+  }
+}
+
+}  // namespace lbg

@@ -1,0 +1,250 @@
+// k_sweep.cu — config 4 ("robustness atlas"): per-trajectory propagators.
+// For every trajectory b:   H_b = h0 + delta_b hd + scale_b hs,
+//   K5  L_b dt  assembled on the GPU by the Kronecker formula (dissipator part
+//       D = sum_k [L_k (x) conj L_k - ...] is trajectory independent, built once),
+//   K4  P_b = exp(L_b dt) by batched Taylor-16 / Paterson-Stockmeyer on DMMA
+//       (the batched complex GEMM of k_tiled.cu),
+//   K3  rho_b <- P_b^steps rho0 with P_b resident in shared memory; epilogue
+//       writes the populations and adds rho_b into the ensemble sum.
+// Trajectories are processed in chunks so the per-trajectory matrices
+// (7 x 105 KB at d = 9) fit a bounded workspace; P_b never leaves the GPU.
+//
+// Replaces, per trajectory, make_model + build_lindbladian + expm + the step
+// loop of lb::grape_chain (proj/src/propagate.cpp:130-160).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.hpp"
+
+namespace lbg {
+
+namespace {
+
+constexpr int64_t kChunk = 4096;
+constexpr int kThetaSq = 0;  // see host side
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+// A_b = scale_dt * (D + coherent(H_b)),  coherent(H)[(i,k),(j,l)] = -i (H_ij d_kl - d_ij H_lk)
+__global__ void sweep_assemble_kernel(const double2* __restrict__ dis, const double2* __restrict__ h0,
+                                      const double2* __restrict__ hd, const double2* __restrict__ hs,
+                                      const double* __restrict__ delta, const double* __restrict__ scale,
+                                      int d, double sdt, double2* __restrict__ A, long long stride) {
+  const int n = d * d;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (e >= n * n) return;
+  const int R = e / n, C = e - R * n;
+  const int i = R / d, k = R - i * d, j = C / d, l = C - j * d;
+  const double db = delta[b], sb = scale[b];
+  double2 acc = dis[e];
+  // -i * x = (x.im, -x.re)
+  if (k == l) {
+    const double2 hij = make_double2(h0[i * d + j].x + db * hd[i * d + j].x + sb * hs[i * d + j].x,
+                                     h0[i * d + j].y + db * hd[i * d + j].y + sb * hs[i * d + j].y);
+    acc.x += hij.y;
+    acc.y -= hij.x;
+  }
+  if (i == j) {
+    const double2 hlk = make_double2(h0[l * d + k].x + db * hd[l * d + k].x + sb * hs[l * d + k].x,
+                                     h0[l * d + k].y + db * hd[l * d + k].y + sb * hs[l * d + k].y);
+    acc.x -= hlk.y;
+    acc.y += hlk.x;
+  }
+  A[b * stride + e] = make_double2(acc.x * sdt, acc.y * sdt);
+}
+
+// batched out = x + c0 I + c1 a1 + c2 a2 + c3 a3 + c4 a4
+__global__ void combo_batched_kernel(double2* __restrict__ out, const double2* __restrict__ x,
+                                     const double2* __restrict__ a1, const double2* __restrict__ a2,
+                                     const double2* __restrict__ a3, const double2* __restrict__ a4,
+                                     double c0, double c1, double c2, double c3, double c4, int n,
+                                     long long stride) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * n) return;
+  const long long o = blockIdx.y * stride + e;
+  const int r = e / n, c = e - r * n;
+  double2 v = x ? x[o] : make_double2(0.0, 0.0);
+  if (r == c) v.x += c0;
+  if (a1) { v.x += c1 * a1[o].x; v.y += c1 * a1[o].y; }
+  if (a2) { v.x += c2 * a2[o].x; v.y += c2 * a2[o].y; }
+  if (a3) { v.x += c3 * a3[o].x; v.y += c3 * a3[o].y; }
+  if (a4) { v.x += c4 * a4[o].x; v.y += c4 * a4[o].y; }
+  out[o] = v;
+}
+
+// per-trajectory 1-norm (max column sum of moduli), max-reduced into *nmax
+__global__ void sweep_norm_kernel(const double2* __restrict__ A, int n, long long stride,
+                                  unsigned long long* __restrict__ nmax) {
+  const int b = blockIdx.x;
+  double best = 0.0;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < n; ++r) s += hypot(A[b * stride + (long long)r * n + c].x, A[b * stride + (long long)r * n + c].y);
+    best = fmax(best, s);
+  }
+  for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(nmax, (unsigned long long)__double_as_longlong(best));
+}
+
+// K3: one CTA per trajectory, P_b resident in shared memory (row stride n = 81
+// complex is odd, so the 32 rows a warp reads per j hit distinct 16-B groups).
+__global__ void __launch_bounds__(96) sweep_step_kernel(const double2* __restrict__ P, long long stride,
+                                                       const double2* __restrict__ rho0, int d,
+                                                       int64_t steps, double* __restrict__ pops,
+                                                       double* __restrict__ ens_sum) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = d * d;
+  double2* ps = reinterpret_cast<double2*>(smem);
+  double2* va = ps + n * n;
+  double2* vb = va + n;
+  const int b = blockIdx.x;
+  const double2* pb = P + b * stride;
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) ps[e] = pb[e];
+  for (int e = threadIdx.x; e < n; e += blockDim.x) va[e] = rho0[e];
+  __syncthreads();
+  const int i = threadIdx.x;
+  for (int64_t s = 0; s < steps; ++s) {
+    if (i < n) {
+      double re = 0.0, im = 0.0, re2 = 0.0, im2 = 0.0;
+      const double2* row = ps + i * n;
+      int j = 0;
+      for (; j + 1 < n; j += 2) {
+        const double2 a = row[j], v = va[j];
+        const double2 a2 = row[j + 1], v2 = va[j + 1];
+        re = fma(a.x, v.x, re);
+        re = fma(-a.y, v.y, re);
+        im = fma(a.x, v.y, im);
+        im = fma(a.y, v.x, im);
+        re2 = fma(a2.x, v2.x, re2);
+        re2 = fma(-a2.y, v2.y, re2);
+        im2 = fma(a2.x, v2.y, im2);
+        im2 = fma(a2.y, v2.x, im2);
+      }
+      if (j < n) {
+        const double2 a = row[j], v = va[j];
+        re = fma(a.x, v.x, re);
+        re = fma(-a.y, v.y, re);
+        im = fma(a.x, v.y, im);
+        im = fma(a.y, v.x, im);
+      }
+      vb[i] = make_double2(re + re2, im + im2);
+    }
+    __syncthreads();
+    double2* t = va;
+    va = vb;
+    vb = t;
+  }
+  if (i < d) pops[(long long)b * d + i] = va[i * d + i].x;
+  for (int e = threadIdx.x; e < n; e += blockDim.x) {
+    atomicAdd(&ens_sum[2 * e], va[e].x);
+    atomicAdd(&ens_sum[2 * e + 1], va[e].y);
+  }
+}
+
+double inv_fact(int k) {
+  double f = 1.0;
+  for (int i = 2; i <= k; ++i) f *= i;
+  return 1.0 / f;
+}
+
+}  // namespace
+
+size_t sweep_workspace(size_t d, int64_t batch) {
+  const size_t n = d * d;
+  const size_t chunk = size_t(std::min<int64_t>(std::max<int64_t>(batch, 1), kChunk));
+  return 7 * align_up(chunk * n * n * 16) + align_up(n * n * 16) + 256;
+}
+
+void launch_sweep(size_t d, const double* h0, const double* hd, const double* hs, size_t n_ops,
+                  const double* ops, const double* delta, const double* scale, double dt,
+                  const double* rho0, int64_t batch, int64_t steps, double* pops, double* ens_sum,
+                  void* work, cudaStream_t s) {
+  if (!work) throw invalid_argument("sweep: workspace required");
+  if (d * d > 96) throw invalid_argument("sweep: supports d*d <= 96");
+  const int n = int(d * d);
+  const long long nn = (long long)n * n;
+  const size_t chunk = size_t(std::min<int64_t>(std::max<int64_t>(batch, 1), kChunk));
+  char* w = static_cast<char*>(work);
+  const size_t mb = align_up(chunk * nn * 16);
+  double2* M[7];
+  for (int q = 0; q < 7; ++q) M[q] = reinterpret_cast<double2*>(w + q * mb);
+  double2* dis = reinterpret_cast<double2*>(w + 7 * mb);
+  unsigned long long* nmax = reinterpret_cast<unsigned long long*>(w + 7 * mb + align_up(nn * 16));
+
+  // trajectory-independent dissipator D = build_lindbladian(H = 0, ops)
+  check_cuda(cudaMemsetAsync(M[0], 0, d * d * 16, s), "memset");
+  launch_build_lindbladian(d, reinterpret_cast<const double*>(M[0]), n_ops, ops,
+                           reinterpret_cast<double*>(dis), s);
+  check_cuda(cudaMemsetAsync(ens_sum, 0, nn > 0 ? size_t(n) * 16 : 0, s), "memset ens");
+  if (batch == 0) return;
+
+  // one pass over all trajectories' norms fixes a common squaring count
+  check_cuda(cudaMemsetAsync(nmax, 0, 8, s), "memset");
+  for (int64_t c0 = 0; c0 < batch; c0 += int64_t(chunk)) {
+    const int cb = int(std::min<int64_t>(int64_t(chunk), batch - c0));
+    sweep_assemble_kernel<<<dim3((nn + 255) / 256, cb), 256, 0, s>>>(
+        dis, reinterpret_cast<const double2*>(h0), reinterpret_cast<const double2*>(hd),
+        reinterpret_cast<const double2*>(hs), delta + c0, scale + c0, int(d), dt, M[0], nn);
+    LBG_CHECK_LAUNCH("sweep_assemble_kernel");
+    sweep_norm_kernel<<<cb, 128, 0, s>>>(M[0], n, nn, nmax);
+    LBG_CHECK_LAUNCH("sweep_norm_kernel");
+  }
+  unsigned long long bits = 0;
+  check_cuda(cudaMemcpyAsync(&bits, nmax, 8, cudaMemcpyDeviceToHost, s), "D2H");
+  check_cuda(cudaStreamSynchronize(s), "sync");
+  double nrm;
+  std::memcpy(&nrm, &bits, 8);
+  if (!std::isfinite(nrm)) throw invalid_argument("sweep: non-finite generator");
+  constexpr double kTheta16 = 0.79;
+  int sq = 0;
+  if (nrm > kTheta16) sq = int(std::ceil(std::log2(nrm / kTheta16)));
+  if (sq > 64) throw runtime_error("sweep: norm requires more than 64 squarings");
+  const double sdt = dt * std::ldexp(1.0, -sq);
+  (void)kThetaSq;
+
+  double c[17];
+  for (int k = 0; k <= 16; ++k) c[k] = inv_fact(k);
+  const size_t smem = size_t(nn + 2 * n) * 16;
+  check_cuda(cudaFuncSetAttribute(sweep_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+             "smem attr");
+  double2 *A1 = M[0], *A2 = M[1], *A3 = M[2], *A4 = M[3], *T = M[4], *MM = M[5], *P = M[6];
+  for (int64_t c0 = 0; c0 < batch; c0 += int64_t(chunk)) {
+    const int cb = int(std::min<int64_t>(int64_t(chunk), batch - c0));
+    const dim3 eg((nn + 255) / 256, cb);
+    sweep_assemble_kernel<<<eg, 256, 0, s>>>(
+        dis, reinterpret_cast<const double2*>(h0), reinterpret_cast<const double2*>(hd),
+        reinterpret_cast<const double2*>(hs), delta + c0, scale + c0, int(d), sdt, A1, nn);
+    LBG_CHECK_LAUNCH("sweep_assemble_kernel");
+    auto mm = [&](const double2* a, const double2* b, double2* out) {
+      launch_zgemm(reinterpret_cast<const double*>(a), reinterpret_cast<const double*>(b),
+                   reinterpret_cast<double*>(out), n, cb, nn, nn, nn, s);
+    };
+    mm(A1, A1, A2);
+    mm(A2, A1, A3);
+    mm(A2, A2, A4);
+    combo_batched_kernel<<<eg, 256, 0, s>>>(T, nullptr, A1, A2, A3, A4, c[12], c[13], c[14], c[15], c[16], n, nn);
+    LBG_CHECK_LAUNCH("combo_batched_kernel");
+    for (int j = 2; j >= 0; --j) {
+      mm(A4, T, MM);
+      double2* dst = (j == 0 && sq == 0) ? P : T;
+      combo_batched_kernel<<<eg, 256, 0, s>>>(dst, MM, A1, A2, A3, nullptr, c[4 * j], c[4 * j + 1],
+                                              c[4 * j + 2], c[4 * j + 3], 0.0, n, nn);
+      LBG_CHECK_LAUNCH("combo_batched_kernel");
+    }
+    double2* cur = T;
+    for (int i = 0; i < sq; ++i) {
+      double2* dst = (i == sq - 1) ? P : (cur == T ? MM : T);
+      mm(cur, cur, dst);
+      cur = dst;
+    }
+    sweep_step_kernel<<<cb, 96, smem, s>>>(P, nn, reinterpret_cast<const double2*>(rho0), int(d), steps,
+                                           pops + c0 * int64_t(d), ens_sum);
+    LBG_CHECK_LAUNCH("sweep_step_kernel");
+  }
+}
+
+}  // namespace lbg

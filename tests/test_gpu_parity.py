@@ -1,0 +1,272 @@
+"""GPU parity: every kernel path through the C-ABI (liblbg.so) against the
+pinned CPU oracle (oracle/lbo.c) and the reference's golden vectors.
+
+Tolerances (BASELINE.json north_star): max |rho_gpu - rho_cpu| <= 1e-10 after
+the full step count; |Tr rho - 1| <= 1e-12 and max |rho - rho^dag| <= 1e-12 on
+GPU outputs. The GPU propagator uses Taylor-16/Paterson-Stockmeyer instead of
+the reference's Pade-13 (both accurate to unit roundoff), so P itself is
+compared at 1e-13 relative; the generator L is compared bit for bit.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL_RHO = 1e-10
+TOL_INV = 1e-12
+ALGOS_FOR = {  # which kernel paths can run a given n
+    4: ("chain", "smem", "tiled"),
+    9: ("chain", "dfma9", "smem", "tiled"),
+    81: ("smem", "tiled"),
+    729: ("tiled",),
+}
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    return torch
+
+
+def invariants(rho):
+    tr = np.abs(np.trace(rho, axis1=-2, axis2=-1) - 1.0).max()
+    herm = np.abs(rho - np.conj(np.swapaxes(rho, -1, -2))).max()
+    return tr, herm
+
+
+# ------------------------------------------------------------ assembly / P ---
+def test_lindbladian_bitwise_vs_reference(lbg, golden, oracle):
+    g = golden["models"]
+    for cfg in range(3):
+        L = lbg.build_lindbladian(g[f"c{cfg}_h"], g[f"c{cfg}_ops"])
+        assert np.array_equal(L, g[f"c{cfg}_L"]), cfg
+    h, ops = lbg.config_model(3)
+    assert np.array_equal(lbg.build_lindbladian(h, ops), oracle.build_lindbladian(h, ops))
+    k = golden["kat"]
+    h2 = np.zeros((2, 2), complex)
+    l2 = np.zeros((1, 2, 2), complex)
+    l2[0, 0, 1] = np.sqrt(0.7)
+    assert np.array_equal(lbg.build_lindbladian(h2, l2), k["ad_L"])
+
+
+def test_non_hermitian_rejected(lbg):
+    h = np.zeros((2, 2), complex)
+    h[0, 1] = 1.0
+    with pytest.raises(ValueError):
+        lbg.build_lindbladian(h, np.zeros((0, 2, 2), complex))
+
+
+def test_expm_vs_reference(lbg, golden):
+    g, k = golden["models"], golden["kat"]
+    for cfg in range(3):
+        P = lbg.expm(g[f"c{cfg}_L"], 0.1)
+        ref = g[f"c{cfg}_P"]
+        assert np.abs(P - ref).max() <= 1e-13 * np.abs(ref).max(), cfg
+        # trace preservation of the propagator: vec(I)^dag P = vec(I)^dag
+        d = int(round(np.sqrt(P.shape[0])))
+        idv = np.eye(d).reshape(-1)
+        assert np.abs(idv @ P - idv).max() <= 1e-14
+    for a, p in (("expm_a", "expm_p"), ("expm_big_a", "expm_big_p")):
+        got = lbg.expm(k[a], 1.0)
+        assert np.abs(got - k[p]).max() <= 1e-12 * np.abs(k[p]).max(), a
+    assert np.abs(lbg.expm(np.zeros((3, 3)), 0.1) - np.eye(3)).max() == 0.0
+    nil = np.zeros((2, 2), complex)
+    nil[0, 1] = 1.0
+    assert np.abs(lbg.expm(nil, 1.0) - np.array([[1, 1], [0, 1]])).max() <= 1e-15
+    with pytest.raises(ValueError):
+        lbg.expm(np.full((2, 2), np.nan), 1.0)
+
+
+def test_expm_d27_vs_oracle(lbg, oracle):
+    h, ops = lbg.config_model(3)
+    L = lbg.build_lindbladian(h, ops)
+    P = lbg.expm(L, 0.1)
+    ref = oracle.expm(L, 0.1)
+    assert np.abs(P - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+# ----------------------------------------------------------- raw step shim ---
+def test_step_shims_vs_oracle(lbg, oracle):
+    rng = np.random.default_rng(11)
+    for n in (1, 4, 9, 16, 81, 729):
+        p = rng.uniform(-1, 1, (n, n)) + 1j * rng.uniform(-1, 1, (n, n))
+        v = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+        want = oracle.step_soa(p, v)
+        scale = np.abs(want).max()
+        assert np.abs(lbg.step_soa(p, v) - want).max() <= 1e-13 * scale
+        assert np.abs(lbg.step_aos(p, v) - want).max() <= 1e-13 * scale
+    v = rng.uniform(-1, 1, 9) + 1j * rng.uniform(-1, 1, 9)
+    assert np.array_equal(lbg.step_soa(np.eye(9), v), v)  # identity bitwise
+    assert lbg.step_aos(np.array([[2 + 1j]]), np.array([1 - 1j]))[0] == 3 - 1j
+
+
+# ------------------------------------------------- golden config subsets ---
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3])
+def test_config_subsets_vs_reference_goldens(lbg, golden, oracle, cfg):
+    g, m = golden["evolve"], golden["models"]
+    if cfg < 3:
+        P = m[f"c{cfg}_P"]
+    else:
+        h, ops = lbg.config_model(3)
+        P = oracle.expm(oracle.build_lindbladian(h, ops), 0.1)
+    rho0, want, steps = g[f"c{cfg}_rho0"], g[f"c{cfg}_out"], int(g[f"c{cfg}_steps"])
+    for algo in ALGOS_FOR[P.shape[0]]:
+        got = lbg.evolve_batch(P, rho0, steps, algo=algo)
+        err = np.abs(got - want).max()
+        assert err <= TOL_RHO, (algo, err)
+        tr, herm = invariants(got)
+        assert tr <= TOL_INV and herm <= TOL_INV, (algo, tr, herm)
+    # the full product path: GPU-built P
+    hh, oo = lbg.config_model(cfg)
+    Pg = lbg.expm(lbg.build_lindbladian(hh, oo), 0.1)
+    got = lbg.evolve_batch(Pg, rho0, steps)
+    assert np.abs(got - want).max() <= TOL_RHO
+
+
+def test_closed_form_damping_every_path(lbg):
+    gamma, dt, n = 0.7, 0.004, 500
+    h = np.zeros((2, 2), complex)
+    l = np.zeros((1, 2, 2), complex)
+    l[0, 0, 1] = np.sqrt(gamma)
+    P = lbg.expm(lbg.build_lindbladian(h, l), dt)
+    rho0 = np.zeros((2, 2), complex)
+    rho0[1, 1] = 1.0
+    want = np.exp(-gamma * n * dt)
+    for algo in ALGOS_FOR[4]:
+        rho = lbg.evolve(P, rho0, n, algo=algo)
+        assert abs(rho[1, 1].real - want) < 1e-10
+        assert abs(rho[0, 0].real - (1 - want)) < 1e-10
+        assert abs(rho[0, 1]) < 1e-12
+        assert lbg.check_state(rho)["passed"]
+
+
+def test_evolve_contract(lbg, golden):
+    P = golden["models"]["c1_P"]
+    rho0 = golden["evolve"]["c1_rho0"][:5]
+    for algo in ALGOS_FOR[9]:
+        assert np.array_equal(lbg.evolve_batch(P, rho0, 0, algo=algo), rho0)  # zero steps
+        direct = lbg.evolve_batch(P, rho0, 10, algo=algo)
+        stacked = lbg.evolve_batch(P, lbg.evolve_batch(P, rho0, 4, algo=algo), 6, algo=algo)
+        assert np.array_equal(direct, stacked), algo  # composes bitwise
+    zero_gen = lbg.expm(np.zeros((9, 9)), 0.1)
+    assert np.abs(lbg.evolve_batch(zero_gen, rho0, 1000) - rho0).max() < 1e-12
+    with pytest.raises(ValueError):
+        lbg.evolve(P, np.eye(3), 1)  # trace 3
+    bad = np.diag([1.0, 0, 0]).astype(complex)
+    bad[0, 1] = 0.5
+    with pytest.raises(ValueError):
+        lbg.evolve(P, bad, 1)  # not Hermitian
+    with pytest.raises(ValueError):
+        lbg.evolve(np.eye(4), np.diag([1.0, 0, 0]), 1)  # shape mismatch
+
+
+# ------------------------------------------------------------- full sizes ---
+def _full_run(lbg, torch, cfg, B, S, algo, check_idx, oracle, P=None):
+    d, _ = lbg.config_dims(cfg)
+    if P is None:
+        h, ops = lbg.config_model(cfg)
+        P = lbg.expm(lbg.build_lindbladian(h, ops), 0.1)
+    rho0 = lbg.ginibre_batch(cfg, 0, B, d)
+    dev = torch.device("cuda")
+    pt = torch.from_numpy(P).to(dev)
+    xt = torch.from_numpy(rho0.reshape(B, d * d)).to(dev)
+    ws = lbg.evolve_workspace(d * d, B, algo)
+    work = torch.empty(max(ws, 1), dtype=torch.uint8, device=dev)
+    lbg.evolve_batch_dev(pt, xt, S, algo=algo, work=work)
+    torch.cuda.synchronize()
+    out = xt.cpu().numpy().reshape(B, d, d)
+    tr, herm = invariants(out)
+    assert tr <= TOL_INV and herm <= TOL_INV, (cfg, tr, herm)
+    for b in check_idx:
+        want = oracle.evolve(P, rho0[b], S)
+        assert np.abs(out[b] - want).max() <= TOL_RHO, (cfg, b)
+    return out
+
+
+def test_config1_full_size(lbg, torch, oracle):
+    rng = np.random.default_rng(0)
+    _full_run(lbg, torch, 1, 1 << 20, 1000, "dfma9", rng.integers(0, 1 << 20, 64), oracle)
+
+
+def test_config2_full_size(lbg, torch, oracle):
+    rng = np.random.default_rng(1)
+    _full_run(lbg, torch, 2, 4096, 1000, "smem", list(rng.integers(0, 4096, 24)) + [4095], oracle)
+
+
+def test_config3_full_size(lbg, torch, oracle):
+    _full_run(lbg, torch, 3, 1024, 200, "tiled", [0, 517, 1023], oracle)
+
+
+def test_tiled_is_linear_at_scale(lbg, torch):
+    """size-independent property at a large, non-physical, ragged shape."""
+    dev = torch.device("cuda")
+    n, B = 200, 333
+    g = torch.Generator(device="cpu").manual_seed(3)
+    P = (torch.randn(n, n, dtype=torch.complex128, generator=g) / n).to(dev)
+    x = torch.randn(B, n, dtype=torch.complex128, generator=g).to(dev)
+    y = torch.randn(B, n, dtype=torch.complex128, generator=g).to(dev)
+    a = 0.3 - 1.2j
+    ws = torch.empty(lbg.evolve_workspace(n, B, "tiled"), dtype=torch.uint8, device=dev)
+    z = a * x + y
+    for t in (x, y, z):
+        lbg.evolve_batch_dev(P, t, 7, algo="tiled", work=ws)
+    torch.cuda.synchronize()
+    assert (z - (a * x + y)).abs().max().item() <= 1e-12 * (a * x + y).abs().max().item()
+    ref = x.clone()
+    # against torch fp64 matmuls (a plain fp64 reference of the same op)
+    x0 = torch.randn(B, n, dtype=torch.complex128, generator=g).to(dev)
+    x1 = x0.clone()
+    lbg.evolve_batch_dev(P, x1, 3, algo="tiled", work=ws)
+    want = x0
+    for _ in range(3):
+        want = want @ P.T
+    torch.cuda.synchronize()
+    assert (x1 - want).abs().max().item() <= 1e-12 * want.abs().max().item()
+    del ref
+
+
+# ----------------------------------------------------------- config 4 sweep ---
+def test_sweep_vs_reference_goldens(lbg, torch, golden):
+    s = golden["sweep"]
+    dev = torch.device("cuda")
+    h0, hd, hs = lbg.config_sweep_terms()
+    _, ops = lbg.config_model(4)
+    B = s["delta"].shape[0]
+    rho0 = np.zeros((9, 9), complex)
+    rho0[0, 0] = 1.0
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    pops = torch.zeros(B, 9, dtype=torch.float64, device=dev)
+    ens = torch.zeros(9, 9, dtype=torch.complex128, device=dev)
+    work = torch.empty(lbg.sweep_workspace(9, B), dtype=torch.uint8, device=dev)
+    lbg.evolve_sweep_dev(T(h0), T(hd), T(hs), T(ops), T(s["delta"]), T(s["scale"]), 0.1, T(rho0),
+                         int(s["steps"]), pops, ens, work)
+    torch.cuda.synchronize()
+    assert np.abs(pops.cpu().numpy() - s["pops"]).max() <= TOL_RHO
+    assert np.abs(ens.cpu().numpy() - s["ens_sum"]).max() <= TOL_RHO * B
+    e = ens.cpu().numpy() / B
+    tr, herm = invariants(e)
+    assert tr <= TOL_INV and herm <= TOL_INV
+
+
+def test_sweep_full_size_invariants(lbg, torch):
+    dev = torch.device("cuda")
+    B = 65536
+    h0, hd, hs = lbg.config_sweep_terms()
+    _, ops = lbg.config_model(4)
+    delta, scale = lbg.sweep_params(0, B)
+    rho0 = np.zeros((9, 9), complex)
+    rho0[0, 0] = 1.0
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    pops = torch.zeros(B, 9, dtype=torch.float64, device=dev)
+    ens = torch.zeros(9, 9, dtype=torch.complex128, device=dev)
+    work = torch.empty(lbg.sweep_workspace(9, B), dtype=torch.uint8, device=dev)
+    lbg.evolve_sweep_dev(T(h0), T(hd), T(hs), T(ops), T(delta), T(scale), 0.1, T(rho0), 500, pops, ens, work)
+    torch.cuda.synchronize()
+    p = pops.cpu().numpy()
+    assert np.abs(p.sum(axis=1) - 1.0).max() <= TOL_INV
+    assert p.min() >= -TOL_INV
+    e = ens.cpu().numpy() / B
+    tr, herm = invariants(e)
+    assert tr <= TOL_INV and herm <= TOL_INV
+    assert np.abs(np.diag(e).real - p.mean(axis=0)).max() <= 1e-12
