@@ -1,0 +1,428 @@
+#!/usr/bin/env python
+"""bench.py — B200 Lindblad propagation engine benchmark (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N ...
+
+Headline workload (BASELINE.json configs[1], "c1"): d = 3 transmon with
+leakage, ONE shared P = exp(L dt) (9x9 complex128), 2^20 independent
+trajectories per GPU, 1,000 propagation steps per pass. One bench "step" = one
+pass of the hot path (vec(rho_b) <- P vec(rho_b), 1,000 times, for every
+trajectory). metric = trajectory-steps/s (whole job), FP64 GFLOP/s counted as
+8 d^4 = 648 flops per trajectory-step. Multi-GPU: trajectories shard with no
+data-path collective (weak scaling: each rank owns 2^20 trajectories with
+global ids rank*2^20 + b, so inputs are independent of N).
+
+value: inputs resident in HBM (151 MB state > 126 MB L2, so no L2 flush is
+needed), CUDA events on the launching stream, barrier + synchronize around
+exactly K passes, max over ranks. e2e: the same metric through the host-buffer
+C-ABI call lbg_evolve_shared_p (H2D of rho0 from pinned memory, rho0
+validation, the steps, D2H of the final states) timed per call.
+roofline: FP64 pipe bound; peak = FP64 DMMA/DFMA throughput measured live by
+lbg_fp64_peak() (MEASURED_PEAKS.json has no FP64 figure). cpu_baseline: the
+reference (oracle/_ref/libref.so, compiled from /root/reference sources with
+its native-fast flags) on a bounded sample, all host threads.
+Extra key "configs": the other BASELINE configs (c0 latency, c2 d=9, c3 d=27,
+c4 per-trajectory sweep) measured the same way at N=1.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {  # cfg: (d, batch per GPU, steps)
+    0: (3, 1, 10000),
+    1: (3, 1 << 20, 1000),
+    2: (9, 4096, 1000),
+    3: (27, 1024, 200),
+    4: (9, 65536, 500),
+}
+WORKLOAD = {
+    0: "c0: d=3 single transmon, 1 trajectory x 10,000 steps, complex128 (latency)",
+    1: "c1: d=3 shared P (9x9), 2^20 Ginibre trajectories x 1,000 steps, complex128",
+    2: "c2: d=9 two transmons, shared P (81x81), 4,096 Ginibre trajectories x 1,000 steps",
+    3: "c3: d=27 three transmons, shared P (729x729, 8.5 MB), 1,024 trajectories x 200 steps",
+    4: "c4: d=9 sweep, per-trajectory L/P built on GPU, 65,536 trajectories x 500 steps",
+}
+KERNEL = {0: "chain_kernel", 1: "dfma9_kernel", 2: "smem_kernel", 3: "tiled_evolve_kernel",
+          4: "sweep_step_kernel"}
+
+
+def flops_per_traj_step(d: int) -> int:
+    return 8 * d ** 4
+
+
+class Clocks:
+    """nvidia-smi samples during the timed region (the recipe's clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+def load_traffic():
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f)
+    return {}
+
+
+# --------------------------------------------------------------- reference ---
+def cpu_reference_rate(cfg: int, sample: int, threads: int, reps: int = 1, warmup: int = 0):
+    """traj-steps/s of the unmodified reference (lb::evolve, native-fast SoA)."""
+    from oracle.bindings import Oracle, Reference
+    o, r = Oracle(), Reference()
+    d, _, S = CONFIGS[cfg]
+    if cfg == 4:
+        dl = np.array([o.sweep_params(42, b)[0] for b in range(sample)])
+        sc = np.array([o.sweep_params(42, b)[1] for b in range(sample)])
+        times = []
+        for i in range(warmup + reps):
+            _, _, secs = r.sweep_batch(dl, sc, steps=S, threads=threads)
+            if i >= warmup:
+                times.append(secs)
+        return sample * S / float(np.mean(times)), times
+    P = r.config_propagator(cfg)
+    if cfg == 0:
+        rho0 = np.zeros((1, 3, 3), complex)
+        rho0[0, 0, 0] = 1.0
+    else:
+        rho0 = np.stack([o.ginibre_rho(42, cfg, b, d) for b in range(sample)])
+    times = []
+    for i in range(warmup + reps):
+        _, secs = r.evolve_batch(P, rho0, S, threads=threads)
+        if i >= warmup:
+            times.append(secs)
+    return rho0.shape[0] * S / float(np.mean(times)), times
+
+
+REF_SAMPLE = {0: 1, 1: 65536, 2: 512, 3: 16, 4: 256}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    cfg = args.config
+    d, B, S = CONFIGS[cfg]
+    threads = os.cpu_count() or 1
+    sample = REF_SAMPLE[cfg]
+    value, times = cpu_reference_rate(cfg, sample, threads, reps=args.steps, warmup=args.warmup)
+    ms = float(np.mean(times)) * 1e3
+    line = {
+        "impl": "reference", "metric": "trajectory-steps/s", "value": value, "unit": "traj-steps/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded Ginibre rho0, counter-based RNG seed 42)",
+        "gflops": value * flops_per_traj_step(d) / 1e9,
+        "config": {"workload": WORKLOAD[cfg], "d": d, "batch_per_gpu": B, "steps_per_pass": S,
+                   "sample_trajectories_per_step": sample},
+        "cpu_baseline": {"value": value, "unit": "traj-steps/s", "cores": threads, "kind": "reference",
+                         "sample": f"{sample} trajectories x {S} steps per bench step through lb::evolve "
+                                   f"(native-fast SoA), {threads} std::threads"},
+        "e2e": {"value": value, "unit": "traj-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------- ours ---
+class Runner:
+    def __init__(self, torch, lbg, dev, rank):
+        self.torch, self.lbg, self.dev, self.rank = torch, lbg, dev, rank
+        self.stream = torch.cuda.current_stream(dev)
+
+    def propagator(self, cfg):
+        h, ops = self.lbg.config_model(cfg)
+        return self.lbg.expm(self.lbg.build_lindbladian(h, ops), 0.1)
+
+    def shared_p_setup(self, cfg, B):
+        d, _, S = CONFIGS[cfg]
+        T = self.torch
+        P = self.propagator(cfg)
+        if cfg == 0:
+            rho0 = np.zeros((1, 3, 3), complex)
+            rho0[0, 0, 0] = 1.0
+        else:
+            rho0 = self.lbg.ginibre_batch(cfg, self.rank * B, B, d)
+        pt = T.from_numpy(P).to(self.dev)
+        xt = T.from_numpy(rho0.reshape(B, d * d)).to(self.dev)
+        ws = self.lbg.evolve_workspace(d * d, B)
+        work = T.empty(max(ws, 1), dtype=T.uint8, device=self.dev)
+        return P, rho0, pt, xt, work
+
+    def time_passes(self, fn, K, W):
+        T = self.torch
+        for _ in range(W):
+            fn()
+        T.cuda.synchronize(self.dev)
+        if T.distributed.is_initialized():
+            T.distributed.barrier()
+        evs = [T.cuda.Event(enable_timing=True) for _ in range(K + 1)]
+        self.lbg.reset_launch_count()
+        evs[0].record(self.stream)
+        for k in range(K):
+            fn()
+            evs[k + 1].record(self.stream)
+        T.cuda.synchronize(self.dev)
+        launches = self.lbg.launch_count()
+        if T.distributed.is_initialized():
+            T.distributed.barrier()
+        per = [evs[k].elapsed_time(evs[k + 1]) for k in range(K)]
+        total = evs[0].elapsed_time(evs[K])
+        return total, per, launches
+
+
+def max_over_ranks(torch, x: float) -> float:
+    if torch.distributed.is_initialized():
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+    return x
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2603_18052_b200 as lbg
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1 and not torch.distributed.is_initialized():
+        torch.distributed.init_process_group("nccl", device_id=dev)
+    lbg.lib()
+    R = Runner(torch, lbg, dev, rank)
+    cfg = args.config
+    d, B, S = CONFIGS[cfg]
+    K, W = args.steps, args.warmup
+    dmma_peak, dfma_peak = lbg.fp64_peak()
+    peak = max(dmma_peak, dfma_peak)
+    traffic = load_traffic()
+
+    # ---- device-resident timed region -----------------------------------
+    if cfg == 4:
+        sweep = SweepCase(torch, lbg, dev, rank, B)
+        fn = sweep.run
+    else:
+        P, rho0, pt, xt, work = R.shared_p_setup(cfg, B)
+        fn = lambda: lbg.evolve_batch_dev(pt, xt, S, work=work, stream=R.stream)  # noqa: E731
+    with Clocks(local) as clk:
+        total_ms, per_ms, launches = R.time_passes(fn, K, W)
+    total_ms = max_over_ranks(torch, total_ms)
+    units = world * B * S * K
+    value = units / (total_ms * 1e-3)
+    ms_step = total_ms / K
+    kernel_ms = float(np.mean(per_ms))
+    achieved = flops_per_traj_step(d) * B * S / (kernel_ms * 1e-3) / 1e12
+
+    # ---- end to end through the host-buffer C-ABI call ---------------------
+    e2e = None
+    if cfg != 4:
+        pin = torch.empty(B * d * d * 2, dtype=torch.float64).pin_memory()
+        host_in = pin.numpy().view(np.complex128).reshape(B, d, d)
+        host_in[...] = rho0
+        pin_out = torch.empty_like(pin).pin_memory()
+        host_out = pin_out.numpy().view(np.complex128).reshape(B, d, d)
+        import ctypes as C
+        L = lbg.lib()
+        dp = C.POINTER(C.c_double)
+        Pc = np.ascontiguousarray(P)
+
+        def call():
+            rc = L.lbg_evolve_shared_p(Pc.ctypes.data_as(dp), d, host_in.ctypes.data_as(dp), B, S,
+                                       host_out.ctypes.data_as(dp), 0)
+            assert rc == 0, L.lbg_last_error()
+        call()
+        reps = max(2, min(K, 5))
+        if torch.distributed.is_initialized():
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            call()
+        e2e_s = max_over_ranks(torch, (time.perf_counter() - t0) / reps)
+        e2e = {"value": world * B * S / e2e_s, "unit": "traj-steps/s",
+               "h2d_bytes_per_step": int(host_in.nbytes + Pc.nbytes), "d2h_bytes_per_step": int(host_out.nbytes),
+               "ms_per_call": e2e_s * 1e3, "call": "lbg_evolve_shared_p (host buffers, synchronous)"}
+    else:
+        e2e = sweep.e2e(reps=2)
+        e2e["value"] = e2e["value"] * world
+
+    line = {
+        "metric": "trajectory-steps/s", "value": value, "unit": "traj-steps/s", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: seeded Ginibre rho0 (counter-based RNG, seed 42), BASELINE config models",
+        "gflops": value * flops_per_traj_step(d) / 1e9,
+        "config": {"workload": WORKLOAD[cfg], "d": d, "batch_per_gpu": B, "global_batch": B * world,
+                   "steps_per_pass": S, "parallelism": f"trajectories sharded over {world} GPU(s), no collective"
+                   if cfg != 4 else f"trajectories sharded over {world} GPU(s), ensemble allreduce",
+                   "l2": "state larger than L2; no flush needed" if cfg == 1 else "working set L2/SMEM resident"},
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic.get(KERNEL[cfg]),
+                     "kernel": KERNEL[cfg],
+                     "peak_source": f"measured live by lbg_fp64_peak(): DMMA {dmma_peak:.2f}, DFMA {dfma_peak:.2f} TF/s "
+                                    "(MEASURED_PEAKS.json has no FP64 entry)",
+                     "flops_per_launch": flops_per_traj_step(d) * B * S, "launch_ms": kernel_ms},
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        try:
+            sample = REF_SAMPLE[cfg]
+            cv, times = cpu_reference_rate(cfg, sample, threads, reps=1, warmup=0)
+            line["cpu_baseline"] = {"value": cv, "unit": "traj-steps/s", "cores": threads, "kind": "reference",
+                                    "sample": f"{sample} trajectories x {S} steps through lb::evolve "
+                                              f"(native-fast SoA), {threads} std::threads, {times[0]:.2f} s"}
+        except Exception as e:  # noqa: BLE001
+            line["cpu_baseline"] = {"value": None, "unit": "traj-steps/s", "cores": threads, "kind": "reference",
+                                    "sample": f"unavailable: {e}"}
+
+    if rank == 0 and world == 1 and not args.no_extra and args.config == 1:
+        line["configs"] = extra_configs(torch, lbg, R, peak)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if torch.distributed.is_initialized():
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+class SweepCase:
+    """Config 4 through lbg_evolve_sweep_dev (+ NCCL allreduce of the ensemble sum)."""
+
+    def __init__(self, torch, lbg, dev, rank, B):
+        self.torch, self.lbg, self.dev, self.B = torch, lbg, dev, B
+        T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+        h0, hd, hs = lbg.config_sweep_terms()
+        _, ops = lbg.config_model(4)
+        delta, scale = lbg.sweep_params(rank * B, B)
+        rho0 = np.zeros((9, 9), complex)
+        rho0[0, 0] = 1.0
+        self.host = (h0, hd, hs, ops, delta, scale, rho0)
+        self.args = [T(h0), T(hd), T(hs), T(ops), T(delta), T(scale), 0.1, T(rho0), CONFIGS[4][2]]
+        self.pops = torch.zeros(B, 9, dtype=torch.float64, device=dev)
+        self.ens = torch.zeros(9, 9, dtype=torch.complex128, device=dev)
+        self.work = torch.empty(lbg.sweep_workspace(9, B), dtype=torch.uint8, device=dev)
+
+    def run(self):
+        self.lbg.evolve_sweep_dev(*self.args, self.pops, self.ens, self.work)
+        if self.torch.distributed.is_initialized():
+            self.torch.distributed.all_reduce(self.ens)
+
+    def e2e(self, reps=2):
+        T, dev = self.torch, self.dev
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            args = [T.from_numpy(np.ascontiguousarray(a)).to(dev) for a in self.host]
+            self.lbg.evolve_sweep_dev(*args[:6], 0.1, args[6], CONFIGS[4][2], self.pops, self.ens, self.work)
+            pops = self.pops.cpu()
+            ens = self.ens.cpu()
+        s = (time.perf_counter() - t0) / reps
+        h2d = sum(a.nbytes for a in self.host)
+        return {"value": self.B * CONFIGS[4][2] / s, "unit": "traj-steps/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(pops.numel() * 8 + ens.numel() * 16), "ms_per_call": s * 1e3,
+                "call": "lbg_evolve_sweep_dev (host inputs copied in, populations + ensemble copied out)"}
+
+
+def extra_configs(torch, lbg, R, peak):
+    out = {}
+    for cfg in (0, 2, 3, 4):
+        d, B, S = CONFIGS[cfg]
+        try:
+            if cfg == 4:
+                case = SweepCase(torch, lbg, R.dev, 0, B)
+                total, per, launches = R.time_passes(case.run, 3, 1)
+            else:
+                _, _, pt, xt, work = R.shared_p_setup(cfg, B)
+                total, per, launches = R.time_passes(
+                    lambda: lbg.evolve_batch_dev(pt, xt, S, work=work, stream=R.stream), 3 if cfg else 5, 1)
+            ms = total / len(per)
+            rate = B * S / (ms * 1e-3)
+            tf = rate * flops_per_traj_step(d) / 1e12
+            entry = {"workload": WORKLOAD[cfg], "value": rate, "unit": "traj-steps/s", "ms_per_pass": ms,
+                     "gflops": tf * 1e3, "kernel": KERNEL[cfg], "gpu_launches_per_pass": launches // len(per)}
+            if cfg == 0:
+                entry["ns_per_step"] = ms * 1e6 / S
+                entry["bound"] = "latency (one dependent chain; no throughput roofline)"
+            else:
+                entry["roofline"] = {"bound": "fp64", "achieved": tf, "peak": peak, "unit": "TFLOP/s",
+                                     "frac": tf / peak}
+            if cfg == 4:
+                entry["note"] = "includes per-trajectory GPU assembly + expm (not counted in flops)"
+            out[f"c{cfg}"] = entry
+        except Exception as e:  # noqa: BLE001
+            out[f"c{cfg}"] = {"error": str(e)}
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=1, choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-extra", action="store_true", help="skip the other configs")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -156,6 +156,10 @@ int lbg_ginibre_batch(uint64_t seed, uint32_t cfg, uint64_t first, int64_t count
 int lbg_sweep_params_batch(uint64_t seed, uint64_t first, int64_t count, double* delta,
                            double* scale);
 
+/* FP64 roofline denominators measured live on the current device (TF/s):
+ * register-only DMMA (m8n8k4 f64) and DFMA loops over every SM. */
+int lbg_fp64_peak(double* dmma_tflops, double* dfma_tflops);
+
 /* Number of kernels this thread launched since the last reset (evidence for
  * bench.py's gpu_launches). */
 int64_t lbg_launch_count(void);

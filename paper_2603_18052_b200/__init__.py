@@ -127,6 +127,15 @@ def _sp(stream):
     return C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
 
 
+def fp64_peak() -> tuple[float, float]:
+    """(DMMA, DFMA) FP64 TF/s measured live on the current device."""
+    a, b = C.c_double(), C.c_double()
+    L = lib()
+    L.lbg_fp64_peak.argtypes = [_dp, _dp]
+    _check(L.lbg_fp64_peak(C.byref(a), C.byref(b)), "fp64_peak")
+    return a.value, b.value
+
+
 def launch_count() -> int:
     return int(lib().lbg_launch_count())
 

@@ -32,12 +32,16 @@ struct AFragLane {
   int di;      // complex row offset within the m8 tile: lane >> 3        (0..3)
   int dj;      // complex col offset within the k4 step: (lane & 3) >> 1 (0..1)
   int comp;    // which double of the complex: ((lane >> 2) ^ lane) & 1
-  double sgn;  // -1 for (row re, col im), else +1
+  unsigned hi_xor;  // 0x80000000 for (row re, col im): flips the sign bit (integer pipe)
   __device__ __forceinline__ AFragLane(int lane) {
     di = lane >> 3;
     dj = (lane & 3) >> 1;
     comp = ((lane >> 2) ^ lane) & 1;
-    sgn = (((lane >> 2) & 1) == 0 && (lane & 1) == 1) ? -1.0 : 1.0;
+    hi_xor = (((lane >> 2) & 1) == 0 && (lane & 1) == 1) ? 0x80000000u : 0u;
+  }
+  // apply the fragment sign without touching the FP64 pipe
+  __device__ __forceinline__ double sign(double x) const {
+    return __hiloint2double(__double2hiint(x) ^ int(hi_xor), __double2loint(x));
   }
 };
 

@@ -23,14 +23,16 @@ namespace {
 constexpr int kSlots = 8;
 __constant__ double2 c_p9[kSlots][81];
 
-template <Layout L>
+// SLOT is a template parameter so every P operand is a compile-time constant
+// bank address (c[0x3][imm]) and ptxas keeps it out of the register file.
+template <int SLOT, Layout L>
 __global__ void __launch_bounds__(128) dfma9_kernel(double* __restrict__ x_re,
                                                     double* __restrict__ x_im,
                                                     double* __restrict__ x_aos, int64_t batch,
-                                                    int64_t steps, int slot) {
+                                                    int64_t steps) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= batch) return;
-  const double2* __restrict__ p = c_p9[slot];
+  const double2* __restrict__ p = c_p9[SLOT];
   double vr[9], vi[9];
 #pragma unroll
   for (int j = 0; j < 9; ++j) {
@@ -108,10 +110,17 @@ void launch_dfma9(const double* /*unused*/, const double* p_dev, double* x_re, d
              "P -> constant bank");
   const int threads = 128;
   const unsigned blocks = static_cast<unsigned>((batch + threads - 1) / threads);
-  if (layout == Layout::soa)
-    dfma9_kernel<Layout::soa><<<blocks, threads, 0, s>>>(x_re, x_im, nullptr, batch, steps, slot);
-  else
-    dfma9_kernel<Layout::aos><<<blocks, threads, 0, s>>>(nullptr, nullptr, x_aos, batch, steps, slot);
+  switch (slot) {
+#define LBG_SLOT(S)                                                                               \
+  case S:                                                                                         \
+    if (layout == Layout::soa)                                                                    \
+      dfma9_kernel<S, Layout::soa><<<blocks, threads, 0, s>>>(x_re, x_im, nullptr, batch, steps); \
+    else                                                                                          \
+      dfma9_kernel<S, Layout::aos><<<blocks, threads, 0, s>>>(nullptr, nullptr, x_aos, batch, steps); \
+    break;
+    LBG_SLOT(0) LBG_SLOT(1) LBG_SLOT(2) LBG_SLOT(3) LBG_SLOT(4) LBG_SLOT(5) LBG_SLOT(6) LBG_SLOT(7)
+#undef LBG_SLOT
+  }
   LBG_CHECK_LAUNCH("dfma9_kernel");
   check_cuda(cudaEventRecord(sp.ev[slot], s), "event record");
 }

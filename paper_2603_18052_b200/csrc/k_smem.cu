@@ -41,12 +41,15 @@ struct SmemGeom {
   }
 };
 
-template <int MG, Layout L>
+// N > 0: n known at compile time (config 2 uses N = 81: no tile predicates,
+// fully unrolled k loop); N == 0: runtime n.
+template <int N, int MG, Layout L>
 __global__ void __launch_bounds__(32 * kWarps, 1)
-    smem_kernel(const double2* __restrict__ p, int n, double* __restrict__ x_re,
+    smem_kernel(const double2* __restrict__ p, int n_rt, double* __restrict__ x_re,
                 double* __restrict__ x_im, double* __restrict__ x_aos, int64_t batch,
                 int64_t steps) {
   extern __shared__ __align__(16) unsigned char smem[];
+  const int n = N > 0 ? N : n_rt;
   const SmemGeom g(n);
   double2* ps = reinterpret_cast<double2*>(smem);
   double* va = reinterpret_cast<double*>(smem + g.p_bytes);
@@ -81,33 +84,49 @@ __global__ void __launch_bounds__(32 * kWarps, 1)
   const int m_begin = mg * MG;
   const int bn = nt * 8 + (lane >> 2);  // B fragment column (trajectory in CTA)
   const int bk = lane & 3;              // B fragment k within the step
+  // per-lane A fragment base (doubles) and per-m-tile stride
+  const double* pa = reinterpret_cast<const double*>(ps) + size_t(m_begin * 4 + af.di) * 2 * g.sp +
+                     2 * af.dj + af.comp;
+  const int mstride = 4 * 2 * g.sp;
+  int mcount = g.mt - m_begin;
+  mcount = mcount < 0 ? 0 : (mcount > MG ? MG : mcount);
 
   for (int64_t s = 0; s < steps; ++s) {
     double acc[MG][2];
 #pragma unroll
     for (int mi = 0; mi < MG; ++mi) acc[mi][0] = acc[mi][1] = 0.0;
     const double* vrow = va + bn * g.sv + bk;
-#pragma unroll 2
-    for (int ks = 0; ks < g.kt; ++ks) {
-      const double bfrag = vrow[ks * 4];
-      const double* pcol = reinterpret_cast<const double*>(ps) + 2 * (ks * 2 + af.dj) + af.comp;
+    // register double buffer: fragments of step ks+1 load while ks computes
+    double a_cur[MG], b_cur;
+    b_cur = vrow[0];
 #pragma unroll
-      for (int mi = 0; mi < MG; ++mi) {
-        const int mt = m_begin + mi;
-        if (mt < g.mt) {
-          const double afrag = af.sgn * pcol[size_t(mt * 4 + af.di) * 2 * g.sp];
-          dmma(acc[mi], afrag, bfrag);
-        }
+    for (int mi = 0; mi < MG; ++mi) a_cur[mi] = (N > 0 || mi < mcount) ? af.sign(pa[mi * mstride]) : 0.0;
+#pragma unroll(N > 0 ? 41 : 1)
+    for (int ks = 0; ks < g.kt; ++ks) {
+      double a_nxt[MG], b_nxt = 0.0;
+      const bool more = ks + 1 < g.kt;
+      if (more) {
+        b_nxt = vrow[(ks + 1) * 4];
+#pragma unroll
+        for (int mi = 0; mi < MG; ++mi)
+          a_nxt[mi] = (N > 0 || mi < mcount) ? af.sign(pa[mi * mstride + 4 * (ks + 1)]) : 0.0;
+      }
+#pragma unroll
+      for (int mi = 0; mi < MG; ++mi)
+        if (N > 0 || mi < mcount) dmma(acc[mi], a_cur[mi], b_cur);
+      if (more) {
+        b_cur = b_nxt;
+#pragma unroll
+        for (int mi = 0; mi < MG; ++mi) a_cur[mi] = a_nxt[mi];
       }
     }
     // epilogue: complex-pair the fragments and write V_next (real form)
 #pragma unroll
     for (int mi = 0; mi < MG; ++mi) {
-      const int mt = m_begin + mi;
-      if (mt < g.mt) {
+      if (N > 0 || mi < mcount) {
         int coff;
         const double2 z = pair_complex(acc[mi], lane, coff);
-        const int i = mt * 4 + (lane >> 3);
+        const int i = (m_begin + mi) * 4 + (lane >> 3);
         const int t = nt * 8 + coff;
         if (i < n) *reinterpret_cast<double2*>(vb + t * g.sv + 2 * i) = z;
       }
@@ -135,19 +154,19 @@ __global__ void __launch_bounds__(32 * kWarps, 1)
   }
 }
 
-template <int MG>
+template <int N, int MG>
 void launch_mg(const double* p, int n, double* x_re, double* x_im, double* x_aos, int64_t batch,
                int64_t steps, Layout layout, cudaStream_t s) {
   const SmemGeom g(n);
   const unsigned blocks = static_cast<unsigned>((batch + kTraj - 1) / kTraj);
   const double2* p2 = reinterpret_cast<const double2*>(p);
   if (layout == Layout::soa) {
-    auto k = smem_kernel<MG, Layout::soa>;
+    auto k = smem_kernel<N, MG, Layout::soa>;
     check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(g.total)),
                "smem attr");
     k<<<blocks, 32 * kWarps, g.total, s>>>(p2, n, x_re, x_im, nullptr, batch, steps);
   } else {
-    auto k = smem_kernel<MG, Layout::aos>;
+    auto k = smem_kernel<N, MG, Layout::aos>;
     check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(g.total)),
                "smem attr");
     k<<<blocks, 32 * kWarps, g.total, s>>>(p2, n, nullptr, nullptr, x_aos, batch, steps);
@@ -163,11 +182,12 @@ void launch_smem(const double* p_dev, std::size_t n, double* x_re, double* x_im,
                  int64_t batch, int64_t steps, Layout layout, cudaStream_t s) {
   if (batch <= 0) return;
   if (!smem_supported(n)) throw invalid_argument("smem kernel supports n <= 84");
+  if (n == 81) return launch_mg<81, 7>(p_dev, 81, x_re, x_im, x_aos, batch, steps, layout, s);
   const int mt = (int(n) + 3) / 4;
   const int mg = (mt + 2) / 3;
   switch (mg) {
 #define LBG_CASE(M) \
-  case M: return launch_mg<M>(p_dev, int(n), x_re, x_im, x_aos, batch, steps, layout, s);
+  case M: return launch_mg<0, M>(p_dev, int(n), x_re, x_im, x_aos, batch, steps, layout, s);
     LBG_CASE(1) LBG_CASE(2) LBG_CASE(3) LBG_CASE(4) LBG_CASE(5) LBG_CASE(6) LBG_CASE(7)
 #undef LBG_CASE
     default: throw invalid_argument("smem kernel: n too large");

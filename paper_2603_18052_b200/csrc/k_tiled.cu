@@ -98,7 +98,7 @@ __device__ __forceinline__ void gemm_tile(const double2* __restrict__ A, long lo
     for (int ks = 0; ks < BK / 2; ++ks) {
       double a[2], b[2];
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi) a[mi] = c.af.sgn * ad[2 * (mi * 4 * SA) + 4 * ks];
+      for (int mi = 0; mi < 2; ++mi) a[mi] = c.af.sign(ad[2 * (mi * 4 * SA) + 4 * ks]);
 #pragma unroll
       for (int ni = 0; ni < 2; ++ni) b[ni] = bd[2 * (2 * ks * SB + ni * 8)];
 #pragma unroll
