@@ -55,7 +55,7 @@ WORKLOAD = {
     4: "c4: d=9 sweep, per-trajectory L/P built on GPU, 65,536 trajectories x 500 steps",
 }
 KERNEL = {0: "chain_kernel", 1: "dfma9_kernel", 2: "smem_kernel", 3: "tiled_evolve_kernel",
-          4: "sweep_step_kernel"}
+          4: "ptm_expm_kernel+ptm_step_kernel"}
 
 
 def flops_per_traj_step(d: int) -> int:
@@ -344,8 +344,8 @@ def run_ours(args):
 class SweepCase:
     """Config 4 through lbg_evolve_sweep_dev (+ NCCL allreduce of the ensemble sum)."""
 
-    def __init__(self, torch, lbg, dev, rank, B):
-        self.torch, self.lbg, self.dev, self.B = torch, lbg, dev, B
+    def __init__(self, torch, lbg, dev, rank, B, mode="auto"):
+        self.torch, self.lbg, self.dev, self.B, self.mode = torch, lbg, dev, B, mode
         T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
         h0, hd, hs = lbg.config_sweep_terms()
         _, ops = lbg.config_model(4)
@@ -359,7 +359,7 @@ class SweepCase:
         self.work = torch.empty(lbg.sweep_workspace(9, B), dtype=torch.uint8, device=dev)
 
     def run(self):
-        self.lbg.evolve_sweep_dev(*self.args, self.pops, self.ens, self.work)
+        self.lbg.evolve_sweep_dev(*self.args, self.pops, self.ens, self.work, mode=self.mode)
         if self.torch.distributed.is_initialized():
             self.torch.distributed.all_reduce(self.ens)
 
@@ -368,7 +368,8 @@ class SweepCase:
         t0 = time.perf_counter()
         for _ in range(reps):
             args = [T.from_numpy(np.ascontiguousarray(a)).to(dev) for a in self.host]
-            self.lbg.evolve_sweep_dev(*args[:6], 0.1, args[6], CONFIGS[4][2], self.pops, self.ens, self.work)
+            self.lbg.evolve_sweep_dev(*args[:6], 0.1, args[6], CONFIGS[4][2], self.pops, self.ens, self.work,
+                                      mode=self.mode)
             pops = self.pops.cpu()
             ens = self.ens.cpu()
         s = (time.perf_counter() - t0) / reps
@@ -402,7 +403,14 @@ def extra_configs(torch, lbg, R, peak):
                 entry["roofline"] = {"bound": "fp64", "achieved": tf, "peak": peak, "unit": "TFLOP/s",
                                      "frac": tf / peak}
             if cfg == 4:
-                entry["note"] = "includes per-trajectory GPU assembly + expm (not counted in flops)"
+                entry["note"] = ("real transfer-matrix mode (L_R = T L T^-1, 4x fewer executed flops than "
+                                 "8 d^4); includes per-trajectory GPU assembly + expm (not counted in flops)")
+                entry["roofline"]["executed_tflops"] = tf / 4.0
+                case = SweepCase(torch, lbg, R.dev, 0, B, mode="complex")
+                total, per, _ = R.time_passes(case.run, 2, 1)
+                msc = total / len(per)
+                entry["complex_mode"] = {"value": B * S / (msc * 1e-3), "ms_per_pass": msc,
+                                         "note": "reference-form complex d^2 x d^2 matrices (k_sweep.cu)"}
             out[f"c{cfg}"] = entry
         except Exception as e:  # noqa: BLE001
             out[f"c{cfg}"] = {"error": str(e)}

@@ -106,12 +106,21 @@ int lbg_evolve_shared_p(const double* p, size_t d, const double* rho0, int64_t b
  * Outputs: pops[b*d + i] = Re rho_b[i][i]; ens_sum (d*d AoS) += sum_b rho_b.
  * Replaces, per trajectory, the make_model + build_lindbladian + expm + step
  * sequence of lb::grape_chain (propagate.cpp:130-160). Device pointers.
+ * mode: LBG_SWEEP_REAL propagates the real coordinates of the (Hermitian)
+ * density matrix with the real d^2 x d^2 representation L_R = T L T^-1 of the
+ * same generator (P_R = T P T^-1; 4x fewer flops; d == 9; rho0 must be exactly
+ * Hermitian — checked, one 81-element D2H). LBG_SWEEP_COMPLEX uses the
+ * complex d^2 x d^2 matrices exactly as the reference does. AUTO = REAL when
+ * it applies, else COMPLEX.
  * ------------------------------------------------------------------------ */
+#define LBG_SWEEP_AUTO 0
+#define LBG_SWEEP_COMPLEX 1
+#define LBG_SWEEP_REAL 2
 size_t lbg_sweep_workspace(size_t d, int64_t batch);
 int lbg_evolve_sweep_dev(size_t d, const double* h0, const double* hd, const double* hs,
                          size_t n_ops, const double* ops, const double* delta,
                          const double* scale, double dt, const double* rho0, int64_t batch,
-                         int64_t steps, double* pops, double* ens_sum, void* work,
+                         int64_t steps, double* pops, double* ens_sum, int mode, void* work,
                          void* stream);
 
 /* ------------------------------------------------------------------------

@@ -39,6 +39,7 @@ LIB_PATH = os.path.join(HERE, "liblbg.so")
 SEED = 42  # lb::kDefaultSeed (proj/include/lb/random.hpp:10)
 
 ALGO = {"auto": 0, "chain": 1, "dfma9": 2, "smem": 3, "tiled": 4}
+SWEEP_MODE = {"auto": 0, "complex": 1, "real": 2}
 
 _dp = C.POINTER(C.c_double)
 _sz = C.c_size_t
@@ -79,7 +80,7 @@ def lib() -> C.CDLL:
     L.lbg_sweep_workspace.argtypes = [_sz, C.c_int64]
     L.lbg_sweep_workspace.restype = _sz
     L.lbg_evolve_sweep_dev.argtypes = [_sz, vp, vp, vp, _sz, vp, vp, vp, C.c_double, vp, C.c_int64,
-                                       C.c_int64, vp, vp, vp, vp]
+                                       C.c_int64, vp, vp, C.c_int, vp, vp]
     L.lbg_check_state_batched_dev.argtypes = [vp, _sz, C.c_int64, vp, vp]
     L.lbg_allreduce_sum_dev.argtypes = [vp, _sz, vp, vp]
     L.lbg_nccl_unique_id.argtypes = [vp]
@@ -272,12 +273,18 @@ def sweep_workspace(d: int, batch: int) -> int:
     return int(lib().lbg_sweep_workspace(d, batch))
 
 
-def evolve_sweep_dev(h0, hd, hs, ops, delta, scale, dt, rho0, n_steps, pops, ens_sum, work, stream=None):
-    """Config-4 sweep on device tensors (see include/lbg.h lbg_evolve_sweep_dev)."""
+def evolve_sweep_dev(h0, hd, hs, ops, delta, scale, dt, rho0, n_steps, pops, ens_sum, work, stream=None,
+                     mode: str = "auto"):
+    """Config-4 sweep on device tensors (see include/lbg.h lbg_evolve_sweep_dev).
+
+    mode "real": real d^2 x d^2 representation of the same generator (4x fewer
+    flops); "complex": the reference's complex matrices; "auto": real when rho0
+    is exactly Hermitian and d == 9."""
     d = h0.shape[0]
     _check(lib().lbg_evolve_sweep_dev(d, _tp(h0), _tp(hd), _tp(hs), ops.shape[0], _tp(ops), _tp(delta),
                                       _tp(scale), float(dt), _tp(rho0), delta.shape[0], int(n_steps),
-                                      _tp(pops), _tp(ens_sum), _tp(work), _sp(stream)), "evolve_sweep_dev")
+                                      _tp(pops), _tp(ens_sum), SWEEP_MODE[mode], _tp(work), _sp(stream)),
+           "evolve_sweep_dev")
 
 
 def check_state_batched_dev(x, d: int, out3, stream=None):

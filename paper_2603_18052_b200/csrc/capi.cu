@@ -283,20 +283,46 @@ int lbg_evolve_shared_p(const double* p, size_t d, const double* rho0, int64_t b
 }
 
 // ---- per-trajectory sweep (config 4) ----
-size_t lbg_sweep_workspace(size_t d, int64_t batch) { return sweep_workspace(d, batch); }
+size_t lbg_sweep_workspace(size_t d, int64_t batch) {
+  const size_t c = sweep_workspace(d, batch);
+  return ptm_sweep_supported(d) ? std::max(c, ptm_sweep_workspace(batch)) : c;
+}
 
 int lbg_evolve_sweep_dev(size_t d, const double* h0, const double* hd, const double* hs, size_t n_ops,
                          const double* ops, const double* delta, const double* scale, double dt,
                          const double* rho0, int64_t batch, int64_t steps, double* pops,
-                         double* ens_sum, void* work, void* stream) {
+                         double* ens_sum, int mode, void* work, void* stream) {
   return guarded([&] {
     if (d == 0) throw invalid_argument("sweep: dimension must be positive");
     if (batch < 0 || steps < 0) throw invalid_argument("sweep: negative batch or steps");
     if (!std::isfinite(dt)) throw invalid_argument("sweep: dt must be finite");
     if (!h0 || !hd || !hs || !delta || !scale || !rho0 || !pops || !ens_sum || (n_ops && !ops))
       throw invalid_argument("sweep: null pointer");
-    launch_sweep(d, h0, hd, hs, n_ops, ops, delta, scale, dt, rho0, batch, steps, pops, ens_sum, work,
-                 as_stream(stream));
+    if (!work) throw invalid_argument("sweep: workspace required");
+    cudaStream_t s = as_stream(stream);
+    bool real = false;
+    if (mode == LBG_SWEEP_REAL || mode == LBG_SWEEP_AUTO) {
+      bool herm = false;
+      if (ptm_sweep_supported(d)) {  // the real representation needs an exactly Hermitian rho0
+        std::vector<double> r(2 * d * d);
+        check_cuda(cudaMemcpyAsync(r.data(), rho0, r.size() * 8, cudaMemcpyDeviceToHost, s), "D2H rho0");
+        check_cuda(cudaStreamSynchronize(s), "sync");
+        herm = true;
+        for (size_t i = 0; i < d; ++i)
+          for (size_t j = 0; j < d; ++j)
+            herm = herm && r[2 * (i * d + j)] == r[2 * (j * d + i)] &&
+                   r[2 * (i * d + j) + 1] == -r[2 * (j * d + i) + 1];
+      }
+      if (mode == LBG_SWEEP_REAL && !herm)
+        throw invalid_argument("sweep: real mode needs d == 9 and an exactly Hermitian rho0");
+      real = herm;
+    } else if (mode != LBG_SWEEP_COMPLEX) {
+      throw invalid_argument("sweep: unknown mode");
+    }
+    if (real)
+      launch_ptm_sweep(d, h0, hd, hs, n_ops, ops, delta, scale, dt, rho0, batch, steps, pops, ens_sum, work, s);
+    else
+      launch_sweep(d, h0, hd, hs, n_ops, ops, delta, scale, dt, rho0, batch, steps, pops, ens_sum, work, s);
   });
 }
 

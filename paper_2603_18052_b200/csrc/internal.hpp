@@ -73,6 +73,14 @@ void launch_sweep(std::size_t d, const double* h0, const double* hd, const doubl
                   double dt, const double* rho0, int64_t batch, int64_t steps, double* pops,
                   double* ens_sum, void* work, cudaStream_t s);
 
+// config 4 in the real (transfer-matrix) representation (k_ptm.cu)
+bool ptm_sweep_supported(std::size_t d);
+std::size_t ptm_sweep_workspace(int64_t batch);
+void launch_ptm_sweep(std::size_t d, const double* h0, const double* hd, const double* hs,
+                      std::size_t n_ops, const double* ops, const double* delta, const double* scale,
+                      double dt, const double* rho0, int64_t batch, int64_t steps, double* pops,
+                      double* ens_sum, void* work, cudaStream_t s);
+
 int sm_count();
 
 }  // namespace lbg

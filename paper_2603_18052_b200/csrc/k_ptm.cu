@@ -1,0 +1,355 @@
+// k_ptm.cu — config 4 in the real (transfer-matrix) representation.
+//
+// A Lindbladian maps Hermitian matrices to Hermitian matrices, so on the real
+// coordinates of a density matrix
+//     x[i*d+j] = Re rho_ij (i <= j),   x[i*d+j] = Im rho_ji = -Im rho_ij (i > j)
+// (the same index space as row-major vec(rho)) it acts as a REAL d^2 x d^2
+// matrix L_R = T L T^-1, and P_R = exp(L_R dt) = T P T^-1 is the same
+// propagator as the reference's complex P = exp(L dt) in another basis. With
+// n = d^2:
+//   L_R[q][s] = f_q( c_qs ),  c_qs = L[q][s]                    (s diagonal)
+//                                  = L[q][s] + L[q][s^T]         (s upper)
+//                                  = i (L[q][s^T] - L[q][s])     (s lower)
+//   f_q = Re for q upper/diagonal, -Im for q lower;  s^T = transposed index.
+// Every L entry comes from the Kronecker formula of lindblad.cpp:37-59 (K5),
+// so the assembly is elementwise. A real n x n matmul is 4x fewer FMAs than
+// the complex one, and a step is n^2 real FMAs instead of 4 n^2.
+//
+// K4 (ptm_expm_kernel): one CTA per trajectory; A_R = dt L_R assembled into
+//   shared memory; Taylor degree 14 in Paterson-Stockmeyer form (s = 3:
+//   A2, A3, then 4 Horner products in A3; 6 real DMMA matmuls, no solve;
+//   truncation <= 2^-54 for ||A||_1 <= 0.53, scaling and squaring otherwise);
+//   three 88x92 padded matrices in shared memory, A and A^2 also kept at each
+//   thread's own accumulator positions so the Horner epilogues never re-read
+//   them. Writes P_R (n x n) to global memory.
+// K3 (ptm_step_kernel): one CTA per trajectory; P_R register resident (each
+//   thread a 2-row x 11-column block), x in shared memory; per step 22 FMAs,
+//   3-level shuffle reduction, one barrier. Epilogue: populations + ensemble sum.
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+#include "internal.hpp"
+
+namespace lbg {
+namespace {
+
+constexpr int D = 9, N = 81;          // config 4 size
+constexpr int MT = 11, KT = 21;       // 8-row m/n tiles (88), 4-wide k steps (84)
+constexpr int RS = 92;                // smem row stride: 92 = 12 (mod 16) -> conflict free
+constexpr int MAT = 88 * RS;          // doubles per padded matrix
+constexpr int WARPS = 11, THREADS = 32 * WARPS;
+constexpr double kTheta14 = 0.53;
+
+__device__ __forceinline__ double2 kron_l(const double2* __restrict__ dis, const double2* __restrict__ h,
+                                          int q, int p) {
+  // L[q][p] = D[q][p] - i (H[i][j] d_kl - d_ij H[l][k]),  q = (i,k), p = (j,l)
+  const int i = q / D, k = q - i * D, j = p / D, l = p - j * D;
+  double2 v = dis[q * N + p];
+  if (k == l) {
+    const double2 a = h[i * D + j];
+    v.x += a.y;
+    v.y -= a.x;
+  }
+  if (i == j) {
+    const double2 a = h[l * D + k];
+    v.x -= a.y;
+    v.y += a.x;
+  }
+  return v;
+}
+
+// acc[m][0..1] = (X * Y)[m*8 + g][w*8 + 2t .. +1], X, Y padded 88 x RS
+__device__ __forceinline__ void mm(const double* __restrict__ X, const double* __restrict__ Y,
+                                   double (&acc)[MT][2], int w, int lane) {
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = 0.0;
+  const double* xa = X + g * RS + t;
+  const double* yb = Y + t * RS + w * 8 + g;
+  double a_cur[MT], b_cur = yb[0];
+#pragma unroll
+  for (int m = 0; m < MT; ++m) a_cur[m] = xa[m * 8 * RS];
+#pragma unroll
+  for (int k = 0; k < KT; ++k) {
+    double a_nxt[MT], b_nxt = 0.0;
+    if (k + 1 < KT) {
+      b_nxt = yb[(k + 1) * 4 * RS];
+#pragma unroll
+      for (int m = 0; m < MT; ++m) a_nxt[m] = xa[m * 8 * RS + (k + 1) * 4];
+    }
+#pragma unroll
+    for (int m = 0; m < MT; ++m) dmma(acc[m], a_cur[m], b_cur);
+    if (k + 1 < KT) {
+      b_cur = b_nxt;
+#pragma unroll
+      for (int m = 0; m < MT; ++m) a_cur[m] = a_nxt[m];
+    }
+  }
+}
+
+__device__ __forceinline__ void store(double* __restrict__ Z, const double (&v)[MT][2], int w, int lane) {
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int m = 0; m < MT; ++m)
+    *reinterpret_cast<double2*>(Z + (m * 8 + g) * RS + w * 8 + 2 * t) = make_double2(v[m][0], v[m][1]);
+}
+
+// acc = acc + c0 I + c1 a1 + c2 a2 at own positions (in place); zero in the padding
+__device__ __forceinline__ void horner_epilogue(double (&acc)[MT][2],
+                                                const double (&a1)[MT][2], const double (&a2)[MT][2],
+                                                double c0, double c1, double c2, int w, int lane,
+                                                bool with_acc) {
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int m = 0; m < MT; ++m)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int r = m * 8 + g, col = w * 8 + 2 * t + c;
+      double x = (with_acc ? acc[m][c] : 0.0) + c1 * a1[m][c] + c2 * a2[m][c];
+      if (r == col) x += c0;
+      acc[m][c] = (r < N && col < N) ? x : 0.0;
+    }
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    ptm_expm_kernel(const double2* __restrict__ dis, const double2* __restrict__ h0,
+                    const double2* __restrict__ hd, const double2* __restrict__ hs,
+                    const double* __restrict__ delta, const double* __restrict__ scale, double dt,
+                    double* __restrict__ p_out) {
+  extern __shared__ __align__(16) double sm[];
+  double* S0 = sm;
+  double* S1 = sm + MAT;
+  double* S2 = sm + 2 * MAT;
+  __shared__ double2 hb[D * D];
+  __shared__ double colsum[88];
+  __shared__ int s_sq;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int b = blockIdx.x;
+  const double db = delta[b], sb = scale[b];
+  for (int e = tid; e < D * D; e += THREADS)
+    hb[e] = make_double2(h0[e].x + db * hd[e].x + sb * hs[e].x, h0[e].y + db * hd[e].y + sb * hs[e].y);
+  for (int e = tid; e < 3 * MAT; e += THREADS) sm[e] = 0.0;
+  __syncthreads();
+  // ---- K5: A_R = L_R (unscaled) into S0 ----
+  for (int e = tid; e < N * N; e += THREADS) {
+    const int q = e / N, s = e - q * N;
+    const int si = s / D, sj = s - si * D;
+    const int st = sj * D + si;
+    double2 c;
+    if (si == sj) {
+      c = kron_l(dis, hb, q, s);
+    } else {
+      const double2 a = kron_l(dis, hb, q, s), bt = kron_l(dis, hb, q, st);
+      c = si < sj ? make_double2(a.x + bt.x, a.y + bt.y) : make_double2(a.y - bt.y, bt.x - a.x);
+    }
+    const int qi = q / D, qj = q - qi * D;
+    S0[q * RS + s] = qi <= qj ? c.x : -c.y;
+  }
+  __syncthreads();
+  // ||A dt||_1 -> squarings (per trajectory)
+  if (tid < N) {
+    double cs = 0.0;
+    for (int r = 0; r < N; ++r) cs += fabs(S0[r * RS + tid]);
+    colsum[tid] = cs * fabs(dt);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double nrm = 0.0;
+    for (int c = 0; c < N; ++c) nrm = fmax(nrm, colsum[c]);
+    s_sq = nrm > kTheta14 ? int(ceil(log2(nrm / kTheta14))) : 0;
+  }
+  __syncthreads();
+  const int sq = s_sq;
+  const double sc = dt * ldexp(1.0, -sq);
+  for (int e = tid; e < N * N; e += THREADS) {
+    const int q = e / N, s = e - q * N;
+    S0[q * RS + s] *= sc;
+  }
+  __syncthreads();
+
+  const int g = lane >> 2, t = lane & 3;
+  double a1[MT][2], a2[MT][2], acc[MT][2];
+#pragma unroll
+  for (int m = 0; m < MT; ++m)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) a1[m][c] = S0[(m * 8 + g) * RS + w * 8 + 2 * t + c];
+  // Taylor coefficients 1/k!, k = 0..14
+  double cf[15];
+  cf[0] = 1.0;
+#pragma unroll
+  for (int k = 1; k < 15; ++k) cf[k] = cf[k - 1] / k;
+
+  mm(S0, S0, acc, w, lane);  // A2
+#pragma unroll
+  for (int m = 0; m < MT; ++m) a2[m][0] = acc[m][0], a2[m][1] = acc[m][1];
+  store(S1, acc, w, lane);
+  __syncthreads();
+  mm(S1, S0, acc, w, lane);  // A3
+  __syncthreads();            // everyone done reading S0/S1
+  store(S2, acc, w, lane);
+  horner_epilogue(acc, a1, a2, cf[12], cf[13], cf[14], w, lane, false);  // T = B4
+  store(S0, acc, w, lane);
+  __syncthreads();
+  double* tcur = S0;
+  double* tnxt = S1;
+#pragma unroll
+  for (int j = 3; j >= 0; --j) {  // T = B_j + A3 T
+    mm(S2, tcur, acc, w, lane);
+    horner_epilogue(acc, a1, a2, cf[3 * j], cf[3 * j + 1], cf[3 * j + 2], w, lane, true);
+    if (j > 0 || sq > 0) {
+      store(tnxt, acc, w, lane);
+      __syncthreads();
+      double* tt = tcur;
+      tcur = tnxt;
+      tnxt = tt;
+    }
+  }
+  for (int i = 0; i < sq; ++i) {  // squarings
+    mm(tcur, tcur, acc, w, lane);
+    if (i + 1 < sq) {
+      store(tnxt, acc, w, lane);
+      __syncthreads();
+      double* tt = tcur;
+      tcur = tnxt;
+      tnxt = tt;
+    }
+  }
+  // ---- P_R -> global (n x n, unpadded) ----
+  double* out = p_out + size_t(b) * N * N;
+#pragma unroll
+  for (int m = 0; m < MT; ++m) {
+    const int r = m * 8 + g, c0 = w * 8 + 2 * t;
+    if (r < N) {
+      if (c0 < N) out[r * N + c0] = acc[m][0];
+      if (c0 + 1 < N) out[r * N + c0 + 1] = acc[m][1];
+    }
+  }
+}
+
+// K3: x <- P_R x for `steps` steps, P_R register resident.
+constexpr int CH = 8, CW = 11;  // 8 column chunks of 11 (88)
+__global__ void __launch_bounds__(THREADS) ptm_step_kernel(const double* __restrict__ p_r,
+                                                           const double* __restrict__ x0, int64_t steps,
+                                                           double* __restrict__ pops,
+                                                           double* __restrict__ ens_x) {
+  __shared__ __align__(16) double xs[2][88];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int rp = w * 4 + (lane >> 3);  // row pair 0..43 (41 used)
+  const int ch = lane & 7;             // column chunk
+  const int r0 = 2 * rp, r1 = 2 * rp + 1;
+  const double* pb = p_r + size_t(blockIdx.x) * N * N;
+  double p0[CW], p1[CW];
+#pragma unroll
+  for (int jj = 0; jj < CW; ++jj) {
+    const int c = ch * CW + jj;
+    p0[jj] = (r0 < N && c < N) ? pb[r0 * N + c] : 0.0;
+    p1[jj] = (r1 < N && c < N) ? pb[r1 * N + c] : 0.0;
+  }
+  for (int e = tid; e < 88; e += THREADS) {
+    xs[0][e] = e < N ? x0[e] : 0.0;
+    xs[1][e] = 0.0;
+  }
+  __syncthreads();
+  int cur = 0;
+  for (int64_t s = 0; s < steps; ++s) {
+    const double* x = xs[cur] + ch * CW;
+    double s0 = 0.0, s1 = 0.0, u0 = 0.0, u1 = 0.0;
+#pragma unroll
+    for (int jj = 0; jj < CW; jj += 2) {
+      s0 = fma(p0[jj], x[jj], s0);
+      s1 = fma(p1[jj], x[jj], s1);
+      if (jj + 1 < CW) {
+        u0 = fma(p0[jj + 1], x[jj + 1], u0);
+        u1 = fma(p1[jj + 1], x[jj + 1], u1);
+      }
+    }
+    s0 += u0;
+    s1 += u1;
+#pragma unroll
+    for (int o = 1; o < CH; o <<= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    }
+    if (ch == 0 && r0 < N) {
+      xs[cur ^ 1][r0] = s0;
+      if (r1 < N) xs[cur ^ 1][r1] = s1;
+    }
+    __syncthreads();
+    cur ^= 1;
+  }
+  if (tid < D) pops[size_t(blockIdx.x) * D + tid] = xs[cur][tid * D + tid];
+  if (tid < N) atomicAdd(&ens_x[tid], xs[cur][tid]);
+}
+
+// complex rho (d x d) <-> real coordinates
+__global__ void rho_to_x_kernel(const double2* __restrict__ rho, double* __restrict__ x) {
+  const int p = threadIdx.x;
+  if (p >= N) return;
+  const int i = p / D, j = p - i * D;
+  x[p] = i <= j ? rho[p].x : -rho[p].y;
+}
+__global__ void x_to_rho_kernel(const double* __restrict__ x, double2* __restrict__ rho) {
+  const int p = threadIdx.x;
+  if (p >= N) return;
+  const int i = p / D, j = p - i * D;
+  if (i == j)
+    rho[p] = make_double2(x[p], 0.0);
+  else if (i < j)
+    rho[p] = make_double2(x[p], x[j * D + i]);
+  else
+    rho[p] = make_double2(x[j * D + i], -x[p]);
+}
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+constexpr int64_t kChunk = 16384;
+
+}  // namespace
+
+size_t ptm_sweep_workspace(int64_t batch) {
+  const size_t chunk = size_t(std::min<int64_t>(std::max<int64_t>(batch, 1), kChunk));
+  return align_up(chunk * N * N * 8) + align_up(size_t(N) * N * 16) + align_up(2 * N * 8) + 256;
+}
+
+bool ptm_sweep_supported(size_t d) { return d == size_t(D); }
+
+void launch_ptm_sweep(size_t d, const double* h0, const double* hd, const double* hs, size_t n_ops,
+                      const double* ops, const double* delta, const double* scale, double dt,
+                      const double* rho0, int64_t batch, int64_t steps, double* pops, double* ens_sum,
+                      void* work, cudaStream_t s) {
+  if (d != size_t(D)) throw invalid_argument("ptm sweep: d must be 9");
+  const size_t chunk = size_t(std::min<int64_t>(std::max<int64_t>(batch, 1), kChunk));
+  char* w = static_cast<char*>(work);
+  double* pr = reinterpret_cast<double*>(w);
+  double2* dis = reinterpret_cast<double2*>(w + align_up(chunk * N * N * 8));
+  double* xv = reinterpret_cast<double*>(w + align_up(chunk * N * N * 8) + align_up(size_t(N) * N * 16));
+  double* x0 = xv;
+  double* ens_x = xv + N;
+  // dissipator D = build_lindbladian(H = 0, ops) (K5, shared by all trajectories)
+  check_cuda(cudaMemsetAsync(ens_x, 0, N * 8, s), "memset");
+  check_cuda(cudaMemsetAsync(pr, 0, d * d * 16, s), "memset");
+  launch_build_lindbladian(d, pr, n_ops, ops, reinterpret_cast<double*>(dis), s);
+  rho_to_x_kernel<<<1, 96, 0, s>>>(reinterpret_cast<const double2*>(rho0), x0);
+  LBG_CHECK_LAUNCH("rho_to_x_kernel");
+  const size_t smem = size_t(3) * MAT * 8;
+  static bool attr = [&] {
+    check_cuda(cudaFuncSetAttribute(ptm_expm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+               "smem attr");
+    return true;
+  }();
+  (void)attr;
+  for (int64_t c0 = 0; c0 < batch; c0 += int64_t(chunk)) {
+    const int cb = int(std::min<int64_t>(int64_t(chunk), batch - c0));
+    ptm_expm_kernel<<<cb, THREADS, smem, s>>>(dis, reinterpret_cast<const double2*>(h0),
+                                              reinterpret_cast<const double2*>(hd),
+                                              reinterpret_cast<const double2*>(hs), delta + c0, scale + c0,
+                                              dt, pr);
+    LBG_CHECK_LAUNCH("ptm_expm_kernel");
+    ptm_step_kernel<<<cb, THREADS, 0, s>>>(pr, x0, steps, pops + c0 * int64_t(D), ens_x);
+    LBG_CHECK_LAUNCH("ptm_step_kernel");
+  }
+  x_to_rho_kernel<<<1, 96, 0, s>>>(ens_x, reinterpret_cast<double2*>(ens_sum));
+  LBG_CHECK_LAUNCH("x_to_rho_kernel");
+}
+
+}  // namespace lbg

@@ -227,7 +227,8 @@ def test_tiled_is_linear_at_scale(lbg, torch):
 
 
 # ----------------------------------------------------------- config 4 sweep ---
-def test_sweep_vs_reference_goldens(lbg, torch, golden):
+@pytest.mark.parametrize("mode", ["complex", "real"])
+def test_sweep_vs_reference_goldens(lbg, torch, golden, mode):
     s = golden["sweep"]
     dev = torch.device("cuda")
     h0, hd, hs = lbg.config_sweep_terms()
@@ -240,7 +241,7 @@ def test_sweep_vs_reference_goldens(lbg, torch, golden):
     ens = torch.zeros(9, 9, dtype=torch.complex128, device=dev)
     work = torch.empty(lbg.sweep_workspace(9, B), dtype=torch.uint8, device=dev)
     lbg.evolve_sweep_dev(T(h0), T(hd), T(hs), T(ops), T(s["delta"]), T(s["scale"]), 0.1, T(rho0),
-                         int(s["steps"]), pops, ens, work)
+                         int(s["steps"]), pops, ens, work, mode=mode)
     torch.cuda.synchronize()
     assert np.abs(pops.cpu().numpy() - s["pops"]).max() <= TOL_RHO
     assert np.abs(ens.cpu().numpy() - s["ens_sum"]).max() <= TOL_RHO * B
@@ -249,7 +250,12 @@ def test_sweep_vs_reference_goldens(lbg, torch, golden):
     assert tr <= TOL_INV and herm <= TOL_INV
 
 
-def test_sweep_full_size_invariants(lbg, torch):
+@pytest.mark.parametrize("mode", ["complex", "real"])
+def test_sweep_full_size_invariants(lbg, torch, mode):
+    _sweep_full(lbg, torch, mode)
+
+
+def _sweep_full(lbg, torch, mode):
     dev = torch.device("cuda")
     B = 65536
     h0, hd, hs = lbg.config_sweep_terms()
@@ -261,7 +267,8 @@ def test_sweep_full_size_invariants(lbg, torch):
     pops = torch.zeros(B, 9, dtype=torch.float64, device=dev)
     ens = torch.zeros(9, 9, dtype=torch.complex128, device=dev)
     work = torch.empty(lbg.sweep_workspace(9, B), dtype=torch.uint8, device=dev)
-    lbg.evolve_sweep_dev(T(h0), T(hd), T(hs), T(ops), T(delta), T(scale), 0.1, T(rho0), 500, pops, ens, work)
+    lbg.evolve_sweep_dev(T(h0), T(hd), T(hs), T(ops), T(delta), T(scale), 0.1, T(rho0), 500, pops, ens, work,
+                         mode=mode)
     torch.cuda.synchronize()
     p = pops.cpu().numpy()
     assert np.abs(p.sum(axis=1) - 1.0).max() <= TOL_INV
@@ -270,3 +277,28 @@ def test_sweep_full_size_invariants(lbg, torch):
     tr, herm = invariants(e)
     assert tr <= TOL_INV and herm <= TOL_INV
     assert np.abs(np.diag(e).real - p.mean(axis=0)).max() <= 1e-12
+    return p, e
+
+
+def test_sweep_modes_agree_at_full_size(lbg, torch):
+    """real transfer-matrix path == complex path within the parity tolerance."""
+    pr, er = _sweep_full(lbg, torch, "real")
+    pc, ec = _sweep_full(lbg, torch, "complex")
+    assert np.abs(pr - pc).max() <= TOL_RHO
+    assert np.abs(er - ec).max() <= TOL_RHO
+
+
+def test_sweep_real_mode_rejects_non_hermitian(lbg, torch):
+    dev = torch.device("cuda")
+    h0, hd, hs = lbg.config_sweep_terms()
+    _, ops = lbg.config_model(4)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    rho0 = np.zeros((9, 9), complex)
+    rho0[0, 0] = 1.0
+    rho0[0, 1] = 1e-3
+    pops = torch.zeros(1, 9, dtype=torch.float64, device=dev)
+    ens = torch.zeros(9, 9, dtype=torch.complex128, device=dev)
+    work = torch.empty(lbg.sweep_workspace(9, 1), dtype=torch.uint8, device=dev)
+    with pytest.raises(ValueError):
+        lbg.evolve_sweep_dev(T(h0), T(hd), T(hs), T(ops), T(np.zeros(1)), T(np.ones(1)), 0.1, T(rho0), 5,
+                             pops, ens, work, mode="real")

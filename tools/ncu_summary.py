@@ -1,0 +1,63 @@
+"""Summarise an .ncu-rep (raw page) into a few roofline-relevant numbers.
+usage: python tools/ncu_summary.py REP [REP...]  -> one JSON object per kernel launch"""
+import csv
+import io
+import json
+import subprocess
+import sys
+
+KEYS = {
+    "gpu__time_duration.sum": "duration",
+    "dram__bytes_read.sum": "dram_read",
+    "dram__bytes_write.sum": "dram_write",
+    "lts__t_bytes.sum": "l2_bytes",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_pipe_pct",
+    "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active": "fp64_inst_pct",
+    "sm__pipe_tensor_op_dmma_cycles_active.avg.pct_of_peak_sustained_active": "dmma_pipe_pct",
+    "sm__pipe_fp64_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed": "fp64_realtime_pct",
+    "launch__registers_per_thread": "regs",
+    "sm__warps_active.avg.pct_of_peak_sustained_active": "warps_active_pct",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum": "smem_wavefronts",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum": "smem_bank_conflicts",
+    "sm__cycles_elapsed.avg": "sm_cycles",
+    "sm__cycles_elapsed.avg.per_second": "sm_clock",
+    "launch__grid_size": "grid",
+    "launch__block_size": "block",
+}
+UNIT = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1, "msecond": 1e-3, "usecond": 1e-6,
+        "nsecond": 1e-9, "ms": 1e-3, "us": 1e-6, "ns": 1e-9, "Ghz": 1e9, "Mhz": 1e6}
+
+
+def summarise(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    head, units = rows[0], rows[1]
+    res = []
+    for r in rows[2:]:
+        d = {"kernel": r[head.index("Kernel Name")][:80]}
+        for k, name in KEYS.items():
+            if k in head:
+                i = head.index(k)
+                try:
+                    v = float(r[i].replace(",", ""))
+                except ValueError:
+                    continue
+                d[name] = v * UNIT.get(units[i], 1.0)
+        stalls = {}
+        for i, h in enumerate(head):
+            if h.startswith("smsp__average_warp_latency_issue_stalled_") and h.endswith(".ratio"):
+                try:
+                    stalls[h.split("stalled_")[1].replace(".ratio", "")] = float(r[i])
+                except ValueError:
+                    pass
+        if stalls:
+            d["top_stalls"] = dict(sorted(stalls.items(), key=lambda x: -x[1])[:5])
+        res.append(d)
+    return res
+
+
+if __name__ == "__main__":
+    for rep in sys.argv[1:]:
+        for d in summarise(rep):
+            print(json.dumps(d))
