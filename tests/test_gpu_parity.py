@@ -302,3 +302,18 @@ def test_sweep_real_mode_rejects_non_hermitian(lbg, torch):
     with pytest.raises(ValueError):
         lbg.evolve_sweep_dev(T(h0), T(hd), T(hs), T(ops), T(np.zeros(1)), T(np.ones(1)), 0.1, T(rho0), 5,
                              pops, ens, work, mode="real")
+
+
+# ------------------------------------------------------- drop-in boundary ---
+def test_reference_evolve_drives_the_gpu_kernel():
+    """tests/cpp/dropin_gate: the reference's own lb::evolve / grape_chain with
+    KernelProfile{"b200", lbg_step_aos, lbg_step_soa} (kernels.hpp:29-33)."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(__file__), "cpp", "_bin", "dropin_gate")
+    if not os.path.exists(exe):
+        pytest.skip("dropin_gate not built (needs the reference headers at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "all criteria passed" in r.stdout
