@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include "../../include/lbg.h"
@@ -56,6 +57,41 @@ struct DevBuf {
     return static_cast<T*>(p);
   }
 };
+
+// Device buffers and streams reused across lbg_evolve_shared_p calls (grown
+// on demand), so the end-to-end call pays no cudaMalloc/cudaFree per call.
+struct Grow {
+  void* ptr = nullptr;
+  size_t cap = 0;
+  void ensure(size_t bytes) {
+    if (bytes <= cap) return;
+    if (ptr) check_cuda(cudaFree(ptr), "cudaFree");
+    ptr = nullptr;
+    check_cuda(cudaMalloc(&ptr, bytes), "cudaMalloc");
+    cap = bytes;
+  }
+};
+struct EvolvePool {
+  std::mutex mu;
+  Grow p, x, chk, w[2];
+  cudaStream_t st[2] = {nullptr, nullptr};
+  cudaEvent_t ev_p = nullptr;
+  void ensure(size_t pb, size_t xb, size_t cb, size_t wb) {
+    if (!st[0]) {
+      for (auto& s : st) check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+      check_cuda(cudaEventCreateWithFlags(&ev_p, cudaEventDisableTiming), "event");
+    }
+    p.ensure(pb);
+    x.ensure(xb);
+    chk.ensure(cb);
+    w[0].ensure(wb);
+    w[1].ensure(wb);
+  }
+};
+EvolvePool& evolve_pool() {
+  static EvolvePool* pool = new EvolvePool;  // intentionally leaked: outlives CUDA teardown
+  return *pool;
+}
 
 // reference is_hermitian (lindblad.cpp:13-20): relative 1e-12 on max |h|
 bool is_hermitian(const double* h, size_t d) {
@@ -265,20 +301,47 @@ int lbg_evolve_shared_p(const double* p, size_t d, const double* rho0, int64_t b
   return guarded([&] {
     if (d == 0) throw invalid_argument("evolve: state dimension must be positive");
     if (batch < 0 || steps < 0) throw invalid_argument("evolve: negative batch or steps");
+    if (batch == 0) return;
     const size_t n = d * d;
-    const size_t xbytes = size_t(batch) * n * 16;
-    DevBuf dp(n * n * 16), dx(xbytes), dchk(3 * 8), dw(lbg_evolve_workspace(n, batch, algo));
-    check_cuda(cudaMemcpy(dp.p, p, n * n * 16, cudaMemcpyHostToDevice), "H2D P");
-    check_cuda(cudaMemcpy(dx.p, rho0, xbytes, cudaMemcpyHostToDevice), "H2D rho0");
-    // propagate.cpp:79 — every rho0 must pass check_state at 1e-8
-    launch_check_state(dx.as<double>(), d, batch, dchk.as<double>(), nullptr);
-    double chk[3];
-    check_cuda(cudaMemcpy(chk, dchk.p, sizeof chk, cudaMemcpyDeviceToHost), "D2H check");
-    if (batch > 0 && !(chk[0] <= 1e-8 && chk[1] <= 1e-8 && chk[2] >= -1e-8))
-      throw invalid_argument("evolve: initial state fails physical-state checks");
-    evolve_dev(dp.as<double>(), n, nullptr, nullptr, dx.as<double>(), batch, steps, algo, dw.p, nullptr,
-               Layout::aos);
-    check_cuda(cudaMemcpy(out, dx.p, xbytes, cudaMemcpyDeviceToHost), "D2H rho");
+    const int chosen = choose_algo(n, batch, algo);
+    // Pipeline: the batch is cut into chunks that alternate between two streams,
+    // so chunk k's H2D, chunk k-1's steps and chunk k-2's D2H overlap (copy
+    // engines and SMs run concurrently). The cooperative tiled kernel is never
+    // run concurrently with itself, so it gets a single chunk.
+    const int64_t min_chunk = 32768;
+    const int nchunks = (chosen == LBG_ALGO_TILED || batch < 2 * min_chunk)
+                            ? 1
+                            : int(std::min<int64_t>(8, batch / min_chunk));
+    const int64_t chunk = (batch + nchunks - 1) / nchunks;
+    EvolvePool& pool = evolve_pool();
+    std::lock_guard<std::mutex> lk(pool.mu);
+    pool.ensure(n * n * 16, size_t(batch) * n * 16, size_t(nchunks) * 3 * 8,
+                lbg_evolve_workspace(n, chunk, algo));
+    double* dp = static_cast<double*>(pool.p.ptr);
+    double* dx = static_cast<double*>(pool.x.ptr);
+    double* dchk = static_cast<double*>(pool.chk.ptr);
+    check_cuda(cudaMemcpyAsync(dp, p, n * n * 16, cudaMemcpyHostToDevice, pool.st[0]), "H2D P");
+    check_cuda(cudaEventRecord(pool.ev_p, pool.st[0]), "event");
+    check_cuda(cudaStreamWaitEvent(pool.st[1], pool.ev_p, 0), "wait");
+    for (int c = 0; c < nchunks; ++c) {
+      const int64_t b0 = c * chunk, nb = std::min<int64_t>(chunk, batch - b0);
+      if (nb <= 0) break;
+      cudaStream_t s = pool.st[c & 1];
+      double* xc = dx + size_t(b0) * n * 2;
+      const size_t bytes = size_t(nb) * n * 16;
+      check_cuda(cudaMemcpyAsync(xc, rho0 + size_t(b0) * n * 2, bytes, cudaMemcpyHostToDevice, s), "H2D rho0");
+      // propagate.cpp:79 — every rho0 must pass check_state at 1e-8
+      launch_check_state(xc, d, nb, dchk + 3 * c, s);
+      evolve_dev(dp, n, nullptr, nullptr, xc, nb, steps, algo, pool.w[c & 1].ptr, s, Layout::aos);
+      check_cuda(cudaMemcpyAsync(out + size_t(b0) * n * 2, xc, bytes, cudaMemcpyDeviceToHost, s), "D2H rho");
+    }
+    std::vector<double> chk(size_t(nchunks) * 3);
+    check_cuda(cudaMemcpyAsync(chk.data(), dchk, chk.size() * 8, cudaMemcpyDeviceToHost, pool.st[1]), "D2H");
+    check_cuda(cudaStreamSynchronize(pool.st[0]), "sync");
+    check_cuda(cudaStreamSynchronize(pool.st[1]), "sync");
+    for (int c = 0; c < nchunks; ++c)
+      if (!(chk[3 * c] <= 1e-8 && chk[3 * c + 1] <= 1e-8 && chk[3 * c + 2] >= -1e-8))
+        throw invalid_argument("evolve: initial state fails physical-state checks");
   });
 }
 

@@ -5,16 +5,20 @@
 // One step is a complex GEMM  V_next (n x B) = P (n x n) * V (n x B).  P and both
 // state buffers (2 x 12 MB at config 3) stay L2-resident (126 MB L2), so the
 // bound is the DMMA pipe. The kernel is PERSISTENT (cooperative launch, all
-// CTAs co-resident): per step every CTA pulls 32x32 complex output tiles from
-// an atomic counter (dynamic balance: 736 tiles on 148 SMs), computes each tile
-// with a 3-stage cp.async pipeline feeding m8n8k4 DMMAs in real form
-// (common.cuh), writes it to the other state buffer, and all CTAs meet at a
-// grid barrier before the next step (every output row needs every input row).
+// CTAs co-resident): per step a producer warp pulls 32x32 complex output tiles
+// from an atomic counter (dynamic balance: 736 tiles on 148 SMs) and streams
+// their K chunks into a 4-stage shared-memory ring with 1-D bulk async copies
+// (cp.async.bulk -> the TMA engine, SASS UBLKCP) signalled through mbarriers
+// (complete_tx); 8 consumer warps wait on the stage's "full" barrier, run the
+// m8n8k4 DMMAs in real form (common.cuh), release the stage on its "empty"
+// barrier and write finished tiles straight from registers to the other state
+// buffer. No block-wide barrier in the main loop; one grid barrier per step
+// (every output row needs every input row).
 //
-// Tile geometry: 32 complex rows (64 real, 8 m-tiles) x 32 columns (4 n-tiles),
-// K chunk 16 complex (8 k-steps); 8 warps, each 2 m-tiles x 2 n-tiles.
-// Shared strides SA = 2 (mod 8), SB = 4 (mod 8) complex make every fragment
-// load bank-conflict free.
+// Tile: 32 complex rows (64 real, 8 m-tiles) x 32 columns (4 n-tiles), K chunk
+// 16 complex (8 k-steps); each consumer warp owns 2 m-tiles x 2 n-tiles.
+// Shared strides SA = 2 (mod 8), SB = 4 (mod 8) complex make every fragment load
+// bank-conflict free. Ragged edges are masked in registers (no smem zeroing).
 //
 // Replaces step_soa_kernel (proj/src/kernels_variants.cpp:26-41) inside
 // evolve (proj/src/propagate.cpp:85-92), batched; the GEMM replaces
@@ -28,116 +32,225 @@ namespace lbg {
 
 namespace {
 
-constexpr int BM = 32, BN = 32, BK = 16, STAGES = 3, THREADS = 256;
+constexpr int BM = 32, BN = 32, BK = 16, STAGES = 4;
+constexpr int CWARPS = 8, THREADS = 32 * (CWARPS + 1);
 constexpr int SA = 18, SB = 36;  // complex strides (see header)
 constexpr int A_ELEMS = BM * SA, B_ELEMS = BK * SB;
-constexpr size_t kSmemBytes = size_t(STAGES) * (A_ELEMS + B_ELEMS) * sizeof(double2);
+constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;  // double2 units
+constexpr size_t kSmemBytes = size_t(STAGES) * STAGE_ELEMS * sizeof(double2) + 256;
 
-struct TileCtx {
-  int tid, lane, wm, wn;
-  AFragLane af;
-  __device__ TileCtx() : tid(threadIdx.x), lane(threadIdx.x & 31), wm((threadIdx.x >> 5) >> 1),
-                         wn((threadIdx.x >> 5) & 1), af(threadIdx.x & 31) {}
+// ---- mbarrier / bulk-copy primitives (PTX) ----------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+struct Ring {
+  double2* data;   // STAGES x (A | B)
+  uint64_t* full;  // STAGES
+  uint64_t* empty; // STAGES
+  int* hdr;        // STAGES x 2: tile id (-1 = end of step), k chunk
 };
 
-__device__ __forceinline__ void load_stage(double2* as, double2* bs, const double2* __restrict__ A,
-                                           long long lda, const double2* __restrict__ B,
-                                           long long ldb, int M, int N, int K, int m0, int n0,
-                                           int k0, int tid) {
-#pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    const int e = tid + r * THREADS;
-    {  // A: 32 rows x 16 complex
-      const int row = e >> 4, col = e & 15;
-      const bool ok = (m0 + row < M) && (k0 + col < K);
-      const double2* src = ok ? A + (long long)(m0 + row) * lda + (k0 + col) : A;
-      cp_async16(as + row * SA + col, src, ok);
-    }
-    {  // B: 16 rows x 32 complex
-      const int row = e >> 5, col = e & 31;
-      const bool ok = (k0 + row < K) && (n0 + col < N);
-      const double2* src = ok ? B + (long long)(k0 + row) * ldb + (n0 + col) : B;
-      cp_async16(bs + row * SB + col, src, ok);
-    }
+__device__ __forceinline__ Ring carve(unsigned char* smem) {
+  Ring r;
+  r.data = reinterpret_cast<double2*>(smem);
+  unsigned char* tail = smem + size_t(STAGES) * STAGE_ELEMS * sizeof(double2);
+  r.full = reinterpret_cast<uint64_t*>(tail);
+  r.empty = r.full + STAGES;
+  r.hdr = reinterpret_cast<int*>(r.empty + STAGES);
+  return r;
+}
+
+struct Problem {  // C (M x N) = A (M x K) * B (K x N), complex row-major
+  const double2* A;
+  long long lda;
+  const double2* B;
+  long long ldb;
+  double2* C;
+  long long ldc;
+  int M, N, K;
+};
+
+__device__ __forceinline__ void advance(int& stage, unsigned& phase) {
+  if (++stage == STAGES) {
+    stage = 0;
+    phase ^= 1u;
   }
 }
 
-// acc[mi][ni][2] += A(m0.., :) * B(:, n0..) over the full K.
-__device__ __forceinline__ void gemm_tile(const double2* __restrict__ A, long long lda,
-                                          const double2* __restrict__ B, long long ldb, int M,
-                                          int N, int K, int m0, int n0, double (&acc)[2][2][2],
-                                          double2* smem, const TileCtx& c) {
-  double2* as = smem;
-  double2* bs = smem + STAGES * A_ELEMS;
-#pragma unroll
-  for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-    for (int ni = 0; ni < 2; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-  const int nk = (K + BK - 1) / BK;
-#pragma unroll
-  for (int st = 0; st < STAGES - 1; ++st) {
-    if (st < nk) load_stage(as + st * A_ELEMS, bs + st * B_ELEMS, A, lda, B, ldb, M, N, K, m0, n0, st * BK, c.tid);
-    cp_async_commit();
-  }
-  // per-lane fragment offsets (doubles) inside a stage
-  const int a_off = 2 * ((c.wm * 2 * 4 + c.af.di) * SA + c.af.dj) + c.af.comp;
-  const int b_off = 2 * (((c.lane & 3) >> 1) * SB + c.wn * 2 * 8 + (c.lane >> 2)) + (c.lane & 1);
+// Producer: one warp streams the K chunks of tile (m0, n0) into the ring.
+__device__ __forceinline__ void produce_tile(const Ring& r, const Problem& p, int tile, int m0, int n0,
+                                             int& stage, unsigned& phase, int lane) {
+  const int nk = (p.K + BK - 1) / BK;
+  const int mrows = min(BM, p.M - m0), ncols = min(BN, p.N - n0);
   for (int kc = 0; kc < nk; ++kc) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    {
-      const int nxt = kc + STAGES - 1;
-      if (nxt < nk)
-        load_stage(as + (nxt % STAGES) * A_ELEMS, bs + (nxt % STAGES) * B_ELEMS, A, lda, B, ldb, M,
-                   N, K, m0, n0, nxt * BK, c.tid);
-      cp_async_commit();
+    const int k0 = kc * BK, kv = min(BK, p.K - k0);
+    mbar_wait(&r.empty[stage], phase ^ 1u);
+    double2* as = r.data + stage * STAGE_ELEMS;
+    double2* bs = as + A_ELEMS;
+    const unsigned bytes = unsigned(mrows * kv + kv * ncols) * 16u;
+    if (lane == 0) {
+      r.hdr[2 * stage] = tile;
+      r.hdr[2 * stage + 1] = kc;
+      mbar_arrive_tx(&r.full[stage], bytes);
     }
-    const double* ad = reinterpret_cast<const double*>(as + (kc % STAGES) * A_ELEMS) + a_off;
-    const double* bd = reinterpret_cast<const double*>(bs + (kc % STAGES) * B_ELEMS) + b_off;
+    __syncwarp();
+    for (int row = lane; row < mrows; row += 32)
+      bulk_g2s(as + row * SA, p.A + (long long)(m0 + row) * p.lda + k0, unsigned(kv) * 16u, &r.full[stage]);
+    for (int row = lane; row < kv; row += 32)
+      bulk_g2s(bs + row * SB, p.B + (long long)(k0 + row) * p.ldb + n0, unsigned(ncols) * 16u, &r.full[stage]);
+    advance(stage, phase);
+  }
+}
+
+__device__ __forceinline__ void produce_end(const Ring& r, int& stage, unsigned& phase, int lane) {
+  mbar_wait(&r.empty[stage], phase ^ 1u);
+  if (lane == 0) {
+    r.hdr[2 * stage] = -1;
+    mbar_arrive(&r.full[stage]);
+  }
+  advance(stage, phase);
+}
+
+// Consumer warps: run tiles until the end-of-step sentinel.
+__device__ __forceinline__ void consume(const Ring& r, const Problem& p, int tiles_m, int& stage,
+                                       unsigned& phase, int warp, int lane) {
+  const AFragLane af(lane);
+  const int wm = warp >> 1, wn = warp & 1;
+  const int nk = (p.K + BK - 1) / BK;
+  const int a_off = 2 * ((wm * 2 * 4 + af.di) * SA + af.dj) + af.comp;
+  const int b_off = 2 * (((lane & 3) >> 1) * SB + wn * 2 * 8 + (lane >> 2)) + (lane & 1);
+  double acc[2][2][2] = {};
+  bool row_ok[2] = {true, true};
+  int m0 = 0, n0 = 0;
+  while (true) {
+    mbar_wait(&r.full[stage], phase);
+    const int tile = r.hdr[2 * stage], kc = r.hdr[2 * stage + 1];
+    if (tile < 0) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&r.empty[stage]);
+      advance(stage, phase);
+      return;
+    }
+    if (kc == 0) {
+      m0 = (tile % tiles_m) * BM;
+      n0 = (tile / tiles_m) * BN;
 #pragma unroll
-    for (int ks = 0; ks < BK / 2; ++ks) {
-      double a[2], b[2];
+      for (int mi = 0; mi < 2; ++mi) {
+        row_ok[mi] = m0 + (wm * 2 + mi) * 4 + af.di < p.M;
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi) a[mi] = c.af.sign(ad[2 * (mi * 4 * SA) + 4 * ks]);
+        for (int ni = 0; ni < 2; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+      }
+    }
+    const double* ad = reinterpret_cast<const double*>(r.data + stage * STAGE_ELEMS) + a_off;
+    const double* bd = reinterpret_cast<const double*>(r.data + stage * STAGE_ELEMS + A_ELEMS) + b_off;
+    const int k0 = kc * BK;
+    if (k0 + BK <= p.K && row_ok[0] && row_ok[1]) {
 #pragma unroll
-      for (int ni = 0; ni < 2; ++ni) b[ni] = bd[2 * (2 * ks * SB + ni * 8)];
+      for (int ks = 0; ks < BK / 2; ++ks) {
+        double a[2], b[2];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) a[mi] = af.sign(ad[2 * (mi * 4 * SA) + 4 * ks]);
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) b[ni] = bd[2 * (2 * ks * SB + ni * 8)];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+      }
+    } else {  // ragged edge: rows >= M and k >= K masked in registers
+#pragma unroll
+      for (int ks = 0; ks < BK / 2; ++ks) {
+        const bool kok = k0 + ks * 2 + af.dj < p.K;
+        double a[2], b[2];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+          a[mi] = (kok && row_ok[mi]) ? af.sign(ad[2 * (mi * 4 * SA) + 4 * ks]) : 0.0;
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) b[ni] = kok ? bd[2 * (2 * ks * SB + ni * 8)] : 0.0;
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&r.empty[stage]);
+    advance(stage, phase);
+    if (kc == nk - 1) {  // tile done: registers -> global
 #pragma unroll
       for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+        for (int ni = 0; ni < 2; ++ni) {
+          int coff;
+          const double2 z = pair_complex(acc[mi][ni], lane, coff);
+          const int i = m0 + (wm * 2 + mi) * 4 + (lane >> 3);
+          const int col = n0 + (wn * 2 + ni) * 8 + coff;
+          if (i < p.M && col < p.N) p.C[(long long)i * p.ldc + col] = z;
+        }
     }
   }
-  cp_async_wait<0>();
-  __syncthreads();  // stages free for the next tile
 }
 
-__device__ __forceinline__ void store_tile(double2* __restrict__ C, long long ldc, int M, int N,
-                                           int m0, int n0, const double (&acc)[2][2][2],
-                                           const TileCtx& c) {
-#pragma unroll
-  for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-    for (int ni = 0; ni < 2; ++ni) {
-      int coff;
-      const double2 z = pair_complex(acc[mi][ni], c.lane, coff);
-      const int i = m0 + (c.wm * 2 + mi) * 4 + (c.lane >> 3);
-      const int col = n0 + (c.wn * 2 + ni) * 8 + coff;
-      if (i < M && col < N) C[(long long)i * ldc + col] = z;
+__device__ __forceinline__ void init_ring(const Ring& r) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&r.full[s], 1);
+      mbar_init(&r.empty[s], CWARPS);
     }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
 }
 
-// ---- plain batched GEMM (expm) --------------------------------------------
+// ---- plain batched GEMM (expm): one tile per CTA -----------------------------
 __global__ void __launch_bounds__(THREADS) zgemm_kernel(const double2* __restrict__ A,
                                                         const double2* __restrict__ B,
                                                         double2* __restrict__ C, int n,
                                                         long long sa, long long sb, long long sc) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const TileCtx c;
-  const int b = blockIdx.z;
-  double acc[2][2][2];
-  gemm_tile(A + b * sa, n, B + b * sb, n, n, n, n, blockIdx.x * BM, blockIdx.y * BN, acc,
-            reinterpret_cast<double2*>(smem_raw), c);
-  store_tile(C + b * sc, n, n, n, blockIdx.x * BM, blockIdx.y * BN, acc, c);
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const Ring r = carve(smem_raw);
+  init_ring(r);
+  const int b = blockIdx.z, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Problem p{A + b * sa, n, B + b * sb, n, C + b * sc, n, n, n, n};
+  const int tiles_m = (n + BM - 1) / BM;
+  const int tile = blockIdx.y * tiles_m + blockIdx.x;
+  int stage = 0;
+  unsigned phase = 0;
+  if (warp == CWARPS) {
+    produce_tile(r, p, tile, blockIdx.x * BM, blockIdx.y * BN, stage, phase, lane);
+    produce_end(r, stage, phase, lane);
+  } else {
+    consume(r, p, tiles_m, stage, phase, warp, lane);
+  }
 }
 
 // ---- persistent stepping ----------------------------------------------------
@@ -167,28 +280,34 @@ __global__ void __launch_bounds__(THREADS) tiled_evolve_kernel(const double2* __
                                                                double2* v0, double2* v1,
                                                                int batch, int64_t steps,
                                                                StepCtl* ctl) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ int s_tile;
-  const TileCtx c;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const Ring r = carve(smem_raw);
+  init_ring(r);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_m = (n + BM - 1) / BM, tiles_n = (batch + BN - 1) / BN;
   const int ntiles = tiles_m * tiles_n;
   double2* cur = v0;
   double2* nxt = v1;
+  int stage = 0;
+  unsigned phase = 0;
   for (int64_t s = 0; s < steps; ++s) {
     const int par = int(s & 1);
-    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->tile_ctr[par ^ 1] = 0u;  // next step's counter
-    while (true) {
-      if (threadIdx.x == 0) s_tile = int(atomicAdd(&ctl->tile_ctr[par], 1u));
-      __syncthreads();
-      const int t = s_tile;
-      __syncthreads();
-      if (t >= ntiles) break;
-      // column-major tile order: consecutive CTAs share the same V columns
-      const int tm = t % tiles_m, tn = t / tiles_m;
-      double acc[2][2][2];
-      gemm_tile(P, n, cur, batch, n, batch, n, tm * BM, tn * BN, acc,
-                reinterpret_cast<double2*>(smem_raw), c);
-      store_tile(nxt, batch, n, batch, tm * BM, tn * BN, acc, c);
+    const Problem p{P, n, cur, batch, nxt, batch, n, batch, n};
+    if (warp == CWARPS) {
+      // generic-proxy stores of the previous step -> async-proxy (bulk copy) reads
+      asm volatile("fence.proxy.async.global;\n" ::: "memory");
+      if (blockIdx.x == 0 && lane == 0) ctl->tile_ctr[par ^ 1] = 0u;  // next step's counter
+      while (true) {
+        int t = 0;
+        if (lane == 0) t = int(atomicAdd(&ctl->tile_ctr[par], 1u));
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= ntiles) break;
+        // column-major tile order: consecutive tiles share the same V columns
+        produce_tile(r, p, t, (t % tiles_m) * BM, (t / tiles_m) * BN, stage, phase, lane);
+      }
+      produce_end(r, stage, phase, lane);
+    } else {
+      consume(r, p, tiles_m, stage, phase, warp, lane);
     }
     grid_barrier(&ctl->barrier, unsigned(s + 1) * gridDim.x);
     double2* tmp = cur;
