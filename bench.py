@@ -226,7 +226,8 @@ class Runner:
 
 def max_over_ranks(torch, x: float) -> float:
     if torch.distributed.is_initialized():
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        on_gpu = torch.distributed.get_backend() == "nccl"
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if on_gpu else "cpu")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
     return x
@@ -238,10 +239,19 @@ def run_ours(args):
     import paper_2603_18052_b200 as lbg
 
     rank, world, local = dist_env()
+    # LBG_BENCH_SHARED_GPU=1 (tests only): every rank on cuda:0 with a gloo
+    # process group, to exercise the multi-rank path on a single GPU. No kernel
+    # waits on another rank, so sharing a GPU cannot deadlock.
+    shared = os.environ.get("LBG_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1 and not torch.distributed.is_initialized():
-        torch.distributed.init_process_group("nccl", device_id=dev)
+        if shared:
+            torch.distributed.init_process_group("gloo")
+        else:
+            torch.distributed.init_process_group("nccl", device_id=dev)
     lbg.lib()
     R = Runner(torch, lbg, dev, rank)
     cfg = args.config
@@ -360,8 +370,14 @@ class SweepCase:
 
     def run(self):
         self.lbg.evolve_sweep_dev(*self.args, self.pops, self.ens, self.work, mode=self.mode)
-        if self.torch.distributed.is_initialized():
-            self.torch.distributed.all_reduce(self.ens)
+        dist = self.torch.distributed
+        if dist.is_initialized():  # the engine's only collective: ensemble sum
+            if dist.get_backend() == "nccl":
+                dist.all_reduce(self.ens)
+            else:
+                host = self.ens.cpu()
+                dist.all_reduce(host)
+                self.ens.copy_(host)
 
     def e2e(self, reps=2):
         T, dev = self.torch, self.dev

@@ -51,16 +51,29 @@ __global__ void __launch_bounds__(32 * kWarps) chain_kernel(const double2* __res
       v0[lane] = x_aos[t * R + lane];
   }
   __syncwarp();
+  // lanes >= R compute too (zero coefficients) and write a dummy slot, so the
+  // step loop has no divergent branch
+  const int slot = active ? lane : R;
+#pragma unroll 1
   for (int64_t s = 0; s < steps; ++s) {
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    // issue every broadcast load of the state first: one shared-memory latency per step
+    double2 vv[N];
 #pragma unroll
-    for (int k = 0; k < R; k += 2) {
-      const double2 vv = *reinterpret_cast<const double2*>(v0 + k);
-      acc[(k >> 1) & 3] = fma(coef[k], vv.x, acc[(k >> 1) & 3]);
-      acc[(k >> 1) & 3] = fma(coef[k + 1], vv.y, acc[(k >> 1) & 3]);
+    for (int j = 0; j < N; ++j) vv[j] = *reinterpret_cast<const double2*>(v0 + 2 * j);
+    constexpr int NA = N >= 6 ? 6 : N;
+    double acc[NA];
+#pragma unroll
+    for (int a = 0; a < NA; ++a) acc[a] = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      acc[j % NA] = fma(coef[2 * j], vv[j].x, acc[j % NA]);
+      acc[j % NA] = fma(coef[2 * j + 1], vv[j].y, acc[j % NA]);
     }
-    const double out = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-    if (active) v1[lane] = out;
+#pragma unroll
+    for (int w = 1; w < NA; w *= 2)
+#pragma unroll
+      for (int a = 0; a + w < NA; a += 2 * w) acc[a] += acc[a + w];
+    v1[slot] = acc[0];
     __syncwarp();
     double* tmp = v0;
     v0 = v1;
