@@ -228,53 +228,54 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 // K3: x <- P_R x for `steps` steps, P_R register resident.
-constexpr int CH = 8, CW = 11;  // 8 column chunks of 11 (88)
-__global__ void __launch_bounds__(THREADS) ptm_step_kernel(const double* __restrict__ p_r,
-                                                           const double* __restrict__ x0, int64_t steps,
-                                                           double* __restrict__ pops,
-                                                           double* __restrict__ ens_x) {
+// One thread per row of P_R: the whole 81-double row lives in registers, so a
+// step is 81 FMAs on broadcast loads of x, one store and one 3-warp barrier —
+// no cross-thread reduction. ~200 registers x 96 threads lets 3 trajectories
+// share an SM; the FP64 pipe, not latency, bounds the step.
+// DFMA latency is 23 cycles on B200 (profiles/r01_latency_probe.json), so the
+// 81-term dot product runs as 12 independent chains (depth 7) and the loads of
+// x are issued in 4 blocks (compiler barrier) to keep the register count at
+// 3 CTAs per SM.
+constexpr int STEP_THREADS = 96;
+constexpr int NACC = 12;
+__global__ void __maxnreg__(224) ptm_step_kernel(const double* __restrict__ p_r,
+                                                                  const double* __restrict__ x0,
+                                                                  int64_t steps, double* __restrict__ pops,
+                                                                  double* __restrict__ ens_x) {
   __shared__ __align__(16) double xs[2][88];
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int rp = w * 4 + (lane >> 3);  // row pair 0..43 (41 used)
-  const int ch = lane & 7;             // column chunk
-  const int r0 = 2 * rp, r1 = 2 * rp + 1;
-  const double* pb = p_r + size_t(blockIdx.x) * N * N;
-  double p0[CW], p1[CW];
+  const int tid = threadIdx.x;
+  const int row = tid < N ? tid : N - 1;  // idle lanes shadow the last row
+  const double* pb = p_r + size_t(blockIdx.x) * N * N + size_t(row) * N;
+  double p[N];
 #pragma unroll
-  for (int jj = 0; jj < CW; ++jj) {
-    const int c = ch * CW + jj;
-    p0[jj] = (r0 < N && c < N) ? pb[r0 * N + c] : 0.0;
-    p1[jj] = (r1 < N && c < N) ? pb[r1 * N + c] : 0.0;
-  }
-  for (int e = tid; e < 88; e += THREADS) {
+  for (int j = 0; j < N; ++j) p[j] = pb[j];
+  for (int e = tid; e < 88; e += STEP_THREADS) {
     xs[0][e] = e < N ? x0[e] : 0.0;
     xs[1][e] = 0.0;
   }
   __syncthreads();
+  const int slot = tid < N ? tid : N;  // idle lanes write a dummy slot
   int cur = 0;
+#pragma unroll 1
   for (int64_t s = 0; s < steps; ++s) {
-    const double* x = xs[cur] + ch * CW;
-    double s0 = 0.0, s1 = 0.0, u0 = 0.0, u1 = 0.0;
+    const double* x = xs[cur];
+    double acc[NACC];
 #pragma unroll
-    for (int jj = 0; jj < CW; jj += 2) {
-      s0 = fma(p0[jj], x[jj], s0);
-      s1 = fma(p1[jj], x[jj], s1);
-      if (jj + 1 < CW) {
-        u0 = fma(p0[jj + 1], x[jj + 1], u0);
-        u1 = fma(p1[jj + 1], x[jj + 1], u1);
-      }
-    }
-    s0 += u0;
-    s1 += u1;
+    for (int a = 0; a < NACC; ++a) acc[a] = 0.0;
 #pragma unroll
-    for (int o = 1; o < CH; o <<= 1) {
-      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    for (int j = 0; j + 1 < N; j += 2) {
+      if (j % 20 == 0) asm volatile("" ::: "memory");  // bound how far loads are hoisted
+      const double2 v = *reinterpret_cast<const double2*>(x + j);
+      acc[j % NACC] = fma(p[j], v.x, acc[j % NACC]);
+      acc[(j + 1) % NACC] = fma(p[j + 1], v.y, acc[(j + 1) % NACC]);
     }
-    if (ch == 0 && r0 < N) {
-      xs[cur ^ 1][r0] = s0;
-      if (r1 < N) xs[cur ^ 1][r1] = s1;
-    }
+    acc[(N - 1) % NACC] = fma(p[N - 1], x[N - 1], acc[(N - 1) % NACC]);
+#pragma unroll
+    for (int w = 1; w < NACC; w *= 2)
+#pragma unroll
+      for (int a = 0; a + w < NACC; a += 2 * w) acc[a] += acc[a + w];
+    const double y = acc[0];
+    xs[cur ^ 1][slot] = y;
     __syncthreads();
     cur ^= 1;
   }
@@ -345,7 +346,7 @@ void launch_ptm_sweep(size_t d, const double* h0, const double* hd, const double
                                               reinterpret_cast<const double2*>(hs), delta + c0, scale + c0,
                                               dt, pr);
     LBG_CHECK_LAUNCH("ptm_expm_kernel");
-    ptm_step_kernel<<<cb, THREADS, 0, s>>>(pr, x0, steps, pops + c0 * int64_t(D), ens_x);
+    ptm_step_kernel<<<cb, STEP_THREADS, 0, s>>>(pr, x0, steps, pops + c0 * int64_t(D), ens_x);
     LBG_CHECK_LAUNCH("ptm_step_kernel");
   }
   x_to_rho_kernel<<<1, 96, 0, s>>>(ens_x, reinterpret_cast<double2*>(ens_sum));
