@@ -22,9 +22,12 @@
 //   three 88x92 padded matrices in shared memory, A and A^2 also kept at each
 //   thread's own accumulator positions so the Horner epilogues never re-read
 //   them. Writes P_R (n x n) to global memory.
-// K3 (ptm_step_kernel): one CTA per trajectory; P_R register resident (each
-//   thread a 2-row x 11-column block), x in shared memory; per step 22 FMAs,
-//   3-level shuffle reduction, one barrier. Epilogue: populations + ensemble sum.
+// K3 (ptm_step_kernel): one CTA per trajectory; P_R register resident (one
+//   row of 81 doubles per thread), x in shared memory; per step 81 FMAs in 12
+//   chains on broadcast loads, one barrier. The SM register file (P_R = 13k
+//   registers per trajectory) caps residency at 2 trajectories per SM, which
+//   bounds this kernel (ncu: 6 warps/SM, FP64 pipe ~40%, "wait" stalls).
+//   Epilogue: populations + ensemble sum.
 #include <algorithm>
 #include <cmath>
 
@@ -41,11 +44,10 @@ constexpr int MAT = 88 * RS;          // doubles per padded matrix
 constexpr int WARPS = 11, THREADS = 32 * WARPS;
 constexpr double kTheta14 = 0.53;
 
-__device__ __forceinline__ double2 kron_l(const double2* __restrict__ dis, const double2* __restrict__ h,
-                                          int q, int p) {
-  // L[q][p] = D[q][p] - i (H[i][j] d_kl - d_ij H[l][k]),  q = (i,k), p = (j,l)
+// coherent Kronecker entries  C[q][p] = -i (H[i][j] d_kl - d_ij H[l][k]),  q = (i,k), p = (j,l)
+__device__ __forceinline__ double2 kron_c(const double2* __restrict__ h, int q, int p) {
   const int i = q / D, k = q - i * D, j = p / D, l = p - j * D;
-  double2 v = dis[q * N + p];
+  double2 v = make_double2(0.0, 0.0);
   if (k == l) {
     const double2 a = h[i * D + j];
     v.x += a.y;
@@ -57,6 +59,30 @@ __device__ __forceinline__ double2 kron_l(const double2* __restrict__ dis, const
     v.y += a.x;
   }
   return v;
+}
+
+// Real-representation entry L_R[q][s] of a complex generator given entry-wise.
+template <class F>
+__device__ __forceinline__ double real_entry(F&& lq, int q, int s) {
+  const int si = s / D, sj = s - si * D;
+  double2 c;
+  if (si == sj) {
+    c = lq(s);
+  } else {
+    const double2 a = lq(s), bt = lq(sj * D + si);
+    c = si < sj ? make_double2(a.x + bt.x, a.y + bt.y) : make_double2(a.y - bt.y, bt.x - a.x);
+  }
+  const int qi = q / D, qj = q - qi * D;
+  return qi <= qj ? c.x : -c.y;
+}
+
+// D_R: the trajectory-independent dissipator part of L_R, from the complex
+// Kronecker-assembled D (k_model.cu build_lindbladian_kernel with H = 0).
+__global__ void ptm_dissipator_kernel(const double2* __restrict__ dis, double* __restrict__ dr) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= N * N) return;
+  const int q = e / N, s = e - q * N;
+  dr[e] = real_entry([&](int p) { return dis[q * N + p]; }, q, s);
 }
 
 // acc[m][0..1] = (X * Y)[m*8 + g][w*8 + 2t .. +1], X, Y padded 88 x RS
@@ -113,7 +139,7 @@ __device__ __forceinline__ void horner_epilogue(double (&acc)[MT][2],
 }
 
 __global__ void __launch_bounds__(THREADS, 1)
-    ptm_expm_kernel(const double2* __restrict__ dis, const double2* __restrict__ h0,
+    ptm_expm_kernel(const double* __restrict__ dr, const double2* __restrict__ h0,
                     const double2* __restrict__ hd, const double2* __restrict__ hs,
                     const double* __restrict__ delta, const double* __restrict__ scale, double dt,
                     double* __restrict__ p_out) {
@@ -134,17 +160,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   // ---- K5: A_R = L_R (unscaled) into S0 ----
   for (int e = tid; e < N * N; e += THREADS) {
     const int q = e / N, s = e - q * N;
-    const int si = s / D, sj = s - si * D;
-    const int st = sj * D + si;
-    double2 c;
-    if (si == sj) {
-      c = kron_l(dis, hb, q, s);
-    } else {
-      const double2 a = kron_l(dis, hb, q, s), bt = kron_l(dis, hb, q, st);
-      c = si < sj ? make_double2(a.x + bt.x, a.y + bt.y) : make_double2(a.y - bt.y, bt.x - a.x);
-    }
-    const int qi = q / D, qj = q - qi * D;
-    S0[q * RS + s] = qi <= qj ? c.x : -c.y;
+    S0[q * RS + s] = dr[e] + real_entry([&](int p) { return kron_c(hb, q, p); }, q, s);
   }
   __syncthreads();
   // ||A dt||_1 -> squarings (per trajectory)
@@ -309,7 +325,8 @@ constexpr int64_t kChunk = 16384;
 
 size_t ptm_sweep_workspace(int64_t batch) {
   const size_t chunk = size_t(std::min<int64_t>(std::max<int64_t>(batch, 1), kChunk));
-  return align_up(chunk * N * N * 8) + align_up(size_t(N) * N * 16) + align_up(2 * N * 8) + 256;
+  return align_up(chunk * N * N * 8) + align_up(size_t(N) * N * 16) + align_up(2 * N * 8) +
+         align_up(size_t(N) * N * 8) + 256;
 }
 
 bool ptm_sweep_supported(size_t d) { return d == size_t(D); }
@@ -326,10 +343,14 @@ void launch_ptm_sweep(size_t d, const double* h0, const double* hd, const double
   double* xv = reinterpret_cast<double*>(w + align_up(chunk * N * N * 8) + align_up(size_t(N) * N * 16));
   double* x0 = xv;
   double* ens_x = xv + N;
+  double* dr = reinterpret_cast<double*>(w + align_up(chunk * N * N * 8) + align_up(size_t(N) * N * 16) +
+                                         align_up(2 * N * 8));
   // dissipator D = build_lindbladian(H = 0, ops) (K5, shared by all trajectories)
   check_cuda(cudaMemsetAsync(ens_x, 0, N * 8, s), "memset");
   check_cuda(cudaMemsetAsync(pr, 0, d * d * 16, s), "memset");
   launch_build_lindbladian(d, pr, n_ops, ops, reinterpret_cast<double*>(dis), s);
+  ptm_dissipator_kernel<<<(N * N + 255) / 256, 256, 0, s>>>(dis, dr);
+  LBG_CHECK_LAUNCH("ptm_dissipator_kernel");
   rho_to_x_kernel<<<1, 96, 0, s>>>(reinterpret_cast<const double2*>(rho0), x0);
   LBG_CHECK_LAUNCH("rho_to_x_kernel");
   const size_t smem = size_t(3) * MAT * 8;
@@ -341,7 +362,7 @@ void launch_ptm_sweep(size_t d, const double* h0, const double* hd, const double
   (void)attr;
   for (int64_t c0 = 0; c0 < batch; c0 += int64_t(chunk)) {
     const int cb = int(std::min<int64_t>(int64_t(chunk), batch - c0));
-    ptm_expm_kernel<<<cb, THREADS, smem, s>>>(dis, reinterpret_cast<const double2*>(h0),
+    ptm_expm_kernel<<<cb, THREADS, smem, s>>>(dr, reinterpret_cast<const double2*>(h0),
                                               reinterpret_cast<const double2*>(hd),
                                               reinterpret_cast<const double2*>(hs), delta + c0, scale + c0,
                                               dt, pr);
