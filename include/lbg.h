@@ -124,6 +124,20 @@ int lbg_evolve_sweep_dev(size_t d, const double* h0, const double* hd, const dou
                          void* stream);
 
 /* ------------------------------------------------------------------------
+ * GRAPE piecewise-constant chain: replaces lb::grape_chain (propagate.hpp:54-58,
+ * propagate.cpp:111-168). Segment j evolves the state steps_per_segment steps
+ * with P_j = exp(dt L(h0 + amplitudes[j] hc, ops)). All P_j are built in one
+ * batched GPU pass (timed as build_ms), then the chain runs on the step kernels
+ * (chain_ms), like ChainTimings (propagate.hpp:37-43). Host buffers: h0, hc
+ * (d x d AoS), ops (n_ops x d x d), amplitudes (segments), rho0 / out (d x d).
+ * rho0 must pass check_state (1e-8); h0 + a hc must be Hermitian (1e-12).
+ * ------------------------------------------------------------------------ */
+int lbg_grape_chain(size_t d, const double* h0, const double* hc, const double* amplitudes,
+                    int64_t segments, int64_t steps_per_segment, double dt, size_t n_ops,
+                    const double* ops, const double* rho0, double* out, double* build_ms,
+                    double* chain_ms);
+
+/* ------------------------------------------------------------------------
  * Batched invariant check: replaces lb::check_state (validate.hpp:22,
  * validate.cpp:10-30) over a batch. x: batch x d x d AoS (device).
  * Writes the max over the batch of |Tr rho - 1| and max|rho_ij - conj rho_ji|,

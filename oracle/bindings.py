@@ -226,6 +226,35 @@ class Reference:
                                            _ptr(out), threads, C.byref(secs)), "evolve_batch")
         return out, secs.value
 
+    def grape_inputs(self, d, segments, seed=42):
+        """cmd_grape's seeded inputs (commands.cpp:123-159)."""
+        L = self.lib
+        L.ref_grape_inputs.argtypes = [C.c_size_t, C.c_size_t, C.c_uint64] + [_dp] * 6
+        h0 = np.zeros((d, d), np.complex128)
+        hc = np.zeros((d, d), np.complex128)
+        op = np.zeros((1, d, d), np.complex128)
+        amps = np.zeros(segments)
+        dt = C.c_double()
+        rho0 = np.zeros((d, d), np.complex128)
+        self._rc(L.ref_grape_inputs(d, segments, seed, _ptr(h0), _ptr(hc), _ptr(op), _ptr(amps), C.byref(dt),
+                                    _ptr(rho0)), "grape_inputs")
+        return h0, hc, op, amps, dt.value, rho0
+
+    def grape_chain(self, h0, hc, amps, steps, dt, ops, rho0):
+        """lb::grape_chain (propagate.cpp:111-168). Returns (final rho, build_ms, chain_ms)."""
+        L = self.lib
+        L.ref_grape_chain.argtypes = [C.c_size_t, _dp, _dp, _dp, C.c_size_t, C.c_size_t, C.c_double,
+                                      C.c_size_t, _dp, _dp, _dp, _dp, _dp]
+        h0, hc, rho0 = (np.ascontiguousarray(x, np.complex128) for x in (h0, hc, rho0))
+        d = h0.shape[0]
+        ops = np.ascontiguousarray(np.asarray(ops, np.complex128).reshape(-1, d, d))
+        amps = np.ascontiguousarray(amps, np.float64)
+        out = np.zeros_like(rho0)
+        b, c = C.c_double(), C.c_double()
+        self._rc(L.ref_grape_chain(d, _ptr(h0), _ptr(hc), _ptr(amps), amps.shape[0], steps, dt, ops.shape[0],
+                                   _ptr(ops), _ptr(rho0), _ptr(out), C.byref(b), C.byref(c)), "grape_chain")
+        return out, b.value, c.value
+
     def sweep_batch(self, deltas, scales, steps=500, threads=1):
         """Config 4 through the reference. Returns (pops (B,9), ens_sum (9,9), seconds)."""
         deltas = np.ascontiguousarray(deltas, np.float64)

@@ -28,6 +28,7 @@
 #include "lb/kernels.hpp"
 #include "lb/lindblad.hpp"
 #include "lb/propagate.hpp"
+#include "lb/random.hpp"
 #include "lb/validate.hpp"
 
 using lb::cplx;
@@ -244,6 +245,51 @@ int ref_sweep_batch(const double* deltas, const double* scales, std::int64_t bat
         for (const auto& acc : partial)
             for (std::size_t e = 0; e < 2 * d * d; ++e) ens_sum[e] += acc[e];
     });
+}
+
+// Inputs of the reference GRAPE benchmark exactly as cmd_grape draws them
+// (commands.cpp:123-159): h0 = random_hermitian(rng(seed), d), dissipator
+// 0.1 a, hc = (a + a^dag)/2, amplitudes U[-1,1] from the same rng, dt =
+// auto_dt of the first segment's generator, rho0 = |d-1><d-1|.
+int ref_grape_inputs(std::size_t d, std::size_t segments, std::uint64_t seed, double* h0,
+                     double* hc, double* op, double* amps, double* dt, double* rho0) {
+  return guarded([&] {
+    auto rng = lb::make_rng(seed);
+    const MatrixAoS h = lb::random_hermitian(rng, d);
+    const MatrixAoS dis = cplx{0.1, 0.0} * lb::lowering_operator(d);
+    const MatrixAoS a = lb::lowering_operator(d);
+    const MatrixAoS c = cplx{0.5, 0.0} * (a + lb::dagger(a));
+    std::uniform_real_distribution<double> u(-1.0, 1.0);
+    for (std::size_t j = 0; j < segments; ++j) amps[j] = u(rng);
+    MatrixAoS h1 = h;
+    lb::add_scaled(h1, cplx{amps[0], 0.0}, c);
+    const double nrm = lb::one_norm(lb::build_lindbladian(lb::make_model(std::move(h1), {dis})).matrix);
+    *dt = nrm > 0.0 ? 0.01 / nrm : 1.0;  // auto_dt, commands.cpp:38-41
+    MatrixAoS r(d, d);
+    r(d - 1, d - 1) = cplx{1.0, 0.0};
+    to_buf(h, h0);
+    to_buf(c, hc);
+    to_buf(dis, op);
+    to_buf(r, rho0);
+  });
+}
+
+// lb::grape_chain (propagate.cpp:111-168) with the native-fast profile, SoA.
+int ref_grape_chain(std::size_t d, const double* h0, const double* hc, const double* amps,
+                    std::size_t segments, std::size_t steps, double dt, std::size_t n_ops,
+                    const double* ops, const double* rho0, double* out, double* build_ms,
+                    double* chain_ms) {
+  return guarded([&] {
+    std::vector<MatrixAoS> ls;
+    for (std::size_t k = 0; k < n_ops; ++k) ls.push_back(from_buf(ops + 2 * k * d * d, d, d));
+    const std::vector<double> a(amps, amps + segments);
+    const lb::GrapeResult g = lb::grape_chain(from_buf(h0, d, d), from_buf(hc, d, d), a, steps, dt, ls,
+                                              from_buf(rho0, d, d), lb::Variant::soa,
+                                              lb::find_profile("native-fast"));
+    to_buf(g.final_state, out);
+    *build_ms = g.timings.build_ms;
+    *chain_ms = g.timings.chain_ms;
+  });
 }
 
 int ref_check_state(const double* rho, std::size_t d, double tol, double* trace_err,

@@ -389,6 +389,65 @@ int lbg_evolve_sweep_dev(size_t d, const double* h0, const double* hd, const dou
   });
 }
 
+int lbg_grape_chain(size_t d, const double* h0, const double* hc, const double* amplitudes,
+                    int64_t segments, int64_t steps_per_segment, double dt, size_t n_ops,
+                    const double* ops, const double* rho0, double* out, double* build_ms,
+                    double* chain_ms) {
+  return guarded([&] {
+    // propagate.cpp:116-118
+    if (segments <= 0 || !amplitudes) throw invalid_argument("grape_chain: amplitudes are empty");
+    if (d == 0 || !h0 || !hc || !rho0 || !out) throw invalid_argument("grape_chain: operator shapes do not conform");
+    if (steps_per_segment < 0) throw invalid_argument("grape_chain: negative steps");
+    if (!std::isfinite(dt)) throw invalid_argument("expm: dt must be finite");
+    // make_model's Hermiticity check on every segment Hamiltonian (lindblad.cpp:28-29)
+    std::vector<double> h(2 * d * d);
+    for (int64_t j = 0; j < segments; ++j) {
+      for (size_t e = 0; e < 2 * d * d; ++e) h[e] = h0[e] + amplitudes[j] * hc[e];
+      if (!is_hermitian(h.data(), d))
+        throw invalid_argument("make_model: Hamiltonian is not Hermitian within 1e-12");
+    }
+    double chk[3];
+    {
+      DevBuf dr(2 * d * d * 8), dc(3 * 8);
+      check_cuda(cudaMemcpy(dr.p, rho0, 2 * d * d * 8, cudaMemcpyHostToDevice), "H2D");
+      launch_check_state(dr.as<double>(), d, 1, dc.as<double>(), nullptr);
+      check_cuda(cudaMemcpy(chk, dc.p, sizeof chk, cudaMemcpyDeviceToHost), "D2H");
+    }
+    if (!(chk[0] <= 1e-8 && chk[1] <= 1e-8 && chk[2] >= -1e-8))
+      throw invalid_argument("evolve: initial state fails physical-state checks");
+    const size_t dd = d * d;
+    std::vector<double> zeros(size_t(segments), 0.0);
+    DevBuf dh0(dd * 16), dhc(dd * 16), dz(dd * 16), dops(n_ops * dd * 16 + 16), damp(size_t(segments) * 8),
+        dzs(size_t(segments) * 8), dx(dd * 16), dw(grape_workspace(d, segments));
+    check_cuda(cudaMemcpy(dh0.p, h0, dd * 16, cudaMemcpyHostToDevice), "H2D");
+    check_cuda(cudaMemcpy(dhc.p, hc, dd * 16, cudaMemcpyHostToDevice), "H2D");
+    check_cuda(cudaMemset(dz.p, 0, dd * 16), "memset");
+    if (n_ops) check_cuda(cudaMemcpy(dops.p, ops, n_ops * dd * 16, cudaMemcpyHostToDevice), "H2D");
+    check_cuda(cudaMemcpy(damp.p, amplitudes, size_t(segments) * 8, cudaMemcpyHostToDevice), "H2D");
+    check_cuda(cudaMemcpy(dzs.p, zeros.data(), size_t(segments) * 8, cudaMemcpyHostToDevice), "H2D");
+    check_cuda(cudaMemcpy(dx.p, rho0, dd * 16, cudaMemcpyHostToDevice), "H2D");
+    cudaEvent_t e0, e1, e2;
+    check_cuda(cudaEventCreate(&e0), "event");
+    check_cuda(cudaEventCreate(&e1), "event");
+    check_cuda(cudaEventCreate(&e2), "event");
+    check_cuda(cudaEventRecord(e0, nullptr), "event");
+    launch_grape(d, dh0.as<double>(), dhc.as<double>(), dz.as<double>(), n_ops, dops.as<double>(),
+                 damp.as<double>(), dzs.as<double>(), segments, steps_per_segment, dt, dx.as<double>(), dw.p,
+                 nullptr, e1);
+    check_cuda(cudaEventRecord(e2, nullptr), "event");
+    check_cuda(cudaEventSynchronize(e2), "sync");
+    float b = 0.f, c = 0.f;
+    check_cuda(cudaEventElapsedTime(&b, e0, e1), "elapsed");
+    check_cuda(cudaEventElapsedTime(&c, e1, e2), "elapsed");
+    if (build_ms) *build_ms = b;
+    if (chain_ms) *chain_ms = c;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+    check_cuda(cudaMemcpy(out, dx.p, dd * 16, cudaMemcpyDeviceToHost), "D2H");
+  });
+}
+
 int lbg_check_state_batched_dev(const double* x, size_t d, int64_t batch, double* out3, void* stream) {
   return guarded([&] {
     if (d == 0 || batch < 0 || !out3) throw invalid_argument("check_state: bad arguments");

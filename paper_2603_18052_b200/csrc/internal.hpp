@@ -68,6 +68,12 @@ void launch_step_once(const double* p, const double* v, double* out, std::size_t
 
 // K3/K4/K5 fused per-trajectory sweep (k_sweep.cu)
 std::size_t sweep_workspace(std::size_t d, int64_t batch);
+// GRAPE chain: batched segment propagators, then the sequential chain (k_sweep.cu)
+std::size_t grape_workspace(std::size_t d, int64_t segments);
+void launch_grape(std::size_t d, const double* h0, const double* hc, const double* zero_h,
+                  std::size_t n_ops, const double* ops, const double* amps, const double* zeros,
+                  int64_t segments, int64_t steps_per_segment, double dt, double* x, void* work,
+                  cudaStream_t s, cudaEvent_t ev_build_end);
 void launch_sweep(std::size_t d, const double* h0, const double* hd, const double* hs,
                   std::size_t n_ops, const double* ops, const double* delta, const double* scale,
                   double dt, const double* rho0, int64_t batch, int64_t steps, double* pops,

@@ -159,12 +159,15 @@ size_t sweep_workspace(size_t d, int64_t batch) {
   return 7 * align_up(chunk * n * n * 16) + align_up(n * n * 16) + 256;
 }
 
-void launch_sweep(size_t d, const double* h0, const double* hd, const double* hs, size_t n_ops,
-                  const double* ops, const double* delta, const double* scale, double dt,
-                  const double* rho0, int64_t batch, int64_t steps, double* pops, double* ens_sum,
-                  void* work, cudaStream_t s) {
-  if (!work) throw invalid_argument("sweep: workspace required");
-  if (d * d > 96) throw invalid_argument("sweep: supports d*d <= 96");
+// Batched complex propagators P_b = exp(dt (D + C(h0 + delta_b hd + scale_b hs)))
+// for b in [0, batch), chunk by chunk: K5 assembly, one norm pass (common
+// squaring count), Taylor-16 / Paterson-Stockmeyer on the batched DMMA GEMM.
+// on_chunk(P, c0, cb) runs after chunk [c0, c0+cb)'s propagators are ready.
+namespace {
+template <class F>
+void propagators_complex(size_t d, const double* h0, const double* hd, const double* hs, size_t n_ops,
+                         const double* ops, const double* delta, const double* scale, double dt,
+                         int64_t batch, void* work, cudaStream_t s, F&& on_chunk) {
   const int n = int(d * d);
   const long long nn = (long long)n * n;
   const size_t chunk = size_t(std::min<int64_t>(std::max<int64_t>(batch, 1), kChunk));
@@ -179,7 +182,6 @@ void launch_sweep(size_t d, const double* h0, const double* hd, const double* hs
   check_cuda(cudaMemsetAsync(M[0], 0, d * d * 16, s), "memset");
   launch_build_lindbladian(d, reinterpret_cast<const double*>(M[0]), n_ops, ops,
                            reinterpret_cast<double*>(dis), s);
-  check_cuda(cudaMemsetAsync(ens_sum, 0, nn > 0 ? size_t(n) * 16 : 0, s), "memset ens");
   if (batch == 0) return;
 
   // one pass over all trajectories' norms fixes a common squaring count
@@ -208,9 +210,6 @@ void launch_sweep(size_t d, const double* h0, const double* hd, const double* hs
 
   double c[17];
   for (int k = 0; k <= 16; ++k) c[k] = inv_fact(k);
-  const size_t smem = size_t(nn + 2 * n) * 16;
-  check_cuda(cudaFuncSetAttribute(sweep_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
-             "smem attr");
   double2 *A1 = M[0], *A2 = M[1], *A3 = M[2], *A4 = M[3], *T = M[4], *MM = M[5], *P = M[6];
   for (int64_t c0 = 0; c0 < batch; c0 += int64_t(chunk)) {
     const int cb = int(std::min<int64_t>(int64_t(chunk), batch - c0));
@@ -241,9 +240,66 @@ void launch_sweep(size_t d, const double* h0, const double* hd, const double* hs
       mm(cur, cur, dst);
       cur = dst;
     }
-    sweep_step_kernel<<<cb, 96, smem, s>>>(P, nn, reinterpret_cast<const double2*>(rho0), int(d), steps,
-                                           pops + c0 * int64_t(d), ens_sum);
-    LBG_CHECK_LAUNCH("sweep_step_kernel");
+    on_chunk(P, c0, cb);
+  }
+}
+
+}  // namespace
+
+void launch_sweep(size_t d, const double* h0, const double* hd, const double* hs, size_t n_ops,
+                  const double* ops, const double* delta, const double* scale, double dt,
+                  const double* rho0, int64_t batch, int64_t steps, double* pops, double* ens_sum,
+                  void* work, cudaStream_t s) {
+  if (!work) throw invalid_argument("sweep: workspace required");
+  if (d * d > 96) throw invalid_argument("sweep: supports d*d <= 96");
+  const int n = int(d * d);
+  const long long nn = (long long)n * n;
+  check_cuda(cudaMemsetAsync(ens_sum, 0, size_t(n) * 16, s), "memset ens");
+  const size_t smem = size_t(nn + 2 * n) * 16;
+  check_cuda(cudaFuncSetAttribute(sweep_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+             "smem attr");
+  propagators_complex(d, h0, hd, hs, n_ops, ops, delta, scale, dt, batch, work, s,
+                      [&](const double2* P, int64_t c0, int cb) {
+                        sweep_step_kernel<<<cb, 96, smem, s>>>(P, nn, reinterpret_cast<const double2*>(rho0),
+                                                               int(d), steps, pops + c0 * int64_t(d), ens_sum);
+                        LBG_CHECK_LAUNCH("sweep_step_kernel");
+                      });
+}
+
+size_t grape_workspace(size_t d, int64_t segments) {
+  const size_t n = d * d;
+  return sweep_workspace(d, segments) + align_up(size_t(segments) * n * n * 16) + align_up(n * 16) +
+         tiled_workspace(n, 1);
+}
+
+// GRAPE piecewise-constant chain (propagate.cpp:111-168): every segment's
+// propagator P_j = exp(dt L(h0 + a_j hc)) is independent of the state, so all
+// of them are built in ONE batched pass (timed as build), then the state walks
+// the chain segment by segment on the step kernels (timed as chain).
+void launch_grape(size_t d, const double* h0, const double* hc, const double* zero_h, size_t n_ops,
+                  const double* ops, const double* amps, const double* zeros, int64_t segments,
+                  int64_t steps_per_segment, double dt, double* x, void* work, cudaStream_t s,
+                  cudaEvent_t ev_build_end) {
+  const size_t n = d * d;
+  const long long nn = (long long)n * n;
+  char* w = static_cast<char*>(work);
+  double2* props = reinterpret_cast<double2*>(w + sweep_workspace(d, segments));
+  void* ework = w + sweep_workspace(d, segments) + align_up(size_t(segments) * nn * 16) + align_up(n * 16);
+  propagators_complex(d, h0, hc, zero_h, n_ops, ops, amps, zeros, dt, segments, w, s,
+                      [&](const double2* P, int64_t c0, int cb) {
+                        check_cuda(cudaMemcpyAsync(props + c0 * nn, P, size_t(cb) * nn * 16,
+                                                   cudaMemcpyDeviceToDevice, s),
+                                   "D2D P");
+                      });
+  if (ev_build_end) check_cuda(cudaEventRecord(ev_build_end, s), "event");
+  for (int64_t j = 0; j < segments; ++j) {
+    const double* pj = reinterpret_cast<const double*>(props + j * nn);
+    if (chain_supported(n))
+      launch_chain(pj, n, nullptr, nullptr, x, 1, steps_per_segment, Layout::aos, s);
+    else if (smem_supported(n))
+      launch_smem(pj, n, nullptr, nullptr, x, 1, steps_per_segment, Layout::aos, s);
+    else
+      launch_tiled_evolve(pj, n, nullptr, nullptr, x, 1, steps_per_segment, Layout::aos, ework, s);
   }
 }
 

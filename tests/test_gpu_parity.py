@@ -317,3 +317,57 @@ def test_reference_evolve_drives_the_gpu_kernel():
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "all criteria passed" in r.stdout
+
+
+def test_nccl_allreduce_single_rank(lbg, torch):
+    """lbg_nccl_* + lbg_allreduce_sum_dev (the engine's one collective) on a
+    1-rank communicator: the sum over one rank is the identity."""
+    import ctypes as C
+    L = lbg.lib()
+    uid = C.create_string_buffer(128)
+    assert L.lbg_nccl_unique_id(C.cast(uid, C.c_void_p)) == 0, L.lbg_last_error()
+    comm = C.c_void_p()
+    assert L.lbg_nccl_comm_init(C.byref(comm), 1, C.cast(uid, C.c_void_p), 0) == 0, L.lbg_last_error()
+    buf = torch.arange(162, dtype=torch.float64, device="cuda")
+    want = buf.clone()
+    assert L.lbg_allreduce_sum_dev(C.c_void_p(buf.data_ptr()), 162, comm, None) == 0, L.lbg_last_error()
+    torch.cuda.synchronize()
+    assert torch.equal(buf, want)
+    assert L.lbg_nccl_comm_destroy(comm) == 0
+
+
+# ------------------------------------------------------------ GRAPE chain ---
+@pytest.mark.parametrize("d,segments", [(3, 100), (9, 20), (27, 3)])
+def test_grape_chain_vs_reference(lbg, reference, d, segments):
+    """lbg_grape_chain vs the reference's own lb::grape_chain on cmd_grape's
+    seeded inputs (commands.cpp:123-159; Table IV shapes, fewer segments at d=27)."""
+    h0, hc, op, amps, dt, rho0 = reference.grape_inputs(d, segments)
+    want, _, _ = reference.grape_chain(h0, hc, amps, 32, dt, op, rho0)
+    got, t = lbg.grape_chain(h0, hc, amps, 32, dt, op, rho0)
+    assert np.abs(got - want).max() <= TOL_RHO
+    tr, herm = invariants(got)
+    assert tr <= TOL_INV and herm <= TOL_INV
+    assert t["build_ms"] > 0 and t["chain_ms"] > 0 and t["segments"] == segments
+
+
+def test_grape_constant_pulse_equals_evolve(lbg):
+    """test_propagate.cpp:216-241: a constant pulse is plain evolution."""
+    rng = np.random.default_rng(31)
+    r = rng.uniform(-1, 1, (3, 3)) + 1j * rng.uniform(-1, 1, (3, 3))
+    h0 = 0.5 * (r + r.conj().T)
+    r = rng.uniform(-1, 1, (3, 3)) + 1j * rng.uniform(-1, 1, (3, 3))
+    hc = 0.5 * (r + r.conj().T)
+    a = np.diag(np.sqrt([1.0, 2.0]), 1).astype(complex)
+    dis = [0.2 * a]
+    rho0 = np.zeros((3, 3), complex)
+    rho0[2, 2] = 1.0
+    amp, dt, sps, seg = 0.8, 0.002, 8, 5
+    got, t = lbg.grape_chain(h0, hc, [amp] * seg, sps, dt, dis, rho0)
+    P = lbg.expm(lbg.build_lindbladian(h0 + amp * hc, dis), dt)
+    want = lbg.evolve(P, rho0, seg * sps)
+    assert np.abs(got - want).max() <= 1e-13
+    assert t["steps_per_segment"] == sps
+    with pytest.raises(ValueError):
+        lbg.grape_chain(h0, hc, [], 4, 0.01, dis, rho0)
+    with pytest.raises(ValueError):
+        lbg.grape_chain(h0, np.zeros((2, 2)), [0.5], 4, 0.01, dis, rho0)
