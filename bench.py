@@ -430,7 +430,31 @@ def extra_configs(torch, lbg, R, peak):
             out[f"c{cfg}"] = entry
         except Exception as e:  # noqa: BLE001
             out[f"c{cfg}"] = {"error": str(e)}
+    out["grape"] = grape_table(lbg)
     return out
+
+
+def grape_table(lbg):
+    """GRAPE piecewise-constant chain (Table IV shapes: d=3/100, d=9/50,
+    d=27/20 segments x 32 steps) on cmd_grape's seeded inputs; the reference's
+    lb::grape_chain timed beside it (single-threaded, as the reference is)."""
+    rows = {}
+    try:
+        from oracle.bindings import Reference
+        ref = Reference()
+    except Exception as e:  # noqa: BLE001
+        return {"error": f"reference unavailable: {e}"}
+    for d, seg in ((3, 100), (9, 50), (27, 20)):
+        h0, hc, op, amps, dt, rho0 = ref.grape_inputs(d, seg)
+        lbg.grape_chain(h0, hc, amps, 32, dt, op, rho0)  # warm-up
+        _, t = lbg.grape_chain(h0, hc, amps, 32, dt, op, rho0)
+        row = {"segments": seg, "steps_per_segment": 32, "gpu_build_ms": t["build_ms"],
+               "gpu_chain_ms": t["chain_ms"], "gpu_points_per_s": t["points_per_s"]}
+        if d < 27:
+            _, b, c = ref.grape_chain(h0, hc, amps, 32, dt, op, rho0)
+            row.update(ref_build_ms=b, ref_chain_ms=c, ref_points_per_s=1000.0 / (b + c))
+        rows[f"d{d}"] = row
+    return rows
 
 
 def main():
