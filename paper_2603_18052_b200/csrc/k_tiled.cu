@@ -32,12 +32,24 @@ namespace lbg {
 
 namespace {
 
-constexpr int BM = 32, BN = 32, BK = 16, STAGES = 4;
+constexpr int BM = 32, BK = 16, STAGES = 4;
 constexpr int CWARPS = 8, THREADS = 32 * (CWARPS + 1);
-constexpr int SA = 18, SB = 36;  // complex strides (see header)
-constexpr int A_ELEMS = BM * SA, B_ELEMS = BK * SB;
-constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;  // double2 units
-constexpr size_t kSmemBytes = size_t(STAGES) * STAGE_ELEMS * sizeof(double2) + 256;
+constexpr int SA = 18;  // complex stride of A rows (see header)
+constexpr int A_ELEMS = BM * SA;
+
+// Tile geometry by tile width BN (complex columns): 32 for the expm GEMM, 16 for
+// the stepper (twice the tiles per step -> half the step-tail granularity).
+// Each consumer warp owns MI m8-tiles x NI n8-tiles; the 8 warps form a
+// WM x WN grid. SB = BN + 4 = 4 (mod 8) keeps B fragment loads conflict free.
+template <int BN_>
+struct Geo {
+  static constexpr int BN = BN_, NI = 2, WN = BN_ / (8 * NI), WM = CWARPS / WN, MI = (BM / 4) / WM;
+  static constexpr int SB = BN_ + 4;
+  static constexpr int B_ELEMS = BK * SB;
+  static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;  // double2 units
+  static constexpr size_t kSmemBytes = size_t(STAGES) * STAGE_ELEMS * sizeof(double2) + 256;
+  static_assert(WN * WM == CWARPS && MI * WM * 4 == BM, "tile geometry");
+};
 
 // ---- mbarrier / bulk-copy primitives (PTX) ----------------------------------
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -54,6 +66,25 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, unsigned bytes) {
                : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+#ifdef LBG_DEBUG_WATCHDOG
+  {
+    const long long t0 = clock64();
+    while (true) {
+      unsigned ok;
+      asm volatile(
+          "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+          : "=r"(ok)
+          : "r"(smem_u32(bar)), "r"(parity)
+          : "memory");
+      if (ok) return;
+      if (clock64() - t0 > 4000000000ll) {
+        printf("WATCHDOG block %d thread %d bar_off %u parity %u\n", blockIdx.x, threadIdx.x,
+               smem_u32(bar) & 0xffffu, parity);
+        return;
+      }
+    }
+  }
+#endif
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -79,10 +110,11 @@ struct Ring {
   int* hdr;        // STAGES x 2: tile id (-1 = end of step), k chunk
 };
 
+template <class G>
 __device__ __forceinline__ Ring carve(unsigned char* smem) {
   Ring r;
   r.data = reinterpret_cast<double2*>(smem);
-  unsigned char* tail = smem + size_t(STAGES) * STAGE_ELEMS * sizeof(double2);
+  unsigned char* tail = smem + size_t(STAGES) * G::STAGE_ELEMS * sizeof(double2);
   r.full = reinterpret_cast<uint64_t*>(tail);
   r.empty = r.full + STAGES;
   r.hdr = reinterpret_cast<int*>(r.empty + STAGES);
@@ -107,8 +139,10 @@ __device__ __forceinline__ void advance(int& stage, unsigned& phase) {
 }
 
 // Producer: one warp streams the K chunks of tile (m0, n0) into the ring.
+template <class G>
 __device__ __forceinline__ void produce_tile(const Ring& r, const Problem& p, int tile, int m0, int n0,
                                              int& stage, unsigned& phase, int lane) {
+  constexpr int BN = G::BN, SB = G::SB, STAGE_ELEMS = G::STAGE_ELEMS;
   const int nk = (p.K + BK - 1) / BK;
   const int mrows = min(BM, p.M - m0), ncols = min(BN, p.N - n0);
   for (int kc = 0; kc < nk; ++kc) {
@@ -141,15 +175,19 @@ __device__ __forceinline__ void produce_end(const Ring& r, int& stage, unsigned&
 }
 
 // Consumer warps: run tiles until the end-of-step sentinel.
+template <class G>
 __device__ __forceinline__ void consume(const Ring& r, const Problem& p, int tiles_m, int& stage,
                                        unsigned& phase, int warp, int lane) {
+  constexpr int BN = G::BN, SB = G::SB, STAGE_ELEMS = G::STAGE_ELEMS, MI = G::MI, NI = G::NI;
   const AFragLane af(lane);
-  const int wm = warp >> 1, wn = warp & 1;
+  const int wm = warp / G::WN, wn = warp % G::WN;
   const int nk = (p.K + BK - 1) / BK;
-  const int a_off = 2 * ((wm * 2 * 4 + af.di) * SA + af.dj) + af.comp;
-  const int b_off = 2 * (((lane & 3) >> 1) * SB + wn * 2 * 8 + (lane >> 2)) + (lane & 1);
-  double acc[2][2][2] = {};
-  bool row_ok[2] = {true, true};
+  const int a_off = 2 * ((wm * MI * 4 + af.di) * SA + af.dj) + af.comp;
+  const int b_off = 2 * (((lane & 3) >> 1) * SB + wn * NI * 8 + (lane >> 2)) + (lane & 1);
+  double acc[MI][NI][2] = {};
+  bool row_ok[MI];
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi) row_ok[mi] = true;
   int m0 = 0, n0 = 0;
   while (true) {
     mbar_wait(&r.full[stage], phase);
@@ -164,42 +202,48 @@ __device__ __forceinline__ void consume(const Ring& r, const Problem& p, int til
       m0 = (tile % tiles_m) * BM;
       n0 = (tile / tiles_m) * BN;
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi) {
-        row_ok[mi] = m0 + (wm * 2 + mi) * 4 + af.di < p.M;
+      for (int mi = 0; mi < MI; ++mi) {
+        row_ok[mi] = m0 + (wm * MI + mi) * 4 + af.di < p.M;
 #pragma unroll
-        for (int ni = 0; ni < 2; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+        for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
       }
     }
     const double* ad = reinterpret_cast<const double*>(r.data + stage * STAGE_ELEMS) + a_off;
     const double* bd = reinterpret_cast<const double*>(r.data + stage * STAGE_ELEMS + A_ELEMS) + b_off;
     const int k0 = kc * BK;
-    if (k0 + BK <= p.K && row_ok[0] && row_ok[1]) {
+    bool all_rows = true;
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi) all_rows = all_rows && row_ok[mi];
+    // row_ok depends on the lane's fragment row: the path choice must be
+    // warp-uniform, mma.sync needs all 32 lanes converged
+    all_rows = __all_sync(0xffffffffu, all_rows);
+    if (k0 + BK <= p.K && all_rows) {
 #pragma unroll
       for (int ks = 0; ks < BK / 2; ++ks) {
-        double a[2], b[2];
+        double a[MI], b[NI];
 #pragma unroll
-        for (int mi = 0; mi < 2; ++mi) a[mi] = af.sign(ad[2 * (mi * 4 * SA) + 4 * ks]);
+        for (int mi = 0; mi < MI; ++mi) a[mi] = af.sign(ad[2 * (mi * 4 * SA) + 4 * ks]);
 #pragma unroll
-        for (int ni = 0; ni < 2; ++ni) b[ni] = bd[2 * (2 * ks * SB + ni * 8)];
+        for (int ni = 0; ni < NI; ++ni) b[ni] = bd[2 * (2 * ks * SB + ni * 8)];
 #pragma unroll
-        for (int mi = 0; mi < 2; ++mi)
+        for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-          for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+          for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
       }
     } else {  // ragged edge: rows >= M and k >= K masked in registers
 #pragma unroll
       for (int ks = 0; ks < BK / 2; ++ks) {
         const bool kok = k0 + ks * 2 + af.dj < p.K;
-        double a[2], b[2];
+        double a[MI], b[NI];
 #pragma unroll
-        for (int mi = 0; mi < 2; ++mi)
+        for (int mi = 0; mi < MI; ++mi)
           a[mi] = (kok && row_ok[mi]) ? af.sign(ad[2 * (mi * 4 * SA) + 4 * ks]) : 0.0;
 #pragma unroll
-        for (int ni = 0; ni < 2; ++ni) b[ni] = kok ? bd[2 * (2 * ks * SB + ni * 8)] : 0.0;
+        for (int ni = 0; ni < NI; ++ni) b[ni] = kok ? bd[2 * (2 * ks * SB + ni * 8)] : 0.0;
 #pragma unroll
-        for (int mi = 0; mi < 2; ++mi)
+        for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-          for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+          for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
       }
     }
     __syncwarp();
@@ -207,13 +251,13 @@ __device__ __forceinline__ void consume(const Ring& r, const Problem& p, int til
     advance(stage, phase);
     if (kc == nk - 1) {  // tile done: registers -> global
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi)
+      for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 2; ++ni) {
+        for (int ni = 0; ni < NI; ++ni) {
           int coff;
           const double2 z = pair_complex(acc[mi][ni], lane, coff);
-          const int i = m0 + (wm * 2 + mi) * 4 + (lane >> 3);
-          const int col = n0 + (wn * 2 + ni) * 8 + coff;
+          const int i = m0 + (wm * MI + mi) * 4 + (lane >> 3);
+          const int col = n0 + (wn * NI + ni) * 8 + coff;
           if (i < p.M && col < p.N) p.C[(long long)i * p.ldc + col] = z;
         }
     }
@@ -236,8 +280,10 @@ __global__ void __launch_bounds__(THREADS) zgemm_kernel(const double2* __restric
                                                         const double2* __restrict__ B,
                                                         double2* __restrict__ C, int n,
                                                         long long sa, long long sb, long long sc) {
+  using G = Geo<32>;
+  constexpr int BN = G::BN;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const Ring r = carve(smem_raw);
+  const Ring r = carve<G>(smem_raw);
   init_ring(r);
   const int b = blockIdx.z, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const Problem p{A + b * sa, n, B + b * sb, n, C + b * sc, n, n, n, n};
@@ -246,14 +292,15 @@ __global__ void __launch_bounds__(THREADS) zgemm_kernel(const double2* __restric
   int stage = 0;
   unsigned phase = 0;
   if (warp == CWARPS) {
-    produce_tile(r, p, tile, blockIdx.x * BM, blockIdx.y * BN, stage, phase, lane);
+    produce_tile<G>(r, p, tile, blockIdx.x * BM, blockIdx.y * BN, stage, phase, lane);
     produce_end(r, stage, phase, lane);
   } else {
-    consume(r, p, tiles_m, stage, phase, warp, lane);
+    consume<G>(r, p, tiles_m, stage, phase, warp, lane);
   }
 }
 
 // ---- persistent stepping ----------------------------------------------------
+using StepGeo = Geo<16>;
 struct StepCtl {
   unsigned int tile_ctr[2];
   unsigned int barrier;
@@ -280,8 +327,10 @@ __global__ void __launch_bounds__(THREADS) tiled_evolve_kernel(const double2* __
                                                                double2* v0, double2* v1,
                                                                int batch, int64_t steps,
                                                                StepCtl* ctl) {
+  using G = StepGeo;
+  constexpr int BN = G::BN;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const Ring r = carve(smem_raw);
+  const Ring r = carve<G>(smem_raw);
   init_ring(r);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_m = (n + BM - 1) / BM, tiles_n = (batch + BN - 1) / BN;
@@ -303,11 +352,11 @@ __global__ void __launch_bounds__(THREADS) tiled_evolve_kernel(const double2* __
         t = __shfl_sync(0xffffffffu, t, 0);
         if (t >= ntiles) break;
         // column-major tile order: consecutive tiles share the same V columns
-        produce_tile(r, p, t, (t % tiles_m) * BM, (t / tiles_m) * BN, stage, phase, lane);
+        produce_tile<G>(r, p, t, (t % tiles_m) * BM, (t / tiles_m) * BN, stage, phase, lane);
       }
       produce_end(r, stage, phase, lane);
     } else {
-      consume(r, p, tiles_m, stage, phase, warp, lane);
+      consume<G>(r, p, tiles_m, stage, phase, warp, lane);
     }
     grid_barrier(&ctl->barrier, unsigned(s + 1) * gridDim.x);
     double2* tmp = cur;
@@ -405,14 +454,15 @@ void launch_tiled_evolve(const double* p_dev, size_t n, double* x_re, double* x_
 
   static int occ = [] {
     check_cuda(cudaFuncSetAttribute(tiled_evolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(kSmemBytes)),
+                                    int(StepGeo::kSmemBytes)),
                "smem attr");
     int o = 0;
-    check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, tiled_evolve_kernel, THREADS, kSmemBytes),
+    check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, tiled_evolve_kernel, THREADS,
+                                                             StepGeo::kSmemBytes),
                "occupancy");
     return o;
   }();
-  const int ntiles = ((ni + BM - 1) / BM) * ((bi + BN - 1) / BN);
+  const int ntiles = ((ni + BM - 1) / BM) * ((bi + StepGeo::BN - 1) / StepGeo::BN);
   int grid = std::min(occ * sm_count(), ntiles);
   if (grid < 1) grid = 1;
   const double2* p2 = reinterpret_cast<const double2*>(p_dev);
@@ -420,7 +470,7 @@ void launch_tiled_evolve(const double* p_dev, size_t n, double* x_re, double* x_
   void* args[] = {(void*)&p2, (void*)&ni, (void*)&v0, (void*)&v1, (void*)&bi, (void*)&st, (void*)&ctl};
   if (steps > 0) {
     check_cuda(cudaLaunchCooperativeKernel((const void*)tiled_evolve_kernel, dim3(grid), dim3(THREADS),
-                                           args, kSmemBytes, s),
+                                           args, StepGeo::kSmemBytes, s),
                "tiled_evolve_kernel (cooperative)");
     note_launch();
   }
@@ -431,13 +481,13 @@ void launch_zgemm(const double* a, const double* b, double* c, int n, int batch,
                   long long stride_b, long long stride_c, cudaStream_t s) {
   static bool init = [] {
     check_cuda(cudaFuncSetAttribute(zgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(kSmemBytes)),
+                                    int(Geo<32>::kSmemBytes)),
                "smem attr");
     return true;
   }();
   (void)init;
-  const dim3 grid((n + BM - 1) / BM, (n + BN - 1) / BN, batch);
-  zgemm_kernel<<<grid, THREADS, kSmemBytes, s>>>(reinterpret_cast<const double2*>(a),
+  const dim3 grid((n + BM - 1) / BM, (n + Geo<32>::BN - 1) / Geo<32>::BN, batch);
+  zgemm_kernel<<<grid, THREADS, Geo<32>::kSmemBytes, s>>>(reinterpret_cast<const double2*>(a),
                                                  reinterpret_cast<const double2*>(b),
                                                  reinterpret_cast<double2*>(c), n, stride_a, stride_b,
                                                  stride_c);

@@ -371,3 +371,21 @@ def test_grape_constant_pulse_equals_evolve(lbg):
         lbg.grape_chain(h0, hc, [], 4, 0.01, dis, rho0)
     with pytest.raises(ValueError):
         lbg.grape_chain(h0, np.zeros((2, 2)), [0.5], 4, 0.01, dis, rho0)
+
+
+@pytest.mark.parametrize("n,B", [(17, 16), (33, 5), (81, 8), (97, 40), (130, 333)])
+def test_tiled_ragged_shapes_vs_torch(lbg, torch, n, B):
+    """Regression: odd n (ragged last K chunk and last M tile) through the TMA /
+    mbarrier tile engine, against torch fp64 matmuls (a plain fp64 reference)."""
+    dev = torch.device("cuda")
+    g = torch.Generator(device="cpu").manual_seed(n)
+    P = (torch.randn(n, n, dtype=torch.complex128, generator=g) / n).to(dev)
+    x0 = torch.randn(B, n, dtype=torch.complex128, generator=g).to(dev)
+    x = x0.clone()
+    ws = torch.empty(max(lbg.evolve_workspace(n, B, "tiled"), 1), dtype=torch.uint8, device=dev)
+    lbg.evolve_batch_dev(P, x, 3, algo="tiled", work=ws)
+    want = x0
+    for _ in range(3):
+        want = want @ P.T
+    torch.cuda.synchronize()
+    assert (x - want).abs().max().item() <= 1e-13 * want.abs().max().item()
