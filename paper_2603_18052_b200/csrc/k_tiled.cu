@@ -300,7 +300,9 @@ __global__ void __launch_bounds__(THREADS) zgemm_kernel(const double2* __restric
 }
 
 // ---- persistent stepping ----------------------------------------------------
-using StepGeo = Geo<16>;
+// 32-wide tiles: 16-wide halves the step-tail granularity but doubles the
+// row copies per MMA and measured 2x slower at config 3 (copy-issue bound).
+using StepGeo = Geo<32>;
 struct StepCtl {
   unsigned int tile_ctr[2];
   unsigned int barrier;
