@@ -32,9 +32,9 @@ namespace lbg {
 
 namespace {
 
-constexpr int BM = 32, BK = 16, STAGES = 4;
+constexpr int BM = 32, BK = 32, STAGES = 3;
 constexpr int CWARPS = 8, THREADS = 32 * (CWARPS + 1);
-constexpr int SA = 18;  // complex stride of A rows (see header)
+constexpr int SA = BK + 2;  // complex stride of A rows: 2 (mod 8), see header
 constexpr int A_ELEMS = BM * SA;
 
 // Tile geometry by tile width BN (complex columns): 32 for the expm GEMM, 16 for
@@ -107,7 +107,7 @@ struct Ring {
   double2* data;   // STAGES x (A | B)
   uint64_t* full;  // STAGES
   uint64_t* empty; // STAGES
-  int* hdr;        // STAGES x 2: tile id (-1 = end of step), k chunk
+  int* hdr;        // STAGES x 4: tile id (-1 = end of step), k chunk, segment [lo, hi] chunks
 };
 
 template <class G>
@@ -138,22 +138,30 @@ __device__ __forceinline__ void advance(int& stage, unsigned& phase) {
   }
 }
 
-// Producer: one warp streams the K chunks of tile (m0, n0) into the ring.
+// Producer: one warp streams iterations [it0, it1) of the flattened
+// (tile, K chunk) space into the ring (stream-K: a CTA's range may start or end
+// inside a tile; the header tells the consumers which part of the tile it is).
 template <class G>
-__device__ __forceinline__ void produce_tile(const Ring& r, const Problem& p, int tile, int m0, int n0,
-                                             int& stage, unsigned& phase, int lane) {
+__device__ __forceinline__ void produce_range(const Ring& r, const Problem& p, int tiles_m, long long it0,
+                                              long long it1, int& stage, unsigned& phase, int lane) {
   constexpr int BN = G::BN, SB = G::SB, STAGE_ELEMS = G::STAGE_ELEMS;
   const int nk = (p.K + BK - 1) / BK;
-  const int mrows = min(BM, p.M - m0), ncols = min(BN, p.N - n0);
-  for (int kc = 0; kc < nk; ++kc) {
+  for (long long it = it0; it < it1; ++it) {
+    const int t = int(it / nk), kc = int(it - (long long)t * nk);
+    const int m0 = (t % tiles_m) * BM, n0 = (t / tiles_m) * BN;
+    const int mrows = min(BM, p.M - m0), ncols = min(BN, p.N - n0);
     const int k0 = kc * BK, kv = min(BK, p.K - k0);
+    const long long tb = (long long)t * nk;
+    const int lo = int(max(it0 - tb, 0ll)), hi = int(min(it1 - 1 - tb, (long long)nk - 1));
     mbar_wait(&r.empty[stage], phase ^ 1u);
     double2* as = r.data + stage * STAGE_ELEMS;
     double2* bs = as + A_ELEMS;
     const unsigned bytes = unsigned(mrows * kv + kv * ncols) * 16u;
     if (lane == 0) {
-      r.hdr[2 * stage] = tile;
-      r.hdr[2 * stage + 1] = kc;
+      r.hdr[4 * stage] = t;
+      r.hdr[4 * stage + 1] = kc;
+      r.hdr[4 * stage + 2] = lo;
+      r.hdr[4 * stage + 3] = hi;
       mbar_arrive_tx(&r.full[stage], bytes);
     }
     __syncwarp();
@@ -168,16 +176,28 @@ __device__ __forceinline__ void produce_tile(const Ring& r, const Problem& p, in
 __device__ __forceinline__ void produce_end(const Ring& r, int& stage, unsigned& phase, int lane) {
   mbar_wait(&r.empty[stage], phase ^ 1u);
   if (lane == 0) {
-    r.hdr[2 * stage] = -1;
+    r.hdr[4 * stage] = -1;
     mbar_arrive(&r.full[stage]);
   }
   advance(stage, phase);
 }
 
 // Consumer warps: run tiles until the end-of-step sentinel.
+// Split tiles (stream-K): a tile cut between two CTAs' ranges has a HEAD part
+// (chunks from 0) and a TAIL part (chunks up to nk-1). The TAIL CTA computes its
+// part at the START of its range and publishes it (partial buffer + epoch
+// flag); the HEAD CTA reaches its part at the END of its range, adds the
+// published partial (fixed order: deterministic) and stores the tile.
+struct SplitK {
+  double2* part;          // ntiles x (CWARPS x 32 lanes x MI x NI) accumulator slots
+  unsigned int* flags;    // ntiles, = epoch when the TAIL partial is published
+  unsigned int epoch;
+};
+__device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, 256;\n" ::: "memory"); }
+
 template <class G>
 __device__ __forceinline__ void consume(const Ring& r, const Problem& p, int tiles_m, int& stage,
-                                       unsigned& phase, int warp, int lane) {
+                                       unsigned& phase, int warp, int lane, const SplitK* sk) {
   constexpr int BN = G::BN, SB = G::SB, STAGE_ELEMS = G::STAGE_ELEMS, MI = G::MI, NI = G::NI;
   const AFragLane af(lane);
   const int wm = warp / G::WN, wn = warp % G::WN;
@@ -191,14 +211,15 @@ __device__ __forceinline__ void consume(const Ring& r, const Problem& p, int til
   int m0 = 0, n0 = 0;
   while (true) {
     mbar_wait(&r.full[stage], phase);
-    const int tile = r.hdr[2 * stage], kc = r.hdr[2 * stage + 1];
+    const int tile = r.hdr[4 * stage], kc = r.hdr[4 * stage + 1];
+    const int lo = r.hdr[4 * stage + 2], hi = r.hdr[4 * stage + 3];
     if (tile < 0) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&r.empty[stage]);
       advance(stage, phase);
       return;
     }
-    if (kc == 0) {
+    if (kc == lo) {
       m0 = (tile % tiles_m) * BM;
       n0 = (tile / tiles_m) * BN;
 #pragma unroll
@@ -249,7 +270,43 @@ __device__ __forceinline__ void consume(const Ring& r, const Problem& p, int til
     __syncwarp();
     if (lane == 0) mbar_arrive(&r.empty[stage]);
     advance(stage, phase);
-    if (kc == nk - 1) {  // tile done: registers -> global
+    if (kc != hi) continue;
+    constexpr int SLOT = CWARPS * 32 * MI * NI;
+    if (sk && lo > 0) {  // TAIL part: publish the partial accumulators
+      double2* dst = sk->part + (long long)tile * SLOT;
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni)
+          __stcg(dst + ((warp * MI + mi) * NI + ni) * 32 + lane, make_double2(acc[mi][ni][0], acc[mi][ni][1]));
+      consumer_bar();
+      if (warp == 0 && lane == 0) {
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(sk->flags + tile), "r"(sk->epoch) : "memory");
+      }
+      continue;
+    }
+    if (sk && hi < nk - 1) {  // HEAD part: add the TAIL partial, then store
+      if (warp == 0 && lane == 0) {
+        while (true) {
+          unsigned v;
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(sk->flags + tile) : "memory");
+          if (v == sk->epoch) break;
+          __nanosleep(32);
+        }
+      }
+      consumer_bar();
+      const double2* src = sk->part + (long long)tile * SLOT;
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) {
+          const double2 q = __ldcg(src + ((warp * MI + mi) * NI + ni) * 32 + lane);
+          acc[mi][ni][0] += q.x;
+          acc[mi][ni][1] += q.y;
+        }
+    }
+    {  // tile done: registers -> global
 #pragma unroll
       for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
@@ -281,7 +338,6 @@ __global__ void __launch_bounds__(THREADS) zgemm_kernel(const double2* __restric
                                                         double2* __restrict__ C, int n,
                                                         long long sa, long long sb, long long sc) {
   using G = Geo<32>;
-  constexpr int BN = G::BN;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const Ring r = carve<G>(smem_raw);
   init_ring(r);
@@ -292,10 +348,11 @@ __global__ void __launch_bounds__(THREADS) zgemm_kernel(const double2* __restric
   int stage = 0;
   unsigned phase = 0;
   if (warp == CWARPS) {
-    produce_tile<G>(r, p, tile, blockIdx.x * BM, blockIdx.y * BN, stage, phase, lane);
+    const long long nk = (n + BK - 1) / BK;
+    produce_range<G>(r, p, tiles_m, tile * nk, (tile + 1) * nk, stage, phase, lane);
     produce_end(r, stage, phase, lane);
   } else {
-    consume<G>(r, p, tiles_m, stage, phase, warp, lane);
+    consume<G>(r, p, tiles_m, stage, phase, warp, lane, nullptr);
   }
 }
 
@@ -328,7 +385,8 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int tar
 __global__ void __launch_bounds__(THREADS) tiled_evolve_kernel(const double2* __restrict__ P, int n,
                                                                double2* v0, double2* v1,
                                                                int batch, int64_t steps,
-                                                               StepCtl* ctl) {
+                                                               StepCtl* ctl, double2* part,
+                                                               unsigned int* flags) {
   using G = StepGeo;
   constexpr int BN = G::BN;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -341,24 +399,21 @@ __global__ void __launch_bounds__(THREADS) tiled_evolve_kernel(const double2* __
   double2* nxt = v1;
   int stage = 0;
   unsigned phase = 0;
+  // stream-K: this CTA's fixed, contiguous share of the step's (tile, K chunk)
+  // iterations; grid <= ntiles keeps every range >= one tile, so a tile is
+  // split across at most two CTAs
+  const long long nk = (n + BK - 1) / BK, work = (long long)ntiles * nk;
+  const long long it0 = work * blockIdx.x / gridDim.x, it1 = work * (blockIdx.x + 1) / gridDim.x;
   for (int64_t s = 0; s < steps; ++s) {
-    const int par = int(s & 1);
     const Problem p{P, n, cur, batch, nxt, batch, n, batch, n};
     if (warp == CWARPS) {
       // generic-proxy stores of the previous step -> async-proxy (bulk copy) reads
       asm volatile("fence.proxy.async.global;\n" ::: "memory");
-      if (blockIdx.x == 0 && lane == 0) ctl->tile_ctr[par ^ 1] = 0u;  // next step's counter
-      while (true) {
-        int t = 0;
-        if (lane == 0) t = int(atomicAdd(&ctl->tile_ctr[par], 1u));
-        t = __shfl_sync(0xffffffffu, t, 0);
-        if (t >= ntiles) break;
-        // column-major tile order: consecutive tiles share the same V columns
-        produce_tile<G>(r, p, t, (t % tiles_m) * BM, (t / tiles_m) * BN, stage, phase, lane);
-      }
+      produce_range<G>(r, p, tiles_m, it0, it1, stage, phase, lane);
       produce_end(r, stage, phase, lane);
     } else {
-      consume<G>(r, p, tiles_m, stage, phase, warp, lane);
+      const SplitK sk{part, flags, unsigned(s + 1)};
+      consume<G>(r, p, tiles_m, stage, phase, warp, lane, &sk);
     }
     grid_barrier(&ctl->barrier, unsigned(s + 1) * gridDim.x);
     double2* tmp = cur;
@@ -437,8 +492,15 @@ int sm_count() {
   return count;
 }
 
+size_t tiled_ntiles(size_t n, int64_t batch) {
+  return ((n + BM - 1) / BM) * ((size_t(batch) + StepGeo::BN - 1) / StepGeo::BN);
+}
+constexpr size_t kSlot = size_t(CWARPS) * 32 * StepGeo::MI * StepGeo::NI;  // double2 per split tile
+
 size_t tiled_workspace(size_t n, int64_t batch) {
-  return 2 * align_up(sizeof(double2) * n * size_t(batch)) + align_up(sizeof(StepCtl));
+  const size_t nt = tiled_ntiles(n, batch);
+  return 2 * align_up(sizeof(double2) * n * size_t(batch)) + align_up(sizeof(StepCtl)) +
+         align_up(nt * kSlot * sizeof(double2)) + align_up(nt * sizeof(unsigned int));
 }
 
 void launch_tiled_evolve(const double* p_dev, size_t n, double* x_re, double* x_im, double* x_aos,
@@ -450,6 +512,11 @@ void launch_tiled_evolve(const double* p_dev, size_t n, double* x_re, double* x_
   double2* v0 = reinterpret_cast<double2*>(w);
   double2* v1 = reinterpret_cast<double2*>(w + align_up(sizeof(double2) * n * size_t(batch)));
   StepCtl* ctl = reinterpret_cast<StepCtl*>(w + 2 * align_up(sizeof(double2) * n * size_t(batch)));
+  const size_t nt = tiled_ntiles(n, batch);
+  double2* part = reinterpret_cast<double2*>(reinterpret_cast<char*>(ctl) + align_up(sizeof(StepCtl)));
+  unsigned int* flags =
+      reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(part) + align_up(nt * kSlot * sizeof(double2)));
+  check_cuda(cudaMemsetAsync(flags, 0, nt * sizeof(unsigned int), s), "memset flags");
   const int ni = int(n), bi = int(batch);
   convert<true>(x_re, x_im, x_aos, v0, ni, bi, layout, s);
   check_cuda(cudaMemsetAsync(ctl, 0, sizeof(StepCtl), s), "memset ctl");
@@ -469,7 +536,8 @@ void launch_tiled_evolve(const double* p_dev, size_t n, double* x_re, double* x_
   if (grid < 1) grid = 1;
   const double2* p2 = reinterpret_cast<const double2*>(p_dev);
   int64_t st = steps;
-  void* args[] = {(void*)&p2, (void*)&ni, (void*)&v0, (void*)&v1, (void*)&bi, (void*)&st, (void*)&ctl};
+  void* args[] = {(void*)&p2, (void*)&ni, (void*)&v0, (void*)&v1, (void*)&bi, (void*)&st, (void*)&ctl,
+                  (void*)&part, (void*)&flags};
   if (steps > 0) {
     check_cuda(cudaLaunchCooperativeKernel((const void*)tiled_evolve_kernel, dim3(grid), dim3(THREADS),
                                            args, StepGeo::kSmemBytes, s),
