@@ -179,6 +179,23 @@ int lbg_ginibre_batch(uint64_t seed, uint32_t cfg, uint64_t first, int64_t count
 int lbg_sweep_params_batch(uint64_t seed, uint64_t first, int64_t count, double* delta,
                            double* scale);
 
+/* ------------------------------------------------------------------------
+ * Text formats of the reference (host only):
+ *  lbg_write_matrix / lbg_read_matrix: the 17-significant-digit interchange
+ *    format of lb::write_matrix / lb::read_matrix (complex_matrix.cpp:166-188);
+ *    pass buf = NULL / out = NULL to query the size / shape first.
+ *  lbg_read_model: lb::read_model (model_io.cpp:37-109): dim / hamiltonian /
+ *    collapse keys or "preset = transmon" (lindblad.cpp:82-100). Call with
+ *    h = ops = NULL to get d and n_ops, then with buffers (h: d*d, ops:
+ *    cap_ops*d*d complex AoS).
+ * Malformed text -> LBG_ERUNTIME, invalid model -> LBG_EINVAL;
+ * lbg_io_last_error() has the message.
+ * ------------------------------------------------------------------------ */
+const char* lbg_io_last_error(void);
+int lbg_write_matrix(const double* a, size_t rows, size_t cols, char* buf, size_t cap, size_t* len);
+int lbg_read_matrix(const char* text, size_t* rows, size_t* cols, double* out, size_t cap_elems);
+int lbg_read_model(const char* text, size_t* d, size_t* n_ops, double* h, double* ops, size_t cap_ops);
+
 /* FP64 roofline denominators measured live on the current device (TF/s):
  * register-only DMMA (m8n8k4 f64) and DFMA loops over every SM. */
 int lbg_fp64_peak(double* dmma_tflops, double* dfma_tflops);

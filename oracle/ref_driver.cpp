@@ -28,7 +28,9 @@
 #include "lb/kernels.hpp"
 #include "lb/lindblad.hpp"
 #include "lb/propagate.hpp"
+#include "lb/model_io.hpp"
 #include "lb/random.hpp"
+#include <sstream>
 #include "lb/validate.hpp"
 
 using lb::cplx;
@@ -289,6 +291,33 @@ int ref_grape_chain(std::size_t d, const double* h0, const double* hc, const dou
     to_buf(g.final_state, out);
     *build_ms = g.timings.build_ms;
     *chain_ms = g.timings.chain_ms;
+  });
+}
+
+// lb::read_model (model_io.cpp:37-109) on a text buffer.
+int ref_read_model(const char* text, std::size_t* d, std::size_t* nops, double* h, double* ops,
+                   std::size_t cap) {
+  return guarded([&] {
+    std::istringstream is(text);
+    const lb::LindbladModel m = lb::read_model(is);
+    *d = m.dim;
+    *nops = m.collapse_ops.size();
+    if (h) to_buf(m.hamiltonian, h);
+    if (ops)
+      for (std::size_t k = 0; k < std::min(cap, m.collapse_ops.size()); ++k)
+        to_buf(m.collapse_ops[k], ops + 2 * k * m.dim * m.dim);
+  });
+}
+
+// lb::write_matrix (complex_matrix.cpp:166-177) into a buffer.
+int ref_write_matrix(const double* a, std::size_t r, std::size_t c, char* buf, std::size_t cap,
+                     std::size_t* len) {
+  return guarded([&] {
+    std::ostringstream os;
+    lb::write_matrix(os, from_buf(a, r, c));
+    const std::string s = os.str();
+    *len = s.size();
+    if (buf && cap > s.size()) std::memcpy(buf, s.c_str(), s.size() + 1);
   });
 }
 

@@ -315,3 +315,56 @@ def evolve_sweep_dev(h0, hd, hs, ops, delta, scale, dt, rho0, n_steps, pops, ens
 def check_state_batched_dev(x, d: int, out3, stream=None):
     _check(lib().lbg_check_state_batched_dev(_tp(x), d, x.shape[0], _tp(out3), _sp(stream)),
            "check_state_batched_dev")
+
+
+# ------------------------------------------------------- text formats (host) ---
+def _io_check(rc: int, what: str) -> None:
+    if rc == 0:
+        return
+    msg = f"{what}: {lib().lbg_io_last_error().decode()}"
+    raise ValueError(msg) if rc == 1 else RuntimeError(msg)
+
+
+def write_matrix(a) -> str:
+    """lb::write_matrix (complex_matrix.cpp:166-177): 17-digit interchange text."""
+    a = _c128(np.atleast_2d(a))
+    L = lib()
+    L.lbg_io_last_error.restype = C.c_char_p
+    L.lbg_write_matrix.argtypes = [_dp, _sz, _sz, C.c_char_p, _sz, C.POINTER(_sz)]
+    n = _sz()
+    _io_check(L.lbg_write_matrix(_p(a), a.shape[0], a.shape[1], None, 0, C.byref(n)), "write_matrix")
+    buf = C.create_string_buffer(n.value + 1)
+    _io_check(L.lbg_write_matrix(_p(a), a.shape[0], a.shape[1], buf, n.value + 1, C.byref(n)), "write_matrix")
+    return buf.value.decode()
+
+
+def read_matrix(text: str):
+    """lb::read_matrix (complex_matrix.cpp:179-188)."""
+    L = lib()
+    L.lbg_io_last_error.restype = C.c_char_p
+    L.lbg_read_matrix.argtypes = [C.c_char_p, C.POINTER(_sz), C.POINTER(_sz), _dp, _sz]
+    r, c = _sz(), _sz()
+    raw = text.encode()
+    _io_check(L.lbg_read_matrix(raw, C.byref(r), C.byref(c), None, 0), "read_matrix")
+    out = np.zeros((r.value, c.value), np.complex128)
+    _io_check(L.lbg_read_matrix(raw, C.byref(r), C.byref(c), _p(out), out.size), "read_matrix")
+    return out
+
+
+def read_model(text: str):
+    """lb::read_model (model_io.cpp:37-109): returns (H, collapse ops)."""
+    L = lib()
+    L.lbg_io_last_error.restype = C.c_char_p
+    L.lbg_read_model.argtypes = [C.c_char_p, C.POINTER(_sz), C.POINTER(_sz), _dp, _dp, _sz]
+    d, k = _sz(), _sz()
+    raw = text.encode()
+    _io_check(L.lbg_read_model(raw, C.byref(d), C.byref(k), None, None, 0), "read_model")
+    h = np.zeros((d.value, d.value), np.complex128)
+    ops = np.zeros((max(k.value, 1), d.value, d.value), np.complex128)
+    _io_check(L.lbg_read_model(raw, C.byref(d), C.byref(k), _p(h), _p(ops), k.value), "read_model")
+    return h, ops[: k.value]
+
+
+def read_model_file(path: str):
+    with open(path) as f:
+        return read_model(f.read())
