@@ -40,6 +40,8 @@ extern "C" {
 #define LBG_ALGO_DFMA9 2   /* K1a: n == 9, P in the constant bank, DFMA (config 1) */
 #define LBG_ALGO_SMEM 3    /* K1b: n <= 84, P resident in shared memory, DMMA (config 2) */
 #define LBG_ALGO_TILED 4   /* K1c: any n, P streamed from L2, persistent DMMA tiles (config 3) */
+#define LBG_ALGO_CTA 5     /* K2b: n <= 96, one CTA per trajectory, P in shared memory (few trajectories) */
+#define LBG_ALGO_ROWSPLIT 6 /* K2c: any n, batch <= 4, P's rows spread over all SMs' shared memory */
 
 const char* lbg_last_error(void);
 const char* lbg_version(void);

@@ -106,11 +106,15 @@ bool is_hermitian(const double* h, size_t d) {
   return scale == 0.0 ? worst == 0.0 : worst <= 1e-12 * scale;
 }
 
-int choose_algo(size_t n, int64_t batch, int algo) {
+// Regime selection: latency kernels for few trajectories,
+// throughput kernels for batches. CTA / ROWSPLIT take the AoS layout only.
+int choose_algo(size_t n, int64_t batch, int algo, Layout layout = Layout::aos) {
   if (algo != LBG_ALGO_AUTO) return algo;
   if (chain_supported(n) && batch <= 512) return LBG_ALGO_CHAIN;
   if (n == 9) return LBG_ALGO_DFMA9;
+  if (layout == Layout::aos && cta_chain_supported(n) && batch <= 256) return LBG_ALGO_CTA;
   if (smem_supported(n)) return LBG_ALGO_SMEM;
+  if (layout == Layout::aos && batch <= 2 && rowsplit_supported(n, batch)) return LBG_ALGO_ROWSPLIT;
   return LBG_ALGO_TILED;
 }
 
@@ -122,7 +126,7 @@ void evolve_dev(const double* p, size_t n, double* x_re, double* x_im, double* x
   if (batch == 0 || steps == 0) return;
   if (layout == Layout::soa && (!x_re || !x_im)) throw invalid_argument("evolve: null state");
   if (layout == Layout::aos && !x_aos) throw invalid_argument("evolve: null state");
-  switch (choose_algo(n, batch, algo)) {
+  switch (choose_algo(n, batch, algo, layout)) {
     case LBG_ALGO_CHAIN:
       if (!chain_supported(n)) throw invalid_argument("evolve: chain kernel needs n <= 16");
       return launch_chain(p, n, x_re, x_im, x_aos, batch, steps, layout, s);
@@ -134,6 +138,12 @@ void evolve_dev(const double* p, size_t n, double* x_re, double* x_im, double* x
       return launch_smem(p, n, x_re, x_im, x_aos, batch, steps, layout, s);
     case LBG_ALGO_TILED:
       return launch_tiled_evolve(p, n, x_re, x_im, x_aos, batch, steps, layout, work, s);
+    case LBG_ALGO_CTA:
+      if (layout != Layout::aos) throw invalid_argument("evolve: cta kernel takes the AoS layout");
+      return launch_cta_chain(p, n, x_aos, batch, steps, s);
+    case LBG_ALGO_ROWSPLIT:
+      if (layout != Layout::aos) throw invalid_argument("evolve: rowsplit kernel takes the AoS layout");
+      return launch_rowsplit(p, n, x_aos, batch, steps, work, s);
     default:
       throw invalid_argument("evolve: unknown algo");
   }
@@ -279,7 +289,11 @@ int lbg_expm(const double* a, size_t n, double dt, double* out) {
 // ---- batched shared-P propagation ----
 size_t lbg_evolve_workspace(size_t n, int64_t batch, int algo) {
   if (n == 0 || batch <= 0) return 0;
-  return choose_algo(n, batch, algo) == LBG_ALGO_TILED ? tiled_workspace(n, batch) : 0;
+  switch (choose_algo(n, batch, algo)) {
+    case LBG_ALGO_TILED: return tiled_workspace(n, batch);
+    case LBG_ALGO_ROWSPLIT: return rowsplit_supported(n, batch) ? rowsplit_workspace(n, batch) : 0;
+    default: return 0;
+  }
 }
 
 int lbg_evolve_shared_p_soa_dev(const double* p, size_t n, double* x_re, double* x_im,

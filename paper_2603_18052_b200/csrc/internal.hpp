@@ -51,6 +51,14 @@ std::size_t tiled_workspace(std::size_t n, int64_t batch);
 void launch_tiled_evolve(const double* p_dev, std::size_t n, double* x_re, double* x_im,
                          double* x_aos, int64_t batch, int64_t steps, Layout layout, void* work,
                          cudaStream_t s);
+// K2b / K2c — latency kernels for one or a few trajectories (k_single.cu)
+bool cta_chain_supported(std::size_t n);
+void launch_cta_chain(const double* p, std::size_t n, double* x_aos, int64_t batch, int64_t steps,
+                      cudaStream_t s);
+bool rowsplit_supported(std::size_t n, int64_t batch);
+std::size_t rowsplit_workspace(std::size_t n, int64_t batch);
+void launch_rowsplit(const double* p, std::size_t n, double* x_aos, int64_t batch, int64_t steps,
+                     void* work, cudaStream_t s);
 // plain batched complex GEMM C[b] = A[b] * B[b] (n x n, AoS), DMMA tiles;
 // strides in complex elements
 void launch_zgemm(const double* a, const double* b, double* c, int n, int batch,

@@ -269,7 +269,7 @@ void launch_sweep(size_t d, const double* h0, const double* hd, const double* hs
 size_t grape_workspace(size_t d, int64_t segments) {
   const size_t n = d * d;
   return sweep_workspace(d, segments) + align_up(size_t(segments) * n * n * 16) + align_up(n * 16) +
-         tiled_workspace(n, 1);
+         std::max(tiled_workspace(n, 1), rowsplit_workspace(n, 1));
 }
 
 // GRAPE piecewise-constant chain (propagate.cpp:111-168): every segment's
@@ -296,8 +296,10 @@ void launch_grape(size_t d, const double* h0, const double* hc, const double* ze
     const double* pj = reinterpret_cast<const double*>(props + j * nn);
     if (chain_supported(n))
       launch_chain(pj, n, nullptr, nullptr, x, 1, steps_per_segment, Layout::aos, s);
-    else if (smem_supported(n))
-      launch_smem(pj, n, nullptr, nullptr, x, 1, steps_per_segment, Layout::aos, s);
+    else if (cta_chain_supported(n))
+      launch_cta_chain(pj, n, x, 1, steps_per_segment, s);
+    else if (rowsplit_supported(n, 1))
+      launch_rowsplit(pj, n, x, 1, steps_per_segment, ework, s);
     else
       launch_tiled_evolve(pj, n, nullptr, nullptr, x, 1, steps_per_segment, Layout::aos, ework, s);
   }

@@ -15,11 +15,16 @@ pytestmark = pytest.mark.gpu
 TOL_RHO = 1e-10
 TOL_INV = 1e-12
 ALGOS_FOR = {  # which kernel paths can run a given n
-    4: ("chain", "smem", "tiled"),
-    9: ("chain", "dfma9", "smem", "tiled"),
-    81: ("smem", "tiled"),
-    729: ("tiled",),
+    4: ("chain", "smem", "tiled", "cta", "rowsplit"),
+    9: ("chain", "dfma9", "smem", "tiled", "cta", "rowsplit"),
+    81: ("smem", "tiled", "cta", "rowsplit"),
+    729: ("tiled", "rowsplit"),
 }
+
+
+def algos(n, batch):
+    """kernel paths applicable to (n, batch): rowsplit takes at most 4 trajectories"""
+    return tuple(a for a in ALGOS_FOR[n] if a != "rowsplit" or batch <= 4)
 
 
 @pytest.fixture(scope="module")
@@ -111,7 +116,7 @@ def test_config_subsets_vs_reference_goldens(lbg, golden, oracle, cfg):
         h, ops = lbg.config_model(3)
         P = oracle.expm(oracle.build_lindbladian(h, ops), 0.1)
     rho0, want, steps = g[f"c{cfg}_rho0"], g[f"c{cfg}_out"], int(g[f"c{cfg}_steps"])
-    for algo in ALGOS_FOR[P.shape[0]]:
+    for algo in algos(P.shape[0], rho0.shape[0]):
         got = lbg.evolve_batch(P, rho0, steps, algo=algo)
         err = np.abs(got - want).max()
         assert err <= TOL_RHO, (algo, err)
@@ -133,7 +138,7 @@ def test_closed_form_damping_every_path(lbg):
     rho0 = np.zeros((2, 2), complex)
     rho0[1, 1] = 1.0
     want = np.exp(-gamma * n * dt)
-    for algo in ALGOS_FOR[4]:
+    for algo in algos(4, 1):
         rho = lbg.evolve(P, rho0, n, algo=algo)
         assert abs(rho[1, 1].real - want) < 1e-10
         assert abs(rho[0, 0].real - (1 - want)) < 1e-10
@@ -144,7 +149,7 @@ def test_closed_form_damping_every_path(lbg):
 def test_evolve_contract(lbg, golden):
     P = golden["models"]["c1_P"]
     rho0 = golden["evolve"]["c1_rho0"][:5]
-    for algo in ALGOS_FOR[9]:
+    for algo in algos(9, 5):
         assert np.array_equal(lbg.evolve_batch(P, rho0, 0, algo=algo), rho0)  # zero steps
         direct = lbg.evolve_batch(P, rho0, 10, algo=algo)
         stacked = lbg.evolve_batch(P, lbg.evolve_batch(P, rho0, 4, algo=algo), 6, algo=algo)
