@@ -62,6 +62,50 @@ def flops_per_traj_step(d: int) -> int:
     return 8 * d ** 4
 
 
+# ---------------------------------------------------- GPU roofline placement ---
+# B200 re-targeting of the reference's CPU model (proj/src/roofline.cpp:62-99:
+# characterize -> place -> classify). Levels are where P lives while stepping;
+# bandwidths are MEASURED (profiles/r01_fp64_peaks.json, MEASURED_PEAKS.json),
+# capacities per the hardware (per-SM for the on-chip levels, since every SM
+# needs its own copy of a shared P).
+B200_PROFILE = {
+    "levels": ["regs/const", "smem", "l2", "hbm"],
+    "capacity_bytes": [None, 227 * 1024, 126 * 2 ** 20, 180 * 10 ** 9],
+    "bw_gbs": [None, 36895.5, 15363.8, 6465.2],
+}
+
+
+def roofline_place(d: int, batch: int, shared_p: bool, peak_tflops: float, tile: int = 32) -> dict:
+    """characterize (8 d^4 flops per trajectory-step; roofline.cpp:62-74), place P
+    on the B200 ladder (roofline.cpp:76-87) and classify (roofline.cpp:93-99):
+    bytes are what one step must pull from P's level for the whole batch."""
+    n = d * d
+    p_bytes = 16 * n * n
+    flops = 8 * d ** 4 * batch
+    prof = B200_PROFILE
+    if shared_p:
+        if d == 3:
+            level, bytes_ = 0, 0  # 9x9 P in the constant bank / uniform registers
+        elif p_bytes <= prof["capacity_bytes"][1]:
+            # each SM re-reads P from SMEM once per step for its tile of trajectories
+            sms = min(148, -(-batch // tile))
+            level, bytes_ = 1, p_bytes * sms
+        elif p_bytes <= prof["capacity_bytes"][2]:
+            # GEMM tiles (tile x tile complex) stream P and the state from L2
+            level, bytes_ = 2, flops / (8 * tile * tile / (16 * 2 * tile))
+        else:
+            level, bytes_ = 3, p_bytes + 32 * n * batch
+    else:
+        level, bytes_ = (0, 0) if n <= 81 else (3, (n * n * 16 + 32 * n) * batch)  # per-trajectory P
+    ai = flops / bytes_ if bytes_ else float("inf")
+    bw = prof["bw_gbs"][level]
+    attainable = peak_tflops if bw is None else min(peak_tflops, ai * bw / 1e3)
+    ridge = None if bw is None else peak_tflops * 1e3 / bw
+    return {"level": prof["levels"][level], "flops_per_step": flops, "bytes_per_step": bytes_,
+            "ai_flop_per_byte": ai, "ridge_flop_per_byte": ridge, "attainable_tflops": attainable,
+            "bound": "compute" if (ridge is None or ai >= ridge) else "memory"}
+
+
 class Clocks:
     """nvidia-smi samples during the timed region (the recipe's clocks line)."""
 
@@ -326,6 +370,7 @@ def run_ours(args):
                                     "(MEASURED_PEAKS.json has no FP64 entry)",
                      "flops_per_launch": flops_per_traj_step(d) * B * S, "launch_ms": kernel_ms},
         "e2e": e2e,
+        "placement": roofline_place(d, B, cfg != 4, peak),
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
@@ -414,10 +459,12 @@ def extra_configs(torch, lbg, R, peak):
                      "gflops": tf * 1e3, "kernel": KERNEL[cfg], "gpu_launches_per_pass": launches // len(per)}
             if cfg == 0:
                 entry["ns_per_step"] = ms * 1e6 / S
-                entry["bound"] = "latency (one dependent chain; no throughput roofline)"
+                entry["bound"] = ("latency: one dependent chain; per step >= 6 dependent FP64 ops x 23 cycles "
+                                  "+ a shared-memory round trip (profiles/r01_latency_probe.json)")
             else:
                 entry["roofline"] = {"bound": "fp64", "achieved": tf, "peak": peak, "unit": "TFLOP/s",
                                      "frac": tf / peak}
+                entry["placement"] = roofline_place(d, B, cfg != 4, peak)
             if cfg == 4:
                 entry["note"] = ("real transfer-matrix mode (L_R = T L T^-1, 4x fewer executed flops than "
                                  "8 d^4); includes per-trajectory GPU assembly + expm (not counted in flops)")
