@@ -100,6 +100,32 @@ int lbg_evolve_shared_p(const double* p, size_t d, const double* rho0, int64_t b
                         int64_t steps, double* out, int algo);
 
 /* ------------------------------------------------------------------------
+ * Density-matrix mode of the same shared-P propagation (opt-in; the complex
+ * entry points above stay the reference-faithful default). lb::evolve only
+ * accepts physical states (propagate.cpp:77-80); a Lindblad propagator maps
+ * Hermitian matrices to Hermitian matrices, so on the real coordinates
+ * x[i*d+j] = Re rho_ij (i <= j), -Im rho_ij (i > j) it is the real matrix
+ * P_R = T P T^-1 (4x fewer flops per step). rho = H + i H' with H, H'
+ * Hermitian, propagated as two real vector sets. mode: LBG_DENSITY_HERMITIAN
+ * asserts H' = 0 (rho stored exactly Hermitian, as GG^dag/tr is) and propagates
+ * H only; LBG_DENSITY_GENERAL always propagates both; LBG_DENSITY_AUTO detects
+ * H' != 0 on the device and skips the H' set when it is zero (no host sync).
+ * P must preserve Hermiticity (every Lindblad propagator does).
+ * d*d <= 84. P: n x n AoS (device), rho: batch x d x d AoS (device, in place),
+ * work: lbg_density_workspace(d*d, batch) bytes.
+ * ------------------------------------------------------------------------ */
+#define LBG_DENSITY_HERMITIAN 0
+#define LBG_DENSITY_GENERAL 1
+#define LBG_DENSITY_AUTO 2
+size_t lbg_density_workspace(size_t n, int64_t batch);
+int lbg_evolve_density_dev(const double* p, size_t d, double* rho, int64_t batch, int64_t steps,
+                           int mode, void* work, void* stream);
+/* host-buffer variant (end-to-end, synchronous, LBG_DENSITY_AUTO): rho0 / out
+ * are batch x d x d AoS; rho0 is validated like propagate.cpp:79. */
+int lbg_evolve_density(const double* p, size_t d, const double* rho0, int64_t batch,
+                       int64_t steps, double* out);
+
+/* ------------------------------------------------------------------------
  * Per-trajectory propagators (config 4, "robustness atlas"): for trajectory b
  *   H_b = h0 + delta[b] * hd + scale[b] * hs,   L_k fixed,
  *   L_b = build_lindbladian(H_b, L_k),  P_b = exp(L_b dt),

@@ -77,6 +77,10 @@ def lib() -> C.CDLL:
     L.lbg_evolve_shared_p_soa_dev.argtypes = [vp, _sz, vp, vp, C.c_int64, C.c_int64, C.c_int, vp, vp]
     L.lbg_evolve_shared_p_aos_dev.argtypes = [vp, _sz, vp, C.c_int64, C.c_int64, C.c_int, vp, vp]
     L.lbg_evolve_shared_p.argtypes = [_dp, _sz, _dp, C.c_int64, C.c_int64, _dp, C.c_int]
+    L.lbg_density_workspace.argtypes = [_sz, C.c_int64]
+    L.lbg_density_workspace.restype = _sz
+    L.lbg_evolve_density_dev.argtypes = [vp, _sz, vp, C.c_int64, C.c_int64, C.c_int, vp, vp]
+    L.lbg_evolve_density.argtypes = [_dp, _sz, _dp, C.c_int64, C.c_int64, _dp]
     L.lbg_sweep_workspace.argtypes = [_sz, C.c_int64]
     L.lbg_sweep_workspace.restype = _sz
     L.lbg_evolve_sweep_dev.argtypes = [_sz, vp, vp, vp, _sz, vp, vp, vp, C.c_double, vp, C.c_int64,
@@ -223,7 +227,8 @@ def step_aos(p, v):
 
 
 def evolve_batch(p, rho0, n_steps: int, algo: str = "auto"):
-    """rho0: (B, d, d) complex -> final states (B, d, d). Host buffers, end-to-end."""
+    """rho0: (B, d, d) complex -> final states (B, d, d). Host buffers, end-to-end.
+    algo "density": the density-matrix mode (lbg_evolve_density, d*d <= 84)."""
     p, rho0 = _c128(p), _c128(rho0)
     if rho0.ndim != 3 or rho0.shape[1] != rho0.shape[2]:
         raise ValueError("evolve: states must be (B, d, d)")
@@ -231,6 +236,9 @@ def evolve_batch(p, rho0, n_steps: int, algo: str = "auto"):
     if p.shape != (d * d, d * d):
         raise ValueError("evolve: state dimension does not match propagator")
     out = np.empty_like(rho0)
+    if algo == "density":
+        _check(lib().lbg_evolve_density(_p(p), d, _p(rho0), B, int(n_steps), _p(out)), "evolve")
+        return out
     _check(lib().lbg_evolve_shared_p(_p(p), d, _p(rho0), B, int(n_steps), _p(out), ALGO[algo]), "evolve")
     return out
 
@@ -292,6 +300,25 @@ def evolve_batch_dev(p, x, n_steps: int, algo: str = "auto", work=None, stream=N
     B = x.shape[0]
     _check(lib().lbg_evolve_shared_p_aos_dev(_tp(p), n, _tp(x), B, int(n_steps), ALGO[algo], _tp(work),
                                              _sp(stream)), "evolve_shared_p_aos_dev")
+
+
+def density_workspace(n: int, batch: int) -> int:
+    return int(lib().lbg_density_workspace(n, batch))
+
+
+DENSITY_MODE = {"hermitian": 0, "general": 1, "auto": 2}
+
+
+def evolve_density_dev(p, rho, n_steps: int, work, mode: str = "auto", stream=None):
+    """Density-matrix mode (include/lbg.h lbg_evolve_density_dev): rho (B, d, d)
+    complex128 on the device, propagated in place through the real coordinates
+    with P_R = T P T^-1. mode "hermitian" asserts rho is stored exactly
+    Hermitian (its anti-Hermitian part is dropped), "general" propagates the
+    anti-Hermitian part too, "auto" does so only when it is non-zero."""
+    d = rho.shape[-1]
+    _check(lib().lbg_evolve_density_dev(_tp(p), d, _tp(rho), rho.shape[0], int(n_steps),
+                                        DENSITY_MODE[mode], _tp(work), _sp(stream)),
+           "evolve_density_dev")
 
 
 def sweep_workspace(d: int, batch: int) -> int:

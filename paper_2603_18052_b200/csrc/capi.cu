@@ -310,52 +310,97 @@ int lbg_evolve_shared_p_aos_dev(const double* p, size_t n, double* x, int64_t ba
   });
 }
 
+}  // extern "C"
+
+namespace {
+// Host-buffer evolve shared by lbg_evolve_shared_p and lbg_evolve_density.
+// Pipeline: the batch is cut into chunks that alternate between two streams,
+// so chunk k's H2D, chunk k-1's steps and chunk k-2's D2H overlap (copy
+// engines and SMs run concurrently). `single` forces one chunk (the
+// cooperative tiled kernel is never run concurrently with itself).
+template <class WorkBytes, class Step>
+void host_evolve_impl(const double* p, size_t d, const double* rho0, int64_t batch, double* out, bool single,
+                      WorkBytes work_bytes, Step step) {
+  if (d == 0) throw invalid_argument("evolve: state dimension must be positive");
+  if (batch < 0) throw invalid_argument("evolve: negative batch or steps");
+  if (batch == 0) return;
+  const size_t n = d * d;
+  const int64_t min_chunk = 32768;
+  const int nchunks = (single || batch < 2 * min_chunk) ? 1 : int(std::min<int64_t>(8, batch / min_chunk));
+  const int64_t chunk = (batch + nchunks - 1) / nchunks;
+  EvolvePool& pool = evolve_pool();
+  std::lock_guard<std::mutex> lk(pool.mu);
+  pool.ensure(n * n * 16, size_t(batch) * n * 16, size_t(nchunks) * 3 * 8, work_bytes(chunk));
+  double* dp = static_cast<double*>(pool.p.ptr);
+  double* dx = static_cast<double*>(pool.x.ptr);
+  double* dchk = static_cast<double*>(pool.chk.ptr);
+  check_cuda(cudaMemcpyAsync(dp, p, n * n * 16, cudaMemcpyHostToDevice, pool.st[0]), "H2D P");
+  check_cuda(cudaEventRecord(pool.ev_p, pool.st[0]), "event");
+  check_cuda(cudaStreamWaitEvent(pool.st[1], pool.ev_p, 0), "wait");
+  for (int c = 0; c < nchunks; ++c) {
+    const int64_t b0 = c * chunk, nb = std::min<int64_t>(chunk, batch - b0);
+    if (nb <= 0) break;
+    cudaStream_t s = pool.st[c & 1];
+    double* xc = dx + size_t(b0) * n * 2;
+    const size_t bytes = size_t(nb) * n * 16;
+    check_cuda(cudaMemcpyAsync(xc, rho0 + size_t(b0) * n * 2, bytes, cudaMemcpyHostToDevice, s), "H2D rho0");
+    // propagate.cpp:79 — every rho0 must pass check_state at 1e-8
+    launch_check_state(xc, d, nb, dchk + 3 * c, s);
+    step(dp, xc, nb, pool.w[c & 1].ptr, s);
+    check_cuda(cudaMemcpyAsync(out + size_t(b0) * n * 2, xc, bytes, cudaMemcpyDeviceToHost, s), "D2H rho");
+  }
+  std::vector<double> chk(size_t(nchunks) * 3);
+  check_cuda(cudaMemcpyAsync(chk.data(), dchk, chk.size() * 8, cudaMemcpyDeviceToHost, pool.st[1]), "D2H");
+  check_cuda(cudaStreamSynchronize(pool.st[0]), "sync");
+  check_cuda(cudaStreamSynchronize(pool.st[1]), "sync");
+  for (int c = 0; c < nchunks; ++c)
+    if (!(chk[3 * c] <= 1e-8 && chk[3 * c + 1] <= 1e-8 && chk[3 * c + 2] >= -1e-8))
+      throw invalid_argument("evolve: initial state fails physical-state checks");
+}
+}  // namespace
+
+extern "C" {
+
 int lbg_evolve_shared_p(const double* p, size_t d, const double* rho0, int64_t batch, int64_t steps,
                         double* out, int algo) {
+  return guarded([&] {
+    if (steps < 0) throw invalid_argument("evolve: negative batch or steps");
+    const size_t n = d * d;
+    const bool single = d > 0 && batch > 0 && choose_algo(n, batch, algo) == LBG_ALGO_TILED;
+    host_evolve_impl(p, d, rho0, batch, out, single,
+                     [&](int64_t chunk) { return lbg_evolve_workspace(n, chunk, algo); },
+                     [&](const double* dp, double* xc, int64_t nb, void* w, cudaStream_t s) {
+                       evolve_dev(dp, n, nullptr, nullptr, xc, nb, steps, algo, w, s, Layout::aos);
+                     });
+  });
+}
+
+int lbg_evolve_density(const double* p, size_t d, const double* rho0, int64_t batch, int64_t steps,
+                       double* out) {
+  return guarded([&] {
+    if (steps < 0) throw invalid_argument("evolve: negative batch or steps");
+    if (d > 0 && !density_supported(d * d)) throw invalid_argument("density mode supports d*d <= 84");
+    host_evolve_impl(p, d, rho0, batch, out, false,
+                     [&](int64_t chunk) { return density_workspace(d * d, chunk); },
+                     [&](const double* dp, double* xc, int64_t nb, void* w, cudaStream_t s) {
+                       launch_density(dp, d, xc, nb, steps, kDensityAuto, w, s);
+                     });
+  });
+}
+
+// ---- density-matrix mode (real coordinates) ----
+size_t lbg_density_workspace(size_t n, int64_t batch) {
+  return (n == 0 || batch <= 0) ? 0 : density_workspace(n, batch);
+}
+
+int lbg_evolve_density_dev(const double* p, size_t d, double* rho, int64_t batch, int64_t steps,
+                           int mode, void* work, void* stream) {
   return guarded([&] {
     if (d == 0) throw invalid_argument("evolve: state dimension must be positive");
     if (batch < 0 || steps < 0) throw invalid_argument("evolve: negative batch or steps");
     if (batch == 0) return;
-    const size_t n = d * d;
-    const int chosen = choose_algo(n, batch, algo);
-    // Pipeline: the batch is cut into chunks that alternate between two streams,
-    // so chunk k's H2D, chunk k-1's steps and chunk k-2's D2H overlap (copy
-    // engines and SMs run concurrently). The cooperative tiled kernel is never
-    // run concurrently with itself, so it gets a single chunk.
-    const int64_t min_chunk = 32768;
-    const int nchunks = (chosen == LBG_ALGO_TILED || batch < 2 * min_chunk)
-                            ? 1
-                            : int(std::min<int64_t>(8, batch / min_chunk));
-    const int64_t chunk = (batch + nchunks - 1) / nchunks;
-    EvolvePool& pool = evolve_pool();
-    std::lock_guard<std::mutex> lk(pool.mu);
-    pool.ensure(n * n * 16, size_t(batch) * n * 16, size_t(nchunks) * 3 * 8,
-                lbg_evolve_workspace(n, chunk, algo));
-    double* dp = static_cast<double*>(pool.p.ptr);
-    double* dx = static_cast<double*>(pool.x.ptr);
-    double* dchk = static_cast<double*>(pool.chk.ptr);
-    check_cuda(cudaMemcpyAsync(dp, p, n * n * 16, cudaMemcpyHostToDevice, pool.st[0]), "H2D P");
-    check_cuda(cudaEventRecord(pool.ev_p, pool.st[0]), "event");
-    check_cuda(cudaStreamWaitEvent(pool.st[1], pool.ev_p, 0), "wait");
-    for (int c = 0; c < nchunks; ++c) {
-      const int64_t b0 = c * chunk, nb = std::min<int64_t>(chunk, batch - b0);
-      if (nb <= 0) break;
-      cudaStream_t s = pool.st[c & 1];
-      double* xc = dx + size_t(b0) * n * 2;
-      const size_t bytes = size_t(nb) * n * 16;
-      check_cuda(cudaMemcpyAsync(xc, rho0 + size_t(b0) * n * 2, bytes, cudaMemcpyHostToDevice, s), "H2D rho0");
-      // propagate.cpp:79 — every rho0 must pass check_state at 1e-8
-      launch_check_state(xc, d, nb, dchk + 3 * c, s);
-      evolve_dev(dp, n, nullptr, nullptr, xc, nb, steps, algo, pool.w[c & 1].ptr, s, Layout::aos);
-      check_cuda(cudaMemcpyAsync(out + size_t(b0) * n * 2, xc, bytes, cudaMemcpyDeviceToHost, s), "D2H rho");
-    }
-    std::vector<double> chk(size_t(nchunks) * 3);
-    check_cuda(cudaMemcpyAsync(chk.data(), dchk, chk.size() * 8, cudaMemcpyDeviceToHost, pool.st[1]), "D2H");
-    check_cuda(cudaStreamSynchronize(pool.st[0]), "sync");
-    check_cuda(cudaStreamSynchronize(pool.st[1]), "sync");
-    for (int c = 0; c < nchunks; ++c)
-      if (!(chk[3 * c] <= 1e-8 && chk[3 * c + 1] <= 1e-8 && chk[3 * c + 2] >= -1e-8))
-        throw invalid_argument("evolve: initial state fails physical-state checks");
+    if (!p || !rho || !work) throw invalid_argument("evolve: null pointer");
+    launch_density(p, d, rho, batch, steps, mode, work, as_stream(stream));
   });
 }
 

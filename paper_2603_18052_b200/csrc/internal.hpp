@@ -59,6 +59,12 @@ bool rowsplit_supported(std::size_t n, int64_t batch);
 std::size_t rowsplit_workspace(std::size_t n, int64_t batch);
 void launch_rowsplit(const double* p, std::size_t n, double* x_aos, int64_t batch, int64_t steps,
                      void* work, cudaStream_t s);
+// density-matrix mode: shared P applied to the real coordinates (k_density.cu)
+bool density_supported(std::size_t n);
+std::size_t density_workspace(std::size_t n, int64_t batch);
+constexpr int kDensityHermitian = 0, kDensityGeneral = 1, kDensityAuto = 2;  // LBG_DENSITY_*
+void launch_density(const double* p, std::size_t d, double* rho, int64_t batch, int64_t steps,
+                    int mode, void* work, cudaStream_t s);
 // plain batched complex GEMM C[b] = A[b] * B[b] (n x n, AoS), DMMA tiles;
 // strides in complex elements
 void launch_zgemm(const double* a, const double* b, double* c, int n, int batch,
