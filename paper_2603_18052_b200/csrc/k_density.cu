@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(128) dfma9r_kernel(double* __restrict__ x, int
   count = live_count(count, half, flag);
   if (int64_t(blockIdx.x) * 128 * TPT >= count) return;
   // TPT trajectories per thread (coalesced: t, t + 128, ...): each P operand
-  // load feeds TPT FMAs, and TPT x 18 independent FMA chains hide DFMA latency
+  // load feeds TPT FMAs, and TPT x 9 independent FMA chains hide DFMA latency
   const int64_t base = int64_t(blockIdx.x) * 128 * TPT + threadIdx.x;
   double v[TPT][9];
 #pragma unroll
@@ -130,21 +130,19 @@ __global__ void __launch_bounds__(128) dfma9r_kernel(double* __restrict__ x, int
     double nv[TPT][9];
 #pragma unroll
     for (int i = 0; i < 9; ++i) {
-      double a[TPT], b[TPT];
+      // one accumulator per (trajectory, row): TPT x 9 independent 9-deep
+      // chains, and no DADD tail (every FP64 instruction is a useful FMA)
+      double a[TPT];
 #pragma unroll
-      for (int u = 0; u < TPT; ++u) a[u] = b[u] = 0.0;
+      for (int u = 0; u < TPT; ++u) a[u] = 0.0;
 #pragma unroll
-      for (int j = 0; j < 9; j += 2) {
-        const double p0 = p[i * 9 + j];
-        const double p1 = j + 1 < 9 ? p[i * 9 + j + 1] : 0.0;
+      for (int j = 0; j < 9; ++j) {
+        const double pij = p[i * 9 + j];
 #pragma unroll
-        for (int u = 0; u < TPT; ++u) {
-          a[u] = fma(p0, v[u][j], a[u]);
-          if (j + 1 < 9) b[u] = fma(p1, v[u][j + 1], b[u]);
-        }
+        for (int u = 0; u < TPT; ++u) a[u] = fma(pij, v[u][j], a[u]);
       }
 #pragma unroll
-      for (int u = 0; u < TPT; ++u) nv[u][i] = a[u] + b[u];
+      for (int u = 0; u < TPT; ++u) nv[u][i] = a[u];
     }
 #pragma unroll
     for (int u = 0; u < TPT; ++u)

@@ -1,4 +1,5 @@
-"""Run one config's hot path a few times (for ncu captures): python tools/prof_cfg.py CFG [PASSES]"""
+"""Run one config's hot path a few times (for ncu captures):
+python tools/prof_cfg.py CFG [PASSES] [density]"""
 import os
 import sys
 
@@ -16,8 +17,16 @@ d, B, S = bench.CONFIGS[cfg]
 if cfg == 4:
     case = bench.SweepCase(torch, lbg, dev, 0, B)
     fn = case.run
+elif len(sys.argv) > 3 and sys.argv[3] == "density":
+    _, rho0, pt, _, _ = R.shared_p_setup(cfg, B)
+    xt = torch.from_numpy(rho0).to(dev)
+    work = torch.empty(lbg.density_workspace(d * d, B), dtype=torch.uint8, device=dev)
+
+    def fn():
+        lbg.evolve_density_dev(pt, xt, S, work)
 else:
     _, _, pt, xt, work = R.shared_p_setup(cfg, B)
+
     def fn():
         lbg.evolve_batch_dev(pt, xt, S, work=work)
 for _ in range(passes):
