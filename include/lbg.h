@@ -224,6 +224,47 @@ int lbg_write_matrix(const double* a, size_t rows, size_t cols, char* buf, size_
 int lbg_read_matrix(const char* text, size_t* rows, size_t* cols, double* out, size_t cap_elems);
 int lbg_read_model(const char* text, size_t* d, size_t* n_ops, double* h, double* ops, size_t cap_ops);
 
+/* ------------------------------------------------------------------------
+ * Kernel benchmark harness: replaces lb::run_bench / lb::write_csv /
+ * lb::write_json (bench.hpp:14-37, bench.cpp:70-158, 202-248) for the GPU.
+ * A bench is a chain of `warmup` untimed + `reps` timed steps of one random
+ * P (uniform [-1,1] re/im from std::mt19937_64(seed), scaled by 1/d^2) on one
+ * random vector, exactly the reference's inputs (bench.cpp:81-86,
+ * random.hpp:12-22); `batch` (GPU extension, >= 1) runs that many copies of
+ * the chain at once. checksum = sum of trajectory 0's final vector.
+ * gflops = 8 d^4 / ns_per_step, gbs = 16 (d^4 + 2 d^2) / ns_per_step
+ * (roofline.cpp:62-74). variant: LBG_VARIANT_AOS / SOA (kernels.hpp:15);
+ * LBG_VARIANT_SIMD is the reference's AVX2 path and fails with LBG_ERUNTIME
+ * like an unavailable variant (bench.cpp:77-78).
+ * lbg_run_bench: timed with CUDA events around the `reps` steps. Errors also
+ * set out->failed and out->error (for the writers' "# failed" rows).
+ * lbg_write_bench_csv / _json: the reference's report formats (same columns
+ * / keys, same number formatting) plus the GPU columns batch, algo,
+ * traj_steps_per_s; buf = NULL queries *len.
+ * ------------------------------------------------------------------------ */
+#define LBG_VARIANT_AOS 0
+#define LBG_VARIANT_SOA 1
+#define LBG_VARIANT_SIMD 2
+typedef struct {
+  size_t dim;
+  int variant;
+  int64_t reps, warmup;
+  uint64_t seed;
+  int64_t batch;
+} lbg_bench_config;
+typedef struct {
+  double ns_per_step, gflops, gbs, checksum_re, checksum_im, traj_steps_per_s;
+  int algo, failed;
+  char error[224];
+} lbg_bench_result;
+const char* lbg_bench_last_error(void); /* message of the last failed inputs / writer call */
+int lbg_bench_inputs(size_t dim, uint64_t seed, double* p, double* v0);
+int lbg_run_bench(const lbg_bench_config* cfg, lbg_bench_result* out);
+int lbg_write_bench_csv(const lbg_bench_config* cfgs, const lbg_bench_result* res, size_t count,
+                        const char* machine, char* buf, size_t cap, size_t* len);
+int lbg_write_bench_json(const lbg_bench_config* cfgs, const lbg_bench_result* res, size_t count,
+                         const char* machine, char* buf, size_t cap, size_t* len);
+
 /* FP64 roofline denominators measured live on the current device (TF/s):
  * register-only DMMA (m8n8k4 f64) and DFMA loops over every SM. */
 int lbg_fp64_peak(double* dmma_tflops, double* dfma_tflops);

@@ -266,3 +266,53 @@ class Reference:
         self._rc(self.lib.ref_sweep_batch(_ptr(deltas), _ptr(scales), B, steps, _ptr(pops), _ptr(ens),
                                           threads, C.byref(secs)), "sweep_batch")
         return pops, ens, secs.value
+
+    # ---- kernel benchmark harness (bench.cpp) ----
+    def bench_inputs(self, dim, seed=42):
+        """(P, v0) exactly as lb::run_bench draws them (bench.cpp:81-86)."""
+        L = self.lib
+        L.ref_bench_inputs.argtypes = [C.c_size_t, C.c_uint64, _dp, _dp]
+        n = dim * dim
+        p = np.zeros((n, n), np.complex128)
+        v = np.zeros(n, np.complex128)
+        self._rc(L.ref_bench_inputs(dim, seed, _ptr(p), _ptr(v)), "bench_inputs")
+        return p, v
+
+    def run_bench(self, dim, variant="soa", reps=50000, warmup=10, seed=42, profile=""):
+        """lb::run_bench -> dict(ns_per_step, gflops, gbs, checksum)."""
+        L = self.lib
+        L.ref_run_bench.argtypes = [C.c_size_t, C.c_int, C.c_size_t, C.c_size_t, C.c_uint64, C.c_char_p, _dp]
+        out = np.zeros(5)
+        v = {"aos": 0, "soa": 1, "simd": 2}[variant]
+        self._rc(L.ref_run_bench(dim, v, reps, warmup, seed, profile.encode(), _ptr(out)), "run_bench")
+        return dict(ns_per_step=out[0], gflops=out[1], gbs=out[2], checksum=complex(out[3], out[4]))
+
+    def write_bench(self, rows, machine, json=False, profile="b200"):
+        """lb::write_csv / lb::write_json (bench.cpp:202-248) of rows: dicts with dim,
+        variant, reps, warmup and either failed/error or ns_per_step, gflops, gbs, checksum."""
+        L = self.lib
+        sz = C.c_size_t
+        L.ref_write_bench.argtypes = [C.c_int, sz, C.POINTER(sz), C.POINTER(C.c_int), C.POINTER(sz),
+                                      C.POINTER(sz), C.POINTER(C.c_int), _dp, C.c_char_p, C.c_char_p,
+                                      C.c_char_p, C.c_char_p, sz, C.POINTER(sz)]
+        n = len(rows)
+        arr = lambda t, xs: (t * max(n, 1))(*xs)  # noqa: E731
+        dims = arr(sz, [r["dim"] for r in rows])
+        var = arr(C.c_int, [{"aos": 0, "soa": 1, "simd": 2}[r["variant"]] for r in rows])
+        reps = arr(sz, [r["reps"] for r in rows])
+        warm = arr(sz, [r["warmup"] for r in rows])
+        failed = arr(C.c_int, [int(r.get("failed", False)) for r in rows])
+        vals = np.zeros(5 * max(n, 1))
+        for i, r in enumerate(rows):
+            if not r.get("failed"):
+                c = complex(r["checksum"])
+                vals[5 * i:5 * i + 5] = [r["ns_per_step"], r["gflops"], r["gbs"], c.real, c.imag]
+        errs = "\n".join(r.get("error", "") for r in rows).encode()
+        ln = sz()
+        self._rc(L.ref_write_bench(int(json), n, dims, var, reps, warm, failed, _ptr(vals), errs,
+                                   profile.encode(), machine.encode(), None, 0, C.byref(ln)), "write_bench")
+        buf = C.create_string_buffer(ln.value + 1)
+        self._rc(L.ref_write_bench(int(json), n, dims, var, reps, warm, failed, _ptr(vals), errs,
+                                   profile.encode(), machine.encode(), buf, ln.value + 1, C.byref(ln)),
+                 "write_bench")
+        return buf.value.decode()

@@ -23,11 +23,13 @@
 #include <thread>
 #include <vector>
 
+#include "lb/bench.hpp"
 #include "lb/complex_matrix.hpp"
 #include "lb/expm.hpp"
 #include "lb/kernels.hpp"
 #include "lb/lindblad.hpp"
 #include "lb/propagate.hpp"
+#include "lb/random.hpp"
 #include "lb/model_io.hpp"
 #include "lb/random.hpp"
 #include <sstream>
@@ -330,6 +332,73 @@ int ref_check_state(const double* rho, std::size_t d, double tol, double* trace_
         *min_diag = r.min_diagonal;
         if (!r.passed) throw std::runtime_error("check_state failed");
     });
+}
+
+// The benchmark harness's inputs exactly as lb::run_bench draws them
+// (bench.cpp:81-86): lb::make_rng + lb::random_matrix, P scaled by 1/d^2.
+int ref_bench_inputs(std::size_t dim, std::uint64_t seed, double* p, double* v0) {
+  return guarded([&] {
+    const std::size_t n = dim * dim;
+    auto rng = lb::make_rng(seed);
+    lb::MatrixAoS pm = lb::random_matrix(rng, n, n);
+    const lb::cplx scale{1.0 / double(dim * dim), 0.0};
+    for (auto& z : pm.data) z *= scale;
+    const lb::VectorAoS v = lb::random_matrix(rng, n, 1);
+    std::memcpy(p, pm.data.data(), n * n * sizeof(lb::cplx));
+    std::memcpy(v0, v.data.data(), n * sizeof(lb::cplx));
+  });
+}
+
+// lb::run_bench (bench.cpp:70-158): out = ns_per_step, gflops, gbs, checksum re, im
+int ref_run_bench(std::size_t dim, int variant, std::size_t reps, std::size_t warmup, std::uint64_t seed,
+                  const char* profile, double* out) {
+  return guarded([&] {
+    lb::BenchConfig c{dim, static_cast<lb::Variant>(variant), reps, warmup, seed, profile ? profile : ""};
+    const lb::BenchResult r = lb::run_bench(c);
+    out[0] = r.ns_per_step;
+    out[1] = r.gflops;
+    out[2] = r.gbs;
+    out[3] = r.checksum.real();
+    out[4] = r.checksum.imag();
+  });
+}
+
+// lb::write_csv / lb::write_json (bench.cpp:202-248) of rows given as arrays:
+// per row dims, variants, reps, warmups, failed flags, values[5] (ns, gflops,
+// gbs, checksum re, im) and '\n'-separated error messages.
+int ref_write_bench(int json, std::size_t count, const std::size_t* dims, const int* variants,
+                    const std::size_t* reps, const std::size_t* warmups, const int* failed,
+                    const double* values, const char* errors, const char* profile, const char* machine,
+                    char* buf, std::size_t cap, std::size_t* len) {
+  return guarded([&] {
+    std::vector<lb::BenchResult> rows(count);
+    std::string errs = errors ? errors : "";
+    std::size_t pos = 0;
+    for (std::size_t i = 0; i < count; ++i) {
+      lb::BenchResult& r = rows[i];
+      r.config.dim = dims[i];
+      r.config.variant = static_cast<lb::Variant>(variants[i]);
+      r.config.reps = reps[i];
+      r.config.warmup = warmups[i];
+      r.profile_name = profile;
+      r.failed = failed[i] != 0;
+      const std::size_t nl = errs.find('\n', pos);
+      r.error = errs.substr(pos, nl == std::string::npos ? std::string::npos : nl - pos);
+      pos = nl == std::string::npos ? errs.size() : nl + 1;
+      r.ns_per_step = values[5 * i];
+      r.gflops = values[5 * i + 1];
+      r.gbs = values[5 * i + 2];
+      r.checksum = lb::cplx{values[5 * i + 3], values[5 * i + 4]};
+    }
+    std::ostringstream os;
+    if (json)
+      lb::write_json(os, rows, machine);
+    else
+      lb::write_csv(os, rows, machine);
+    const std::string s = os.str();
+    *len = s.size();
+    if (buf && cap > s.size()) std::memcpy(buf, s.c_str(), s.size() + 1);
+  });
 }
 
 }  // extern "C"

@@ -395,3 +395,84 @@ def read_model(text: str):
 def read_model_file(path: str):
     with open(path) as f:
         return read_model(f.read())
+
+
+# ---------------------------------------------------- benchmark harness ---
+class BenchConfig(C.Structure):
+    """lbg_bench_config (include/lbg.h) — lb::BenchConfig (bench.hpp:14-21) + batch."""
+    _fields_ = [("dim", C.c_size_t), ("variant", C.c_int), ("reps", C.c_int64), ("warmup", C.c_int64),
+                ("seed", C.c_uint64), ("batch", C.c_int64)]
+
+
+class BenchResult(C.Structure):
+    """lbg_bench_result — lb::BenchResult (bench.hpp:23-32) + the GPU columns."""
+    _fields_ = [("ns_per_step", C.c_double), ("gflops", C.c_double), ("gbs", C.c_double),
+                ("checksum_re", C.c_double), ("checksum_im", C.c_double), ("traj_steps_per_s", C.c_double),
+                ("algo", C.c_int), ("failed", C.c_int), ("error", C.c_char * 224)]
+
+
+VARIANT = {"aos": 0, "soa": 1, "simd": 2}
+
+
+def bench_config(dim: int, variant: str = "soa", reps: int = 50000, warmup: int = 10, seed: int = SEED,
+                 batch: int = 1) -> BenchConfig:
+    return BenchConfig(dim, VARIANT[variant], reps, warmup, seed, batch)
+
+
+def bench_inputs(dim: int, seed: int = SEED):
+    """(P, v0) of lb::run_bench (bench.cpp:81-86), bit-identical to the reference."""
+    n = dim * dim
+    p = np.zeros((n, n), np.complex128)
+    v = np.zeros(n, np.complex128)
+    L = lib()
+    L.lbg_bench_inputs.argtypes = [_sz, C.c_uint64, _dp, _dp]
+    L.lbg_bench_last_error.restype = C.c_char_p
+    rc = L.lbg_bench_inputs(dim, seed, _p(p), _p(v))
+    if rc:
+        raise ValueError(L.lbg_bench_last_error().decode())
+    return p, v
+
+
+def run_bench(cfg: BenchConfig, raise_on_error: bool = True) -> BenchResult:
+    """lb::run_bench on the GPU (lbg_run_bench): a timed chain of cfg.reps steps."""
+    L = lib()
+    L.lbg_run_bench.argtypes = [C.POINTER(BenchConfig), C.POINTER(BenchResult)]
+    res = BenchResult()
+    rc = L.lbg_run_bench(C.byref(cfg), C.byref(res))
+    if rc and raise_on_error:
+        _check(rc, "run_bench")
+    return res
+
+
+def run_matrix(dims, variants, reps: int, warmup: int, seed: int = SEED, batch: int = 1):
+    """lb::run_matrix (bench.cpp:160-185): every (dim, variant); failures kept as rows."""
+    cfgs = [bench_config(d, v, reps, warmup, seed, batch) for d in dims for v in variants]
+    return cfgs, [run_bench(c, raise_on_error=False) for c in cfgs]
+
+
+def _write_bench(fn_name: str, cfgs, results, machine: str) -> str:
+    L = lib()
+    fn = getattr(L, fn_name)
+    fn.argtypes = [C.POINTER(BenchConfig), C.POINTER(BenchResult), _sz, C.c_char_p, C.c_char_p, _sz,
+                   C.POINTER(_sz)]
+    L.lbg_bench_last_error.restype = C.c_char_p
+    n = len(cfgs)
+    ca = (BenchConfig * max(n, 1))(*cfgs)
+    ra = (BenchResult * max(n, 1))(*results)
+    ln = _sz()
+    if fn(ca, ra, n, machine.encode(), None, 0, C.byref(ln)):
+        raise ValueError(L.lbg_bench_last_error().decode())
+    buf = C.create_string_buffer(ln.value + 1)
+    if fn(ca, ra, n, machine.encode(), buf, ln.value + 1, C.byref(ln)):
+        raise ValueError(L.lbg_bench_last_error().decode())
+    return buf.value.decode()
+
+
+def write_bench_csv(cfgs, results, machine: str) -> str:
+    """lb::write_csv (bench.cpp:202-221) + GPU columns."""
+    return _write_bench("lbg_write_bench_csv", cfgs, results, machine)
+
+
+def write_bench_json(cfgs, results, machine: str) -> str:
+    """lb::write_json (bench.cpp:223-246) + GPU keys."""
+    return _write_bench("lbg_write_bench_json", cfgs, results, machine)

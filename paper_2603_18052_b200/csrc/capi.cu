@@ -126,6 +126,21 @@ void evolve_dev(const double* p, size_t n, double* x_re, double* x_im, double* x
   if (batch == 0 || steps == 0) return;
   if (layout == Layout::soa && (!x_re || !x_im)) throw invalid_argument("evolve: null state");
   if (layout == Layout::aos && !x_aos) throw invalid_argument("evolve: null state");
+  if (layout == Layout::soa && algo == LBG_ALGO_AUTO) {
+    // the latency kernels take AoS: SoA callers in that regime are staged
+    // through an interleaved copy in the workspace (lbg_evolve_workspace sizes it)
+    const int a = choose_algo(n, batch, LBG_ALGO_AUTO, Layout::aos);
+    if (a == LBG_ALGO_CTA || a == LBG_ALGO_ROWSPLIT) {
+      if (!work) throw invalid_argument("evolve: workspace required");
+      const size_t inner = a == LBG_ALGO_ROWSPLIT ? rowsplit_workspace(n, batch) : 0;
+      double* stage = reinterpret_cast<double*>(static_cast<char*>(work) + ((inner + 255) & ~size_t(255)));
+      const long long count = (long long)batch * (long long)n;
+      launch_planes_to_aos(x_re, x_im, count, stage, s);
+      evolve_dev(p, n, nullptr, nullptr, stage, batch, steps, a, work, s, Layout::aos);
+      launch_aos_to_planes(stage, count, x_re, x_im, s);
+      return;
+    }
+  }
   switch (choose_algo(n, batch, algo, layout)) {
     case LBG_ALGO_CHAIN:
       if (!chain_supported(n)) throw invalid_argument("evolve: chain kernel needs n <= 16");
@@ -289,10 +304,15 @@ int lbg_expm(const double* a, size_t n, double dt, double* out) {
 // ---- batched shared-P propagation ----
 size_t lbg_evolve_workspace(size_t n, int64_t batch, int algo) {
   if (n == 0 || batch <= 0) return 0;
-  switch (choose_algo(n, batch, algo)) {
+  const int a = choose_algo(n, batch, algo);
+  // SoA callers of the AoS-only latency kernels stage an interleaved copy
+  const size_t stage = algo == LBG_ALGO_AUTO && (a == LBG_ALGO_CTA || a == LBG_ALGO_ROWSPLIT)
+                           ? size_t(batch) * n * 16 : 0;
+  switch (a) {
     case LBG_ALGO_TILED: return tiled_workspace(n, batch);
-    case LBG_ALGO_ROWSPLIT: return rowsplit_supported(n, batch) ? rowsplit_workspace(n, batch) : 0;
-    default: return 0;
+    case LBG_ALGO_ROWSPLIT:
+      return rowsplit_supported(n, batch) ? ((rowsplit_workspace(n, batch) + 255) & ~size_t(255)) + stage : 0;
+    default: return stage;
   }
 }
 
@@ -402,6 +422,100 @@ int lbg_evolve_density_dev(const double* p, size_t d, double* rho, int64_t batch
     if (!p || !rho || !work) throw invalid_argument("evolve: null pointer");
     launch_density(p, d, rho, batch, steps, mode, work, as_stream(stream));
   });
+}
+
+// ---- kernel benchmark harness (bench.cpp:70-158) ----
+int lbg_run_bench(const lbg_bench_config* cfg, lbg_bench_result* out) {
+  if (out) std::memset(out, 0, sizeof *out);
+  const int rc = guarded([&] {
+    if (!cfg || !out) throw invalid_argument("bench: null config or result");
+    if (cfg->dim < 1) throw invalid_argument("bench: dim must be >= 1");
+    if (cfg->reps < 1) throw invalid_argument("bench: reps must be >= 1");
+    if (cfg->warmup < 0) throw invalid_argument("bench: warmup must be >= 0");
+    if (cfg->variant == LBG_VARIANT_SIMD)
+      throw lbg::runtime_error("bench: simd variant unavailable on this platform");
+    if (cfg->variant != LBG_VARIANT_AOS && cfg->variant != LBG_VARIANT_SOA)
+      throw invalid_argument("bench: unknown variant");
+    const size_t d = cfg->dim, n = d * d;
+    const int64_t batch = cfg->batch < 1 ? 1 : cfg->batch;
+    std::vector<double> p(2 * n * n), v0(2 * n);
+    if (lbg_bench_inputs(d, cfg->seed, p.data(), v0.data()) != LBG_OK)
+      throw invalid_argument(lbg_bench_last_error());
+    const Layout layout = cfg->variant == LBG_VARIANT_SOA ? Layout::soa : Layout::aos;
+    // automatic regime; SoA inputs in the latency regime are staged to AoS (evolve_dev)
+    const int algo = choose_algo(n, batch, LBG_ALGO_AUTO, Layout::aos);
+    // state: AoS (batch x n complex) or SoA planes; every trajectory starts at v0
+    std::vector<double> x0(size_t(batch) * 2 * n);
+    for (int64_t b = 0; b < batch; ++b)
+      for (size_t e = 0; e < n; ++e) {
+        if (layout == Layout::aos) {
+          x0[(size_t(b) * n + e) * 2] = v0[2 * e];
+          x0[(size_t(b) * n + e) * 2 + 1] = v0[2 * e + 1];
+        } else {
+          x0[size_t(b) * n + e] = v0[2 * e];
+          x0[size_t(batch) * n + size_t(b) * n + e] = v0[2 * e + 1];
+        }
+      }
+    DevBuf dp(p.size() * 8), dx(x0.size() * 8), dw(std::max<size_t>(lbg_evolve_workspace(n, batch, LBG_ALGO_AUTO), 1));
+    check_cuda(cudaMemcpy(dp.p, p.data(), p.size() * 8, cudaMemcpyHostToDevice), "H2D");
+    check_cuda(cudaMemcpy(dx.p, x0.data(), x0.size() * 8, cudaMemcpyHostToDevice), "H2D");
+    double* xa = dx.as<double>();
+    double* xr = layout == Layout::soa ? xa : nullptr;
+    double* xi = layout == Layout::soa ? xa + size_t(batch) * n : nullptr;
+    auto run = [&](int64_t steps) {
+      evolve_dev(dp.as<double>(), n, xr, xi, layout == Layout::aos ? xa : nullptr, batch, steps, LBG_ALGO_AUTO,
+                 dw.p, nullptr, layout);
+    };
+    cudaEvent_t e0, e1;
+    check_cuda(cudaEventCreate(&e0), "event");
+    check_cuda(cudaEventCreate(&e1), "event");
+    float ms = 0.f;
+    try {
+      run(cfg->warmup);  // bench.cpp:96-100 / 122-125: same chain, untimed
+      check_cuda(cudaEventRecord(e0, nullptr), "event record");
+      run(cfg->reps);
+      check_cuda(cudaEventRecord(e1, nullptr), "event record");
+      check_cuda(cudaEventSynchronize(e1), "event sync");
+      check_cuda(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+    } catch (...) {
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      throw;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const double block_ns = double(ms) * 1e6;
+    const double resolution_ns = 500.0;  // CUDA event timer resolution
+    if (resolution_ns > 0.1 * block_ns)  // bench.cpp:140-144
+      throw lbg::runtime_error("bench: timer resolution (500 ns) exceeds 10% of the measured block; increase reps");
+    std::vector<double> fin(2 * n);
+    if (layout == Layout::aos) {
+      check_cuda(cudaMemcpy(fin.data(), xa, 2 * n * 8, cudaMemcpyDeviceToHost), "D2H");
+    } else {
+      std::vector<double> re(n), im(n);
+      check_cuda(cudaMemcpy(re.data(), xr, n * 8, cudaMemcpyDeviceToHost), "D2H");
+      check_cuda(cudaMemcpy(im.data(), xi, n * 8, cudaMemcpyDeviceToHost), "D2H");
+      for (size_t e = 0; e < n; ++e) {
+        fin[2 * e] = re[e];
+        fin[2 * e + 1] = im[e];
+      }
+    }
+    std::complex<double> checksum{0.0, 0.0};  // bench.cpp:106,133: sum of the final vector
+    for (size_t e = 0; e < n; ++e) checksum += std::complex<double>{fin[2 * e], fin[2 * e + 1]};
+    const double d2 = double(d) * double(d), d4 = d2 * d2;
+    out->ns_per_step = block_ns / double(cfg->reps);
+    out->gflops = 8.0 * d4 / out->ns_per_step;
+    out->gbs = (d4 + 2.0 * d2) * 16.0 / out->ns_per_step;
+    out->checksum_re = checksum.real();
+    out->checksum_im = checksum.imag();
+    out->traj_steps_per_s = double(batch) * double(cfg->reps) / (block_ns * 1e-9);
+    out->algo = algo;
+  });
+  if (rc != LBG_OK && out) {
+    out->failed = 1;
+    std::snprintf(out->error, sizeof out->error, "%s", g_err.c_str());
+  }
+  return rc;
 }
 
 // ---- per-trajectory sweep (config 4) ----

@@ -77,6 +77,9 @@ void expm_dev(const double* a, std::size_t n, double dt, double* out, double* wo
               cudaStream_t s);
 void launch_check_state(const double* x, std::size_t d, int64_t batch, double* out3,
                         cudaStream_t s);
+void launch_planes_to_aos(const double* re, const double* im, long long count, double* out,
+                          cudaStream_t s);
+void launch_aos_to_planes(const double* in, long long count, double* re, double* im, cudaStream_t s);
 void launch_step_once(const double* p, const double* v, double* out, std::size_t n,
                       cudaStream_t s);
 

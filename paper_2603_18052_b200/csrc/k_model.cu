@@ -151,6 +151,22 @@ __global__ void check_state_init(unsigned long long* keys) {
 }
 
 // one matvec out[i] = sum_j P[i][j] v[j] (the raw-pointer shim), ascending j
+// SoA planes <-> AoS (interleaved) for the AoS-only latency kernels
+__global__ void planes_to_aos_kernel(const double* __restrict__ re, const double* __restrict__ im, long long count,
+                                     double2* __restrict__ out) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e < count) out[e] = make_double2(re[e], im[e]);
+}
+__global__ void aos_to_planes_kernel(const double2* __restrict__ in, long long count, double* __restrict__ re,
+                                     double* __restrict__ im) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e < count) {
+    const double2 z = in[e];
+    re[e] = z.x;
+    im[e] = z.y;
+  }
+}
+
 __global__ void step_once_kernel(const double2* __restrict__ p, const double2* __restrict__ v,
                                  double2* __restrict__ out, int n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -263,6 +279,18 @@ void launch_step_once(const double* p, const double* v, double* out, size_t n, c
       reinterpret_cast<const double2*>(p), reinterpret_cast<const double2*>(v),
       reinterpret_cast<double2*>(out), int(n));
   LBG_CHECK_LAUNCH("step_once_kernel");
+}
+
+void launch_planes_to_aos(const double* re, const double* im, long long count, double* out, cudaStream_t s) {
+  if (count <= 0) return;
+  planes_to_aos_kernel<<<unsigned((count + 255) / 256), 256, 0, s>>>(re, im, count, reinterpret_cast<double2*>(out));
+  LBG_CHECK_LAUNCH("planes_to_aos_kernel");
+}
+void launch_aos_to_planes(const double* in, long long count, double* re, double* im, cudaStream_t s) {
+  if (count <= 0) return;
+  aos_to_planes_kernel<<<unsigned((count + 255) / 256), 256, 0, s>>>(reinterpret_cast<const double2*>(in), count,
+                                                                     re, im);
+  LBG_CHECK_LAUNCH("aos_to_planes_kernel");
 }
 
 }  // namespace lbg
