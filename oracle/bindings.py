@@ -61,6 +61,7 @@ class Oracle:
         L.lbo_uniform.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64]
         L.lbo_uniform.restype = C.c_double
         L.lbo_ginibre_rho.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, sz, _dp]
+        L.lbo_ginibre_batch.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, sz, _dp]
         L.lbo_sweep_params.argtypes = [C.c_uint64, C.c_uint64, _dp, _dp]
 
     def kron(self, a, b):
@@ -140,6 +141,11 @@ class Oracle:
     def ginibre_rho(self, seed, cfg, traj, d):
         out = np.zeros((d, d), np.complex128)
         self.lib.lbo_ginibre_rho(seed, cfg, traj, d, _ptr(out))
+        return out
+
+    def ginibre_batch(self, seed, cfg, first, count, d):
+        out = np.zeros((count, d, d), np.complex128)
+        self.lib.lbo_ginibre_batch(seed, cfg, first, count, d, _ptr(out))
         return out
 
     def sweep_params(self, seed, traj):

@@ -479,6 +479,11 @@ void lbo_ginibre_rho(uint64_t seed, uint32_t cfg, uint64_t traj, size_t d, doubl
     free(g); free(gd);
 }
 
+/* trajectories [first, first + count) of lbo_ginibre_rho, out: count x d x d */
+void lbo_ginibre_batch(uint64_t seed, uint32_t cfg, uint64_t first, uint64_t count, size_t d, double* out) {
+  for (uint64_t b = 0; b < count; ++b) lbo_ginibre_rho(seed, cfg, first + b, d, out + b * 2 * d * d);
+}
+
 void lbo_sweep_params(uint64_t seed, uint64_t traj, double* delta, double* s) {
     const double u = lbo_uniform(seed, 4, traj, 0);
     const double v = lbo_uniform(seed, 4, traj, 1);
