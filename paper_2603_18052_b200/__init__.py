@@ -226,9 +226,33 @@ def step_aos(p, v):
     return out
 
 
-def evolve_batch(p, rho0, n_steps: int, algo: str = "auto"):
+def simd_available() -> bool:
+    """lb::simd_available (kernels.hpp): the reference's AVX2 path has no GPU
+    counterpart; the GPU kernels serve the aos and soa variants."""
+    return False
+
+
+def step_simd(p, v):
+    """lb::step_simd (propagate.hpp:26-28): throws like the reference on a
+    platform without the SIMD path (std::runtime_error)."""
+    raise RuntimeError("step_simd: SIMD variant unavailable on this platform")
+
+
+def _layout_check(layout: str) -> None:
+    # lb::Variant (kernels.hpp:15); evolve throws std::runtime_error for an
+    # unavailable variant (propagate.cpp:99-100)
+    if layout == "simd":
+        raise RuntimeError("evolve: SIMD variant unavailable on this platform")
+    if layout not in ("aos", "soa"):
+        raise ValueError(f"evolve: unknown layout {layout!r}")
+
+
+def evolve_batch(p, rho0, n_steps: int, algo: str = "auto", layout: str = "soa"):
     """rho0: (B, d, d) complex -> final states (B, d, d). Host buffers, end-to-end.
-    algo "density": the density-matrix mode (lbg_evolve_density, d*d <= 84)."""
+    algo "density": the density-matrix mode (lbg_evolve_density, d*d <= 84).
+    layout: the reference's Variant; both "aos" and "soa" run the GPU kernels
+    (the device layout is the engine's choice), "simd" raises like lb::evolve."""
+    _layout_check(layout)
     p, rho0 = _c128(p), _c128(rho0)
     if rho0.ndim != 3 or rho0.shape[1] != rho0.shape[2]:
         raise ValueError("evolve: states must be (B, d, d)")
@@ -243,12 +267,14 @@ def evolve_batch(p, rho0, n_steps: int, algo: str = "auto"):
     return out
 
 
-def evolve(p, rho0, n_steps: int, algo: str = "auto"):
-    """lb::evolve for one trajectory (propagate.cpp:75-109), on the GPU."""
+def evolve(p, rho0, n_steps: int, layout: str = "soa", algo: str = "auto"):
+    """lb::evolve(prop, rho0, n_steps, layout) for one trajectory
+    (propagate.hpp:33-34, propagate.cpp:75-109), on the GPU."""
+    _layout_check(layout)
     rho0 = _c128(rho0)
     if rho0.ndim != 2 or rho0.shape[0] != rho0.shape[1]:
         raise ValueError("evolve: state must be square")
-    return evolve_batch(p, rho0[None], n_steps, algo)[0]
+    return evolve_batch(p, rho0[None], n_steps, algo, layout)[0]
 
 
 def grape_chain(h0, hc, amplitudes, steps_per_segment: int, dt: float, dissipators, rho0):

@@ -76,6 +76,14 @@ def test_python_validation_before_gpu(lbg):
         lbg.expm(np.zeros((2, 3)), 0.1)
     with pytest.raises(ValueError):
         lbg.config_dims(7)
+    # lb::Variant::simd has no GPU counterpart: std::runtime_error like propagate.cpp:99-100
+    assert not lbg.simd_available()
+    with pytest.raises(RuntimeError):
+        lbg.evolve(np.eye(4), np.diag([1.0, 0.0]).astype(complex), 1, layout="simd")
+    with pytest.raises(RuntimeError):
+        lbg.step_simd(np.eye(4), np.zeros(4))
+    with pytest.raises(ValueError):
+        lbg.evolve(np.eye(4), np.diag([1.0, 0.0]).astype(complex), 1, layout="avx512")
 
 
 def test_check_state_host_contract(lbg):
