@@ -5,11 +5,14 @@
 // One step is a complex GEMM  V_next (n x B) = P (n x n) * V (n x B).  P and both
 // state buffers (2 x 12 MB at config 3) stay L2-resident (126 MB L2), so the
 // bound is the DMMA pipe. The kernel is PERSISTENT (cooperative launch, all
-// CTAs co-resident): per step a producer warp pulls 32x32 complex output tiles
-// from an atomic counter (dynamic balance: 736 tiles on 148 SMs) and streams
-// their K chunks into a 4-stage shared-memory ring with 1-D bulk async copies
-// (cp.async.bulk -> the TMA engine, SASS UBLKCP) signalled through mbarriers
-// (complete_tx); 8 consumer warps wait on the stage's "full" barrier, run the
+// CTAs co-resident): per step a producer warp walks its CTA's stream-K range of
+// (32x32 complex output tile, K chunk) iterations and streams each chunk into a
+// 3-stage shared-memory ring with TWO 2-D tensor-map TMA copies (A box 32 rows
+// x 34 complex, B box 32 rows x 36 complex: the box is 2 / 4 complex wider than
+// the chunk so the TMA writes the padded, bank-conflict-free row strides
+// directly; out-of-range rows / columns arrive zero-filled) signalled through
+// mbarriers (complete_tx). The plain GEMM (expm) uses per-row 1-D bulk copies
+// (cp.async.bulk) into the same ring. 8 consumer warps wait on the stage's "full" barrier, run the
 // m8n8k4 DMMAs in real form (common.cuh), release the stage on its "empty"
 // barrier and write finished tiles straight from registers to the other state
 // buffer. No block-wide barrier in the main loop; one grid barrier per step
@@ -23,6 +26,8 @@
 // Replaces step_soa_kernel (proj/src/kernels_variants.cpp:26-41) inside
 // evolve (proj/src/propagate.cpp:85-92), batched; the GEMM replaces
 // lb::matmul (proj/src/complex_matrix.cpp:30-56) inside expm.
+#include <cuda.h>  // CUtensorMap (driver types only; the encoder comes via cudaGetDriverEntryPoint)
+
 #include <algorithm>
 
 #include "common.cuh"
@@ -32,7 +37,7 @@ namespace lbg {
 
 namespace {
 
-constexpr int BM = 32, BK = 32, STAGES = 3;
+constexpr int BM = 32, BK = 32, STAGES = 2;
 constexpr int CWARPS = 8, THREADS = 32 * (CWARPS + 1);
 constexpr int SA = BK + 2;  // complex stride of A rows: 2 (mod 8), see header
 constexpr int A_ELEMS = BM * SA;
@@ -103,6 +108,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       : "memory");
 }
 
+// 2-D tensor-map TMA: box at coordinates {c0 (innermost, doubles), c1 (rows)}
+__device__ __forceinline__ void tma_g2s_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
 struct Ring {
   double2* data;   // STAGES x (A | B)
   uint64_t* full;  // STAGES
@@ -169,6 +183,37 @@ __device__ __forceinline__ void produce_range(const Ring& r, const Problem& p, i
       bulk_g2s(as + row * SA, p.A + (long long)(m0 + row) * p.lda + k0, unsigned(kv) * 16u, &r.full[stage]);
     for (int row = lane; row < kv; row += 32)
       bulk_g2s(bs + row * SB, p.B + (long long)(k0 + row) * p.ldb + n0, unsigned(ncols) * 16u, &r.full[stage]);
+    advance(stage, phase);
+  }
+}
+
+// Same iteration space, one elected lane, two 2-D TMA copies per chunk. The
+// boxes are SA / SB complex wide, so each smem row lands at the padded stride;
+// rows >= M and columns >= K / N are zero-filled by the TMA unit.
+template <class G>
+__device__ __forceinline__ void produce_range_tma(const Ring& r, const Problem& p, const CUtensorMap* map_a,
+                                                  const CUtensorMap* map_b, int tiles_m, long long it0,
+                                                  long long it1, int& stage, unsigned& phase, int lane) {
+  constexpr int BN = G::BN, STAGE_ELEMS = G::STAGE_ELEMS;
+  constexpr unsigned kBytes = unsigned(STAGE_ELEMS) * 16u;  // full boxes, OOB fill included
+  const int nk = (p.K + BK - 1) / BK;
+  for (long long it = it0; it < it1; ++it) {
+    const int t = int(it / nk), kc = int(it - (long long)t * nk);
+    const int m0 = (t % tiles_m) * BM, n0 = (t / tiles_m) * BN;
+    const long long tb = (long long)t * nk;
+    const int lo = int(max(it0 - tb, 0ll)), hi = int(min(it1 - 1 - tb, (long long)nk - 1));
+    mbar_wait(&r.empty[stage], phase ^ 1u);
+    if (lane == 0) {
+      double2* as = r.data + stage * STAGE_ELEMS;
+      r.hdr[4 * stage] = t;
+      r.hdr[4 * stage + 1] = kc;
+      r.hdr[4 * stage + 2] = lo;
+      r.hdr[4 * stage + 3] = hi;
+      mbar_arrive_tx(&r.full[stage], kBytes);
+      tma_g2s_2d(as, map_a, 2 * kc * BK, m0, &r.full[stage]);
+      tma_g2s_2d(as + A_ELEMS, map_b, 2 * n0, kc * BK, &r.full[stage]);
+    }
+    __syncwarp();
     advance(stage, phase);
   }
 }
@@ -386,7 +431,10 @@ __global__ void __launch_bounds__(THREADS) tiled_evolve_kernel(const double2* __
                                                                double2* v0, double2* v1,
                                                                int batch, int64_t steps,
                                                                StepCtl* ctl, double2* part,
-                                                               unsigned int* flags) {
+                                                               unsigned int* flags,
+                                                               const __grid_constant__ CUtensorMap map_p,
+                                                               const __grid_constant__ CUtensorMap map_v0,
+                                                               const __grid_constant__ CUtensorMap map_v1) {
   using G = StepGeo;
   constexpr int BN = G::BN;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -409,7 +457,7 @@ __global__ void __launch_bounds__(THREADS) tiled_evolve_kernel(const double2* __
     if (warp == CWARPS) {
       // generic-proxy stores of the previous step -> async-proxy (bulk copy) reads
       asm volatile("fence.proxy.async.global;\n" ::: "memory");
-      produce_range<G>(r, p, tiles_m, it0, it1, stage, phase, lane);
+      produce_range_tma<G>(r, p, &map_p, (s & 1) ? &map_v1 : &map_v0, tiles_m, it0, it1, stage, phase, lane);
       produce_end(r, stage, phase, lane);
     } else {
       const SplitK sk{part, flags, unsigned(s + 1)};
@@ -480,6 +528,37 @@ void convert(double* x_re, double* x_im, double* x_aos, double2* v, int n, int b
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    check_cuda(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q),
+               "cuTensorMapEncodeTiled entry point");
+    if (q != cudaDriverEntryPointSuccess || !p) throw cuda_error("cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// rows x cols complex row-major matrix viewed as FP64 [rows][2 cols]; the box
+// is box_rows x box_cplx complex (box_cplx may exceed the chunk: padded stride)
+CUtensorMap complex_map(const double2* base, size_t rows, size_t cols, unsigned box_rows, unsigned box_cplx) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {cuuint64_t(2 * cols), cuuint64_t(rows)};
+  const cuuint64_t strides[1] = {cuuint64_t(cols * sizeof(double2))};
+  const cuuint32_t box[2] = {cuuint32_t(2 * box_cplx), cuuint32_t(box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult rc = encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double2*>(base), dims,
+                                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (rc != CUDA_SUCCESS) throw cuda_error("cuTensorMapEncodeTiled failed (" + std::to_string(int(rc)) + ")");
+  return m;
+}
+
 }  // namespace
 
 int sm_count() {
@@ -536,8 +615,12 @@ void launch_tiled_evolve(const double* p_dev, size_t n, double* x_re, double* x_
   if (grid < 1) grid = 1;
   const double2* p2 = reinterpret_cast<const double2*>(p_dev);
   int64_t st = steps;
+  // A = P (n x n), B = the state V[k][b] (n x batch); boxes of BM x SA and BK x SB complex
+  CUtensorMap map_p = complex_map(p2, n, n, BM, SA);
+  CUtensorMap map_v0 = complex_map(v0, n, size_t(batch), BK, StepGeo::SB);
+  CUtensorMap map_v1 = complex_map(v1, n, size_t(batch), BK, StepGeo::SB);
   void* args[] = {(void*)&p2, (void*)&ni, (void*)&v0, (void*)&v1, (void*)&bi, (void*)&st, (void*)&ctl,
-                  (void*)&part, (void*)&flags};
+                  (void*)&part, (void*)&flags, (void*)&map_p, (void*)&map_v0, (void*)&map_v1};
   if (steps > 0) {
     check_cuda(cudaLaunchCooperativeKernel((const void*)tiled_evolve_kernel, dim3(grid), dim3(THREADS),
                                            args, StepGeo::kSmemBytes, s),
