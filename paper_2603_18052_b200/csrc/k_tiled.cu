@@ -11,8 +11,8 @@
 // x 34 complex, B box 32 rows x 36 complex: the box is 2 / 4 complex wider than
 // the chunk so the TMA writes the padded, bank-conflict-free row strides
 // directly; out-of-range rows / columns arrive zero-filled) signalled through
-// mbarriers (complete_tx). The plain GEMM (expm) uses per-row 1-D bulk copies
-// (cp.async.bulk) into the same ring. 8 consumer warps wait on the stage's "full" barrier, run the
+// mbarriers (complete_tx); the plain batched GEMM (expm) uses the same producer
+// with the batch stacked as rows of one tensor. 8 consumer warps wait on the stage's "full" barrier, run the
 // m8n8k4 DMMAs in real form (common.cuh), release the stage on its "empty"
 // barrier and write finished tiles straight from registers to the other state
 // buffer. No block-wide barrier in the main loop; one grid barrier per step
@@ -100,14 +100,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
 // 2-D tensor-map TMA: box at coordinates {c0 (innermost, doubles), c1 (rows)}
 __device__ __forceinline__ void tma_g2s_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
   asm volatile(
@@ -155,45 +147,14 @@ __device__ __forceinline__ void advance(int& stage, unsigned& phase) {
 // Producer: one warp streams iterations [it0, it1) of the flattened
 // (tile, K chunk) space into the ring (stream-K: a CTA's range may start or end
 // inside a tile; the header tells the consumers which part of the tile it is).
-template <class G>
-__device__ __forceinline__ void produce_range(const Ring& r, const Problem& p, int tiles_m, long long it0,
-                                              long long it1, int& stage, unsigned& phase, int lane) {
-  constexpr int BN = G::BN, SB = G::SB, STAGE_ELEMS = G::STAGE_ELEMS;
-  const int nk = (p.K + BK - 1) / BK;
-  for (long long it = it0; it < it1; ++it) {
-    const int t = int(it / nk), kc = int(it - (long long)t * nk);
-    const int m0 = (t % tiles_m) * BM, n0 = (t / tiles_m) * BN;
-    const int mrows = min(BM, p.M - m0), ncols = min(BN, p.N - n0);
-    const int k0 = kc * BK, kv = min(BK, p.K - k0);
-    const long long tb = (long long)t * nk;
-    const int lo = int(max(it0 - tb, 0ll)), hi = int(min(it1 - 1 - tb, (long long)nk - 1));
-    mbar_wait(&r.empty[stage], phase ^ 1u);
-    double2* as = r.data + stage * STAGE_ELEMS;
-    double2* bs = as + A_ELEMS;
-    const unsigned bytes = unsigned(mrows * kv + kv * ncols) * 16u;
-    if (lane == 0) {
-      r.hdr[4 * stage] = t;
-      r.hdr[4 * stage + 1] = kc;
-      r.hdr[4 * stage + 2] = lo;
-      r.hdr[4 * stage + 3] = hi;
-      mbar_arrive_tx(&r.full[stage], bytes);
-    }
-    __syncwarp();
-    for (int row = lane; row < mrows; row += 32)
-      bulk_g2s(as + row * SA, p.A + (long long)(m0 + row) * p.lda + k0, unsigned(kv) * 16u, &r.full[stage]);
-    for (int row = lane; row < kv; row += 32)
-      bulk_g2s(bs + row * SB, p.B + (long long)(k0 + row) * p.ldb + n0, unsigned(ncols) * 16u, &r.full[stage]);
-    advance(stage, phase);
-  }
-}
-
 // Same iteration space, one elected lane, two 2-D TMA copies per chunk. The
 // boxes are SA / SB complex wide, so each smem row lands at the padded stride;
 // rows >= M and columns >= K / N are zero-filled by the TMA unit.
 template <class G>
 __device__ __forceinline__ void produce_range_tma(const Ring& r, const Problem& p, const CUtensorMap* map_a,
                                                   const CUtensorMap* map_b, int tiles_m, long long it0,
-                                                  long long it1, int& stage, unsigned& phase, int lane) {
+                                                  long long it1, int& stage, unsigned& phase, int lane,
+                                                  int a_row0 = 0, int b_row0 = 0) {
   constexpr int BN = G::BN, STAGE_ELEMS = G::STAGE_ELEMS;
   constexpr unsigned kBytes = unsigned(STAGE_ELEMS) * 16u;  // full boxes, OOB fill included
   const int nk = (p.K + BK - 1) / BK;
@@ -210,8 +171,8 @@ __device__ __forceinline__ void produce_range_tma(const Ring& r, const Problem& 
       r.hdr[4 * stage + 2] = lo;
       r.hdr[4 * stage + 3] = hi;
       mbar_arrive_tx(&r.full[stage], kBytes);
-      tma_g2s_2d(as, map_a, 2 * kc * BK, m0, &r.full[stage]);
-      tma_g2s_2d(as + A_ELEMS, map_b, 2 * n0, kc * BK, &r.full[stage]);
+      tma_g2s_2d(as, map_a, 2 * kc * BK, a_row0 + m0, &r.full[stage]);
+      tma_g2s_2d(as + A_ELEMS, map_b, 2 * n0, b_row0 + kc * BK, &r.full[stage]);
     }
     __syncwarp();
     advance(stage, phase);
@@ -378,10 +339,16 @@ __device__ __forceinline__ void init_ring(const Ring& r) {
 }
 
 // ---- plain batched GEMM (expm): one tile per CTA -----------------------------
+// A batch of matrices with stride n*n is one tensor of n*batch rows (stride 0:
+// n rows); a box reaching past row n of matrix b reads rows of matrix b+1 —
+// A rows >= n only feed outputs that are never stored, and B rows k >= n meet
+// A columns k >= n, which the TMA zero-fills — so the product is exact.
 __global__ void __launch_bounds__(THREADS) zgemm_kernel(const double2* __restrict__ A,
                                                         const double2* __restrict__ B,
                                                         double2* __restrict__ C, int n,
-                                                        long long sa, long long sb, long long sc) {
+                                                        long long sa, long long sb, long long sc,
+                                                        const __grid_constant__ CUtensorMap map_a,
+                                                        const __grid_constant__ CUtensorMap map_b) {
   using G = Geo<32>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const Ring r = carve<G>(smem_raw);
@@ -394,7 +361,8 @@ __global__ void __launch_bounds__(THREADS) zgemm_kernel(const double2* __restric
   unsigned phase = 0;
   if (warp == CWARPS) {
     const long long nk = (n + BK - 1) / BK;
-    produce_range<G>(r, p, tiles_m, tile * nk, (tile + 1) * nk, stage, phase, lane);
+    produce_range_tma<G>(r, p, &map_a, &map_b, tiles_m, tile * nk, (tile + 1) * nk, stage, phase, lane,
+                         sa ? b * n : 0, sb ? b * n : 0);
     produce_end(r, stage, phase, lane);
   } else {
     consume<G>(r, p, tiles_m, stage, phase, warp, lane, nullptr);
@@ -639,11 +607,18 @@ void launch_zgemm(const double* a, const double* b, double* c, int n, int batch,
     return true;
   }();
   (void)init;
+  const long long nn = (long long)n * n;
+  if ((stride_a != 0 && stride_a != nn) || (stride_b != 0 && stride_b != nn))
+    throw invalid_argument("zgemm: batch strides must be 0 or n*n");
   const dim3 grid((n + BM - 1) / BM, (n + Geo<32>::BN - 1) / Geo<32>::BN, batch);
+  const CUtensorMap map_a = complex_map(reinterpret_cast<const double2*>(a), size_t(n) * (stride_a ? batch : 1),
+                                        size_t(n), BM, SA);
+  const CUtensorMap map_b = complex_map(reinterpret_cast<const double2*>(b), size_t(n) * (stride_b ? batch : 1),
+                                        size_t(n), BK, Geo<32>::SB);
   zgemm_kernel<<<grid, THREADS, Geo<32>::kSmemBytes, s>>>(reinterpret_cast<const double2*>(a),
                                                  reinterpret_cast<const double2*>(b),
                                                  reinterpret_cast<double2*>(c), n, stride_a, stride_b,
-                                                 stride_c);
+                                                 stride_c, map_a, map_b);
   LBG_CHECK_LAUNCH("zgemm_kernel");
 }
 
