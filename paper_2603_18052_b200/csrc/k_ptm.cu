@@ -77,12 +77,14 @@ __device__ __forceinline__ double real_entry(F&& lq, int q, int s) {
 }
 
 // D_R: the trajectory-independent dissipator part of L_R, from the complex
-// Kronecker-assembled D (k_model.cu build_lindbladian_kernel with H = 0).
+// Kronecker-assembled D (k_model.cu build_lindbladian_kernel with H = 0),
+// written in the padded 88 x RS shared-memory layout of the expm kernel (zero
+// padding) so each trajectory stages it with ONE bulk copy.
 __global__ void ptm_dissipator_kernel(const double2* __restrict__ dis, double* __restrict__ dr) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= N * N) return;
-  const int q = e / N, s = e - q * N;
-  dr[e] = real_entry([&](int p) { return dis[q * N + p]; }, q, s);
+  if (e >= MAT) return;
+  const int q = e / RS, s = e - q * RS;
+  dr[e] = (q < N && s < N) ? real_entry([&](int p) { return dis[q * N + p]; }, q, s) : 0.0;
 }
 
 // acc[m][0..1] = (X * Y)[m*8 + g][w*8 + 2t .. +1], X, Y padded 88 x RS
@@ -150,17 +152,38 @@ __global__ void __launch_bounds__(THREADS, 1)
   __shared__ double2 hb[D * D];
   __shared__ double colsum[88];
   __shared__ int s_sq;
+  __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int b = blockIdx.x;
+  // D_R (padded, zeros outside 81 x 81) -> S0 with one bulk async copy; S1 / S2
+  // need no clearing: every matmul stores all 88 x 88 entries it is read at
+  if (tid == 0) {
+    const unsigned sb32 = static_cast<unsigned>(__cvta_generic_to_shared(&bar));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sb32));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sb32), "r"(unsigned(MAT * 8))
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            static_cast<unsigned>(__cvta_generic_to_shared(S0))),
+        "l"(dr), "r"(unsigned(MAT * 8)), "r"(sb32)
+        : "memory");
+  }
   const double db = delta[b], sb = scale[b];
   for (int e = tid; e < D * D; e += THREADS)
     hb[e] = make_double2(h0[e].x + db * hd[e].x + sb * hs[e].x, h0[e].y + db * hd[e].y + sb * hs[e].y);
-  for (int e = tid; e < 3 * MAT; e += THREADS) sm[e] = 0.0;
-  __syncthreads();
-  // ---- K5: A_R = L_R (unscaled) into S0 ----
+  __syncthreads();  // hb ready, barrier initialised
+  {
+    const unsigned sb32 = static_cast<unsigned>(__cvta_generic_to_shared(&bar));
+    asm volatile(
+        "{\n.reg .pred p;\nWAIT_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra WAIT_%=;\n}\n" ::"r"(
+            sb32)
+        : "memory");
+  }
+  // ---- K5: A_R = D_R + coherent part (unscaled), in place in S0 ----
   for (int e = tid; e < N * N; e += THREADS) {
     const int q = e / N, s = e - q * N;
-    S0[q * RS + s] = dr[e] + real_entry([&](int p) { return kron_c(hb, q, p); }, q, s);
+    S0[q * RS + s] += real_entry([&](int p) { return kron_c(hb, q, p); }, q, s);
   }
   __syncthreads();
   // ||A dt||_1 -> squarings (per trajectory)
@@ -326,7 +349,7 @@ constexpr int64_t kChunk = 16384;
 size_t ptm_sweep_workspace(int64_t batch) {
   const size_t chunk = size_t(std::min<int64_t>(std::max<int64_t>(batch, 1), kChunk));
   return align_up(chunk * N * N * 8) + align_up(size_t(N) * N * 16) + align_up(2 * N * 8) +
-         align_up(size_t(N) * N * 8) + 256;
+         align_up(size_t(MAT) * 8) + 256;
 }
 
 bool ptm_sweep_supported(size_t d) { return d == size_t(D); }
@@ -349,7 +372,7 @@ void launch_ptm_sweep(size_t d, const double* h0, const double* hd, const double
   check_cuda(cudaMemsetAsync(ens_x, 0, N * 8, s), "memset");
   check_cuda(cudaMemsetAsync(pr, 0, d * d * 16, s), "memset");
   launch_build_lindbladian(d, pr, n_ops, ops, reinterpret_cast<double*>(dis), s);
-  ptm_dissipator_kernel<<<(N * N + 255) / 256, 256, 0, s>>>(dis, dr);
+  ptm_dissipator_kernel<<<(MAT + 255) / 256, 256, 0, s>>>(dis, dr);
   LBG_CHECK_LAUNCH("ptm_dissipator_kernel");
   rho_to_x_kernel<<<1, 96, 0, s>>>(reinterpret_cast<const double2*>(rho0), x0);
   LBG_CHECK_LAUNCH("rho_to_x_kernel");
