@@ -42,6 +42,9 @@ void launch_dfma9(const double* p_aos_host_or_null, const double* p_dev, double*
 bool chain_supported(std::size_t n);
 void launch_chain(const double* p_dev, std::size_t n, double* x_re, double* x_im, double* x_aos,
                   int64_t batch, int64_t steps, Layout layout, cudaStream_t s);
+// GRAPE chain over all segments in one launch, one trajectory (k_chain.cu)
+void launch_chain_segments(const double* props, std::size_t n, int64_t segments, int64_t sps,
+                           double* x_aos, cudaStream_t s);
 // K1b — n <= 84, P resident in shared memory, DMMA (k_smem.cu)
 bool smem_supported(std::size_t n);
 void launch_smem(const double* p_dev, std::size_t n, double* x_re, double* x_im, double* x_aos,

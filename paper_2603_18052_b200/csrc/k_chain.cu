@@ -21,6 +21,39 @@ namespace {
 
 constexpr int kWarps = 4;
 
+// `steps` steps of one warp's chain: lane `slot` writes its real-form output
+// row; v0 / v1 ping-pong in shared memory. Returns the buffer holding the state.
+template <int N>
+__device__ __forceinline__ double* chain_steps(const double (&coef)[2 * N], double* v0, double* v1, int slot,
+                                               int64_t steps) {
+#pragma unroll 1
+  for (int64_t s = 0; s < steps; ++s) {
+    // issue every broadcast load of the state first: one shared-memory latency per step
+    double2 vv[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) vv[j] = *reinterpret_cast<const double2*>(v0 + 2 * j);
+    constexpr int NA = N >= 6 ? 6 : N;
+    double acc[NA];
+#pragma unroll
+    for (int a = 0; a < NA; ++a) acc[a] = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      acc[j % NA] = fma(coef[2 * j], vv[j].x, acc[j % NA]);
+      acc[j % NA] = fma(coef[2 * j + 1], vv[j].y, acc[j % NA]);
+    }
+#pragma unroll
+    for (int w = 1; w < NA; w *= 2)
+#pragma unroll
+      for (int a = 0; a + w < NA; a += 2 * w) acc[a] += acc[a + w];
+    v1[slot] = acc[0];
+    __syncwarp();
+    double* tmp = v0;
+    v0 = v1;
+    v1 = tmp;
+  }
+  return v0;
+}
+
 template <int N, Layout L>
 __global__ void __launch_bounds__(32 * kWarps) chain_kernel(const double2* __restrict__ p,
                                                            double* __restrict__ x_re,
@@ -54,31 +87,7 @@ __global__ void __launch_bounds__(32 * kWarps) chain_kernel(const double2* __res
   // lanes >= R compute too (zero coefficients) and write a dummy slot, so the
   // step loop has no divergent branch
   const int slot = active ? lane : R;
-#pragma unroll 1
-  for (int64_t s = 0; s < steps; ++s) {
-    // issue every broadcast load of the state first: one shared-memory latency per step
-    double2 vv[N];
-#pragma unroll
-    for (int j = 0; j < N; ++j) vv[j] = *reinterpret_cast<const double2*>(v0 + 2 * j);
-    constexpr int NA = N >= 6 ? 6 : N;
-    double acc[NA];
-#pragma unroll
-    for (int a = 0; a < NA; ++a) acc[a] = 0.0;
-#pragma unroll
-    for (int j = 0; j < N; ++j) {
-      acc[j % NA] = fma(coef[2 * j], vv[j].x, acc[j % NA]);
-      acc[j % NA] = fma(coef[2 * j + 1], vv[j].y, acc[j % NA]);
-    }
-#pragma unroll
-    for (int w = 1; w < NA; w *= 2)
-#pragma unroll
-      for (int a = 0; a + w < NA; a += 2 * w) acc[a] += acc[a + w];
-    v1[slot] = acc[0];
-    __syncwarp();
-    double* tmp = v0;
-    v0 = v1;
-    v1 = tmp;
-  }
+  v0 = chain_steps<N>(coef, v0, v1, slot, steps);
   if (active) {
     if (L == Layout::soa) {
       if (a)
@@ -103,7 +112,65 @@ void launch_n(const double* p, double* x_re, double* x_im, double* x_aos, int64_
   LBG_CHECK_LAUNCH("chain_kernel");
 }
 
+// GRAPE chain (propagate.cpp:144-156) in ONE launch: segment j applies
+// props[j] for sps steps. The next segment's real-form row is loaded into
+// registers while the current segment runs, so a segment switch costs no
+// global-memory latency and no kernel launch.
+template <int N>
+__global__ void __launch_bounds__(32 * kWarps) chain_segments_kernel(const double2* __restrict__ props,
+                                                                     int64_t segments, int64_t sps,
+                                                                     double* __restrict__ x_aos) {
+  constexpr int R = 2 * N;
+  // per-warp buffers as in chain_kernel (a lane-dependent address keeps the
+  // state loads in the vector pipe, where ptxas issues them all up front)
+  __shared__ __align__(16) double vbuf[kWarps][2][R + 2];
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  const bool active = lane < R;
+  const int i = lane >> 1, a = lane & 1;
+  double coef[R], next[R];
+  auto load_row = [&](int64_t j, double (&c)[R]) {
+    const double2* p = props + j * N * N;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      const double2 z = active ? __ldg(p + i * N + k) : make_double2(0.0, 0.0);
+      c[2 * k] = a ? z.y : z.x;
+      c[2 * k + 1] = a ? z.x : -z.y;
+    }
+  };
+  load_row(0, coef);
+  double* v0 = vbuf[wi][0];
+  if (active) v0[lane] = x_aos[lane];
+  __syncwarp();
+  const int slot = active ? lane : R;
+#pragma unroll 1
+  for (int64_t seg = 0; seg < segments; ++seg) {
+    if (seg + 1 < segments) load_row(seg + 1, next);
+    v0 = chain_steps<N>(coef, v0, v0 == vbuf[wi][0] ? vbuf[wi][1] : vbuf[wi][0], slot, sps);
+#pragma unroll
+    for (int k = 0; k < R; ++k) coef[k] = next[k];
+  }
+  if (active) x_aos[lane] = v0[lane];
+}
+
 }  // namespace
+
+void launch_chain_segments(const double* props, std::size_t n, int64_t segments, int64_t sps, double* x_aos,
+                           cudaStream_t s) {
+  if (segments <= 0 || sps <= 0) return;
+  const double2* p2 = reinterpret_cast<const double2*>(props);
+  switch (n) {
+#define LBG_CASE(N)                                                                    \
+  case N:                                                                              \
+    chain_segments_kernel<N><<<1, 32, 0, s>>>(p2, segments, sps, x_aos); \
+    break;
+    LBG_CASE(1) LBG_CASE(2) LBG_CASE(3) LBG_CASE(4) LBG_CASE(5) LBG_CASE(6) LBG_CASE(7)
+    LBG_CASE(8) LBG_CASE(9) LBG_CASE(10) LBG_CASE(11) LBG_CASE(12) LBG_CASE(13) LBG_CASE(14)
+    LBG_CASE(15) LBG_CASE(16)
+#undef LBG_CASE
+    default: throw invalid_argument("segmented chain kernel supports n <= 16");
+  }
+  LBG_CHECK_LAUNCH("chain_segments_kernel");
+}
 
 bool chain_supported(std::size_t n) { return n >= 1 && n <= 16; }
 

@@ -145,6 +145,110 @@ __global__ void __launch_bounds__(96) sweep_step_kernel(const double2* __restric
   }
 }
 
+// GRAPE segment propagators for n = d^2 <= 16 in ONE launch: one CTA per
+// segment, thread e owns element e of every n x n matrix, everything in shared
+// memory. Same construction as the batched path (sweep_assemble_kernel +
+// Taylor-16 / Paterson-Stockmeyer), with the squaring count chosen per segment
+// on the device (no host round trip for the norm).
+constexpr int kSmallN = 16;
+__device__ __forceinline__ double2 small_mm(const double2* __restrict__ X, const double2* __restrict__ Y, int n,
+                                            int r, int c) {
+  double re = 0.0, im = 0.0;
+  for (int k = 0; k < n; ++k) {
+    const double2 a = X[r * n + k], b = Y[k * n + c];
+    re = fma(a.x, b.x, re);
+    re = fma(-a.y, b.y, re);
+    im = fma(a.x, b.y, im);
+    im = fma(a.y, b.x, im);
+  }
+  return make_double2(re, im);
+}
+
+__global__ void __launch_bounds__(kSmallN * kSmallN) grape_small_build_kernel(
+    const double2* __restrict__ dis, const double2* __restrict__ h0, const double2* __restrict__ hc,
+    const double* __restrict__ amps, int d, double dt, double theta, const double* __restrict__ cf,
+    double2* __restrict__ props) {
+  constexpr int NN = kSmallN * kSmallN;
+  __shared__ double2 A[NN], A2[NN], A3[NN], A4[NN], T[NN], U[NN];
+  __shared__ double colsum[kSmallN];
+  __shared__ int s_sq;
+  const int n = d * d, e = threadIdx.x, seg = blockIdx.x;
+  const bool own = e < n * n;
+  const int r = own ? e / n : 0, c = own ? e - r * n : 0;
+  const double aj = amps[seg];
+  if (own) {  // dt * (D + coherent(h0 + a_j hc))
+    const int i = r / d, k = r - i * d, j = c / d, l = c - j * d;
+    double2 acc = dis[e];
+    if (k == l) {
+      const double2 hij = make_double2(h0[i * d + j].x + aj * hc[i * d + j].x, h0[i * d + j].y + aj * hc[i * d + j].y);
+      acc.x += hij.y;
+      acc.y -= hij.x;
+    }
+    if (i == j) {
+      const double2 hlk = make_double2(h0[l * d + k].x + aj * hc[l * d + k].x, h0[l * d + k].y + aj * hc[l * d + k].y);
+      acc.x -= hlk.y;
+      acc.y += hlk.x;
+    }
+    A[e] = make_double2(acc.x * dt, acc.y * dt);
+  }
+  __syncthreads();
+  if (e < n) {
+    double cs = 0.0;
+    for (int q = 0; q < n; ++q) cs += hypot(A[q * n + e].x, A[q * n + e].y);
+    colsum[e] = cs;
+  }
+  __syncthreads();
+  if (e == 0) {
+    double nrm = 0.0;
+    for (int q = 0; q < n; ++q) nrm = fmax(nrm, colsum[q]);
+    int sq = nrm > theta ? int(ceil(log2(nrm / theta))) : 0;
+    s_sq = sq < 0 ? 0 : sq;
+  }
+  __syncthreads();
+  const int sq = s_sq;
+  const double sc = ldexp(1.0, -sq);
+  if (own) A[e] = make_double2(A[e].x * sc, A[e].y * sc);
+  __syncthreads();
+  auto combo = [&](double2 x, double c0, double c1, double c2, double c3) {
+    double2 v = x;
+    if (r == c) v.x += c0;
+    v.x += c1 * A[e].x; v.y += c1 * A[e].y;
+    v.x += c2 * A2[e].x; v.y += c2 * A2[e].y;
+    v.x += c3 * A3[e].x; v.y += c3 * A3[e].y;
+    return v;
+  };
+  if (own) A2[e] = small_mm(A, A, n, r, c);
+  __syncthreads();
+  if (own) {
+    A3[e] = small_mm(A2, A, n, r, c);
+    A4[e] = small_mm(A2, A2, n, r, c);
+  }
+  __syncthreads();
+  if (own) {  // T = c12 I + c13 A + c14 A2 + c15 A3 + c16 A4
+    double2 v = combo(make_double2(0.0, 0.0), cf[12], cf[13], cf[14], cf[15]);
+    v.x += cf[16] * A4[e].x;
+    v.y += cf[16] * A4[e].y;
+    T[e] = v;
+  }
+  __syncthreads();
+  for (int j = 2; j >= 0; --j) {  // T = A4 T + B_j
+    double2 v = make_double2(0.0, 0.0);
+    if (own) v = combo(small_mm(A4, T, n, r, c), cf[4 * j], cf[4 * j + 1], cf[4 * j + 2], cf[4 * j + 3]);
+    __syncthreads();
+    if (own) T[e] = v;
+    __syncthreads();
+  }
+  for (int q = 0; q < sq; ++q) {
+    double2 v = make_double2(0.0, 0.0);
+    if (own) v = small_mm(T, T, n, r, c);
+    __syncthreads();
+    if (own) T[e] = v;
+    __syncthreads();
+  }
+  if (own) props[(long long)seg * n * n + e] = T[e];
+  (void)U;
+}
+
 double inv_fact(int k) {
   double f = 1.0;
   for (int i = 2; i <= k; ++i) f *= i;
@@ -285,6 +389,23 @@ void launch_grape(size_t d, const double* h0, const double* hc, const double* ze
   char* w = static_cast<char*>(work);
   double2* props = reinterpret_cast<double2*>(w + sweep_workspace(d, segments));
   void* ework = w + sweep_workspace(d, segments) + align_up(size_t(segments) * nn * 16) + align_up(n * 16);
+  if (n <= size_t(kSmallN)) {
+    // small systems (d <= 4): two launches in total — every propagator in one
+    // build kernel, then the whole chain in one kernel
+    double2* dis = reinterpret_cast<double2*>(w);
+    double* cf = reinterpret_cast<double*>(w + align_up(nn * 16));
+    double hcf[17];
+    for (int k = 0; k <= 16; ++k) hcf[k] = inv_fact(k);
+    check_cuda(cudaMemcpyAsync(cf, hcf, sizeof hcf, cudaMemcpyHostToDevice, s), "H2D coefficients");
+    launch_build_lindbladian(d, zero_h, n_ops, ops, reinterpret_cast<double*>(dis), s);
+    grape_small_build_kernel<<<unsigned(segments), kSmallN * kSmallN, 0, s>>>(
+        dis, reinterpret_cast<const double2*>(h0), reinterpret_cast<const double2*>(hc), amps, int(d), dt, 0.79,
+        cf, props);
+    LBG_CHECK_LAUNCH("grape_small_build_kernel");
+    if (ev_build_end) check_cuda(cudaEventRecord(ev_build_end, s), "event");
+    launch_chain_segments(reinterpret_cast<const double*>(props), n, segments, steps_per_segment, x, s);
+    return;
+  }
   propagators_complex(d, h0, hc, zero_h, n_ops, ops, amps, zeros, dt, segments, w, s,
                       [&](const double2* P, int64_t c0, int cb) {
                         check_cuda(cudaMemcpyAsync(props + c0 * nn, P, size_t(cb) * nn * 16,
