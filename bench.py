@@ -106,6 +106,15 @@ def roofline_place(d: int, batch: int, shared_p: bool, peak_tflops: float, tile:
             "bound": "compute" if (ridge is None or ai >= ridge) else "memory"}
 
 
+def reference_model(lbg, mprof, d: int) -> dict:
+    """The reference's own roofline (roofline.cpp:62-99: characterize -> place
+    -> classify, per single matvec) evaluated on the measured B200 profile."""
+    k = lbg.place(lbg.characterize(d), mprof)
+    c = lbg.classify(k, mprof)
+    return {"flops": k.flops, "bytes": k.bytes, "ai": k.ai, "placement": lbg.LEVELS[k.placement],
+            "ridge": lbg.ridge_point(mprof, k.placement), **c}
+
+
 class Clocks:
     """nvidia-smi samples during the timed region (the recipe's clocks line)."""
 
@@ -312,6 +321,13 @@ def run_ours(args):
     K, W = args.steps, args.warmup
     dmma_peak, dfma_peak = lbg.fp64_peak()
     peak = max(dmma_peak, dfma_peak)
+    # the B200 ladder measured live (lbg_measure_machine_profile): SMEM, L2, HBM,
+    # host-over-PCIe bandwidths feed the placement model below
+    mprof = lbg.measure_machine_profile()
+    bw = list(mprof.bandwidth_gbs)
+    B200_PROFILE["bw_gbs"] = [None, bw[0], bw[1], bw[2]]
+    B200_PROFILE["capacity_bytes"] = [None, int(mprof.capacity_bytes[0]), int(mprof.capacity_bytes[1]),
+                                      int(mprof.capacity_bytes[2])]
     traffic = load_traffic()
 
     # ---- device-resident timed region -----------------------------------
@@ -383,6 +399,10 @@ def run_ours(args):
                      "flops_per_launch": flops_per_traj_step(d) * B * S, "launch_ms": kernel_ms},
         "e2e": e2e,
         "placement": roofline_place(d, B, cfg != 4, peak),
+        "machine_profile": dict(mprof.as_dict(), levels=["smem/SM", "l2", "hbm", "host(pcie)"],
+                                source="lbg_measure_machine_profile (measured now); file format of "
+                                       "lb::write_profile"),
+        "reference_roofline": reference_model(lbg, mprof, d),
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }

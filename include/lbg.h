@@ -265,6 +265,50 @@ int lbg_write_bench_csv(const lbg_bench_config* cfgs, const lbg_bench_result* re
 int lbg_write_bench_json(const lbg_bench_config* cfgs, const lbg_bench_result* res, size_t count,
                          const char* machine, char* buf, size_t cap, size_t* len);
 
+/* ------------------------------------------------------------------------
+ * Roofline model on the GPU: replaces lb::characterize / place / classify /
+ * ridge_point, lb::MachineProfile and its text format (roofline.hpp:11-80,
+ * roofline.cpp:44-182). The B200 ladder fills the reference's 4-level shape:
+ *   level 0 "L1"   shared memory per SM (capacity: bytes per SM),
+ *   level 1 "L2"   L2 cache,
+ *   level 2 "L3"   HBM,
+ *   level 3 "DRAM" host memory over PCIe (pinned H2D),
+ * peak_gflops = FP64 (DMMA) peak. lbg_measure_machine_profile measures every
+ * number on the current device; lbg_write/read_machine_profile use the
+ * reference's "key = value" file (peak_gflops, bw_l1..bw_dram GB/s,
+ * cap_l1..cap_l3 bytes), so lb::read_profile loads a B200 profile and the
+ * reference's own place/classify run against it. Characterize / place /
+ * classify follow the reference exactly (8 d^4 flops, 16 (d^4 + 2 d^2) bytes,
+ * smallest level whose capacity holds the working set, memory bound iff
+ * ai < peak / bw). Invalid profiles -> LBG_EINVAL, malformed text ->
+ * LBG_ERUNTIME; lbg_roofline_last_error() has the message.
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  char name[64];
+  double peak_gflops;
+  double bandwidth_gbs[4];
+  uint64_t capacity_bytes[3];
+} lbg_machine_profile;
+typedef struct {
+  size_t dim;
+  uint64_t flops, bytes;
+  double ai;
+  uint64_t working_set_bytes;
+  int placement; /* 0..3 = L1, L2, L3, DRAM; -1 = unset */
+} lbg_kernel_character;
+#define LBG_MEMORY_BOUND 0
+#define LBG_COMPUTE_BOUND 1
+const char* lbg_roofline_last_error(void);
+int lbg_measure_machine_profile(lbg_machine_profile* out);
+int lbg_validate_profile(const lbg_machine_profile* m);
+int lbg_characterize(size_t d, lbg_kernel_character* out);
+int lbg_place(lbg_kernel_character* k, const lbg_machine_profile* m);
+int lbg_ridge_point(const lbg_machine_profile* m, int level, double* out);
+int lbg_classify(const lbg_kernel_character* k, const lbg_machine_profile* m, int* bound,
+                 double* attainable_gflops);
+int lbg_write_machine_profile(const lbg_machine_profile* m, char* buf, size_t cap, size_t* len);
+int lbg_read_machine_profile(const char* text, const char* name, lbg_machine_profile* out);
+
 /* FP64 roofline denominators measured live on the current device (TF/s):
  * register-only DMMA (m8n8k4 f64) and DFMA loops over every SM. */
 int lbg_fp64_peak(double* dmma_tflops, double* dfma_tflops);

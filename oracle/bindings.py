@@ -322,3 +322,36 @@ class Reference:
                                    profile.encode(), machine.encode(), buf, ln.value + 1, C.byref(ln)),
                  "write_bench")
         return buf.value.decode()
+
+    # ---- roofline (roofline.cpp) ----
+    def read_profile(self, text, name="m"):
+        L = self.lib
+        L.ref_read_profile.argtypes = [C.c_char_p, C.c_char_p, _dp, _dp, C.POINTER(C.c_uint64)]
+        peak = C.c_double()
+        bw = np.zeros(4)
+        cap = (C.c_uint64 * 3)()
+        self._rc(L.ref_read_profile(text.encode(), name.encode(), C.byref(peak), _ptr(bw), cap), "read_profile")
+        return dict(peak_gflops=peak.value, bandwidth_gbs=list(bw), capacity_bytes=list(cap))
+
+    def write_profile(self, name, peak, bw, cap):
+        L = self.lib
+        L.ref_write_profile.argtypes = [C.c_char_p, C.c_double, _dp, C.POINTER(C.c_uint64), C.c_char_p,
+                                        C.c_size_t, C.POINTER(C.c_size_t)]
+        bw = np.ascontiguousarray(bw, np.float64)
+        capa = (C.c_uint64 * 3)(*cap)
+        ln = C.c_size_t()
+        self._rc(L.ref_write_profile(name.encode(), peak, _ptr(bw), capa, None, 0, C.byref(ln)), "write_profile")
+        buf = C.create_string_buffer(ln.value + 1)
+        self._rc(L.ref_write_profile(name.encode(), peak, _ptr(bw), capa, buf, ln.value + 1, C.byref(ln)),
+                 "write_profile")
+        return buf.value.decode()
+
+    def roofline(self, d, peak, bw, cap):
+        """characterize -> place -> classify: dict(flops, bytes, ai, placement, bound, attainable_gflops)"""
+        L = self.lib
+        L.ref_roofline.argtypes = [C.c_size_t, C.c_double, _dp, C.POINTER(C.c_uint64), _dp]
+        out = np.zeros(6)
+        bw = np.ascontiguousarray(bw, np.float64)
+        self._rc(L.ref_roofline(d, peak, _ptr(bw), (C.c_uint64 * 3)(*cap), _ptr(out)), "roofline")
+        return dict(flops=int(out[0]), bytes=int(out[1]), ai=out[2], placement=int(out[3]), bound=int(out[4]),
+                    attainable_gflops=out[5])

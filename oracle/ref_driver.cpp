@@ -30,6 +30,7 @@
 #include "lb/lindblad.hpp"
 #include "lb/propagate.hpp"
 #include "lb/random.hpp"
+#include "lb/roofline.hpp"
 #include "lb/model_io.hpp"
 #include "lb/random.hpp"
 #include <sstream>
@@ -398,6 +399,52 @@ int ref_write_bench(int json, std::size_t count, const std::size_t* dims, const 
     const std::string s = os.str();
     *len = s.size();
     if (buf && cap > s.size()) std::memcpy(buf, s.c_str(), s.size() + 1);
+  });
+}
+
+// ---- roofline (roofline.cpp): profiles as peak + bw[4] + cap[3] arrays ----
+static lb::MachineProfile prof_from(const char* name, double peak, const double* bw, const std::uint64_t* cap) {
+  lb::MachineProfile m;
+  m.name = name ? name : "";
+  m.peak_gflops = peak;
+  for (int i = 0; i < 4; ++i) m.bandwidth_gbs[i] = bw[i];
+  for (int i = 0; i < 3; ++i) m.capacity_bytes[i] = cap[i];
+  return m;
+}
+
+int ref_read_profile(const char* text, const char* name, double* peak, double* bw, std::uint64_t* cap) {
+  return guarded([&] {
+    std::istringstream is(text);
+    const lb::MachineProfile m = lb::read_profile(is, name);
+    *peak = m.peak_gflops;
+    for (int i = 0; i < 4; ++i) bw[i] = m.bandwidth_gbs[i];
+    for (int i = 0; i < 3; ++i) cap[i] = m.capacity_bytes[i];
+  });
+}
+
+int ref_write_profile(const char* name, double peak, const double* bw, const std::uint64_t* cap, char* buf,
+                      std::size_t capb, std::size_t* len) {
+  return guarded([&] {
+    std::ostringstream os;
+    lb::write_profile(os, prof_from(name, peak, bw, cap));
+    const std::string s = os.str();
+    *len = s.size();
+    if (buf && capb > s.size()) std::memcpy(buf, s.c_str(), s.size() + 1);
+  });
+}
+
+// characterize -> place -> classify; out: flops, bytes, ai, placement, bound, attainable
+int ref_roofline(std::size_t d, double peak, const double* bw, const std::uint64_t* cap, double* out) {
+  return guarded([&] {
+    const lb::MachineProfile m = prof_from("m", peak, bw, cap);
+    const lb::KernelCharacter k = lb::place(lb::characterize(d), m);
+    const lb::Classification c = lb::classify(k, m);
+    out[0] = double(k.flops);
+    out[1] = double(k.bytes);
+    out[2] = k.ai;
+    out[3] = double(static_cast<int>(*k.placement));
+    out[4] = c.bound == lb::Bound::memory_bound ? 0.0 : 1.0;
+    out[5] = c.attainable_gflops;
   });
 }
 

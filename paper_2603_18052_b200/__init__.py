@@ -502,3 +502,97 @@ def write_bench_csv(cfgs, results, machine: str) -> str:
 def write_bench_json(cfgs, results, machine: str) -> str:
     """lb::write_json (bench.cpp:223-246) + GPU keys."""
     return _write_bench("lbg_write_bench_json", cfgs, results, machine)
+
+
+# ------------------------------------------------------------- roofline ---
+class MachineProfile(C.Structure):
+    """lbg_machine_profile — lb::MachineProfile (roofline.hpp:27-36) on the B200
+    ladder: L1 = shared memory per SM, L2 = L2, L3 = HBM, DRAM = host over PCIe."""
+    _fields_ = [("name", C.c_char * 64), ("peak_gflops", C.c_double), ("bandwidth_gbs", C.c_double * 4),
+                ("capacity_bytes", C.c_uint64 * 3)]
+
+    def as_dict(self):
+        return dict(name=self.name.decode(), peak_gflops=self.peak_gflops, bandwidth_gbs=list(self.bandwidth_gbs),
+                    capacity_bytes=list(self.capacity_bytes))
+
+
+class KernelCharacter(C.Structure):
+    """lbg_kernel_character — lb::KernelCharacter (roofline.hpp:16-24)."""
+    _fields_ = [("dim", C.c_size_t), ("flops", C.c_uint64), ("bytes", C.c_uint64), ("ai", C.c_double),
+                ("working_set_bytes", C.c_uint64), ("placement", C.c_int)]
+
+
+LEVELS = ("L1", "L2", "L3", "DRAM")
+
+
+def _roof(rc: int, what: str) -> None:
+    if rc == 0:
+        return
+    L = lib()
+    L.lbg_roofline_last_error.restype = C.c_char_p
+    msg = f"{what}: {L.lbg_roofline_last_error().decode()}"
+    raise ValueError(msg) if rc == 1 else RuntimeError(msg)
+
+
+def machine_profile(name: str, peak_gflops: float, bandwidth_gbs, capacity_bytes) -> MachineProfile:
+    return MachineProfile(name.encode()[:63], peak_gflops, (C.c_double * 4)(*bandwidth_gbs),
+                          (C.c_uint64 * 3)(*capacity_bytes))
+
+
+def measure_machine_profile() -> MachineProfile:
+    """Every figure of the B200 ladder measured on the current device."""
+    L = lib()
+    L.lbg_measure_machine_profile.argtypes = [C.POINTER(MachineProfile)]
+    m = MachineProfile()
+    _check(L.lbg_measure_machine_profile(C.byref(m)), "measure_machine_profile")
+    return m
+
+
+def characterize(d: int) -> KernelCharacter:
+    L = lib()
+    L.lbg_characterize.argtypes = [_sz, C.POINTER(KernelCharacter)]
+    k = KernelCharacter()
+    _roof(L.lbg_characterize(d, C.byref(k)), "characterize")
+    return k
+
+
+def place(k: KernelCharacter, m: MachineProfile) -> KernelCharacter:
+    L = lib()
+    L.lbg_place.argtypes = [C.POINTER(KernelCharacter), C.POINTER(MachineProfile)]
+    out = KernelCharacter.from_buffer_copy(k)
+    _roof(L.lbg_place(C.byref(out), C.byref(m)), "place")
+    return out
+
+
+def ridge_point(m: MachineProfile, level: int) -> float:
+    L = lib()
+    L.lbg_ridge_point.argtypes = [C.POINTER(MachineProfile), C.c_int, _dp]
+    r = C.c_double()
+    _roof(L.lbg_ridge_point(C.byref(m), level, C.byref(r)), "ridge_point")
+    return r.value
+
+
+def classify(k: KernelCharacter, m: MachineProfile) -> dict:
+    L = lib()
+    L.lbg_classify.argtypes = [C.POINTER(KernelCharacter), C.POINTER(MachineProfile), C.POINTER(C.c_int), _dp]
+    b, a = C.c_int(), C.c_double()
+    _roof(L.lbg_classify(C.byref(k), C.byref(m), C.byref(b), C.byref(a)), "classify")
+    return dict(bound="memory_bound" if b.value == 0 else "compute_bound", attainable_gflops=a.value)
+
+
+def write_machine_profile(m: MachineProfile) -> str:
+    L = lib()
+    L.lbg_write_machine_profile.argtypes = [C.POINTER(MachineProfile), C.c_char_p, _sz, C.POINTER(_sz)]
+    ln = _sz()
+    _roof(L.lbg_write_machine_profile(C.byref(m), None, 0, C.byref(ln)), "write_profile")
+    buf = C.create_string_buffer(ln.value + 1)
+    _roof(L.lbg_write_machine_profile(C.byref(m), buf, ln.value + 1, C.byref(ln)), "write_profile")
+    return buf.value.decode()
+
+
+def read_machine_profile(text: str, name: str = "") -> MachineProfile:
+    L = lib()
+    L.lbg_read_machine_profile.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(MachineProfile)]
+    m = MachineProfile()
+    _roof(L.lbg_read_machine_profile(text.encode(), name.encode(), C.byref(m)), "read_profile")
+    return m
