@@ -346,7 +346,8 @@ void host_evolve_impl(const double* p, size_t d, const double* rho0, int64_t bat
   if (batch == 0) return;
   const size_t n = d * d;
   const int64_t min_chunk = 32768;
-  const int nchunks = (single || batch < 2 * min_chunk) ? 1 : int(std::min<int64_t>(8, batch / min_chunk));
+  constexpr int64_t max_chunks = 16;  // measured at c1: 4 -> 21.2, 8 -> 20.6, 16 -> 20.2, 32 -> 21.1 ms per call
+  const int nchunks = (single || batch < 2 * min_chunk) ? 1 : int(std::min<int64_t>(max_chunks, batch / min_chunk));
   const int64_t chunk = (batch + nchunks - 1) / nchunks;
   EvolvePool& pool = evolve_pool();
   std::lock_guard<std::mutex> lk(pool.mu);
