@@ -539,6 +539,10 @@ def extra_configs(torch, lbg, R, peak):
         except Exception as e:  # noqa: BLE001
             out[f"c{cfg}_density"] = {"error": str(e)}
     out["grape"] = grape_table(lbg)
+    try:
+        out["propagator_build"] = expm_table(torch, lbg, R)
+    except Exception as e:  # noqa: BLE001
+        out["propagator_build"] = {"error": str(e)}
     return out
 
 
@@ -586,6 +590,60 @@ def density_entry(torch, lbg, R, cfg, peak):
                          "frac": executed / peak},
             "note": "real coordinates of the Hermitian rho (2 d^4 flops per traj-step); the headline "
                     "keeps the reference's complex 8 d^4 arithmetic"}
+
+
+def expm_table(torch, lbg, R):
+    """the propagator build (K5 assembly + K4 expm) on device
+    buffers, CUDA events, vs the reference's lb::build_lindbladian + lb::expm
+    (Pade-13) on one host core; and batched state validation (K6) over the c1
+    batch vs lb::check_state on a host sample."""
+    rows = {}
+    try:
+        from oracle.bindings import Reference
+        ref = Reference()
+    except Exception as e:  # noqa: BLE001
+        ref = None
+        rows["reference"] = f"unavailable: {e}"
+    T, dev = torch, R.dev
+    for cfg, d in ((1, 3), (2, 9), (3, 27)):
+        h, ops = lbg.config_model(cfg)
+        n = d * d
+        hd = T.from_numpy(np.ascontiguousarray(h)).to(dev)
+        od = T.from_numpy(np.ascontiguousarray(ops)).to(dev)
+        Ld = T.empty((n, n), dtype=T.complex128, device=dev)
+        Pd = T.empty((n, n), dtype=T.complex128, device=dev)
+        wk = T.empty(lbg.lib().lbg_expm_workspace(n), dtype=T.uint8, device=dev)
+        L = lbg.lib()
+
+        def build():
+            lbg._check(L.lbg_build_lindbladian_dev(d, lbg._tp(hd), ops.shape[0], lbg._tp(od), lbg._tp(Ld),
+                                                   lbg._sp(R.stream)), "build")
+            lbg._check(L.lbg_expm_dev(lbg._tp(Ld), n, 0.1, lbg._tp(Pd), lbg._tp(wk), lbg._sp(R.stream)), "expm")
+        total, per, launches = R.time_passes(build, 5, 2)
+        row = {"gpu_ms": total / len(per), "gpu_launches": launches // len(per)}
+        if ref is not None:
+            t0 = time.perf_counter()
+            ref.expm(ref.build_lindbladian(h, ops), 0.1)
+            row["ref_ms"] = (time.perf_counter() - t0) * 1e3
+            row["speedup"] = row["ref_ms"] / row["gpu_ms"]
+        rows[f"d{d}"] = row
+    # K6: check_state over the whole c1 batch
+    d, B, _ = CONFIGS[1]
+    rho = lbg.ginibre_batch(1, 0, B, d)
+    xd = T.from_numpy(rho).to(dev)
+    o3 = T.empty(3, dtype=T.float64, device=dev)
+    total, per, _ = R.time_passes(lambda: lbg.check_state_batched_dev(xd, d, o3, stream=R.stream), 5, 2)
+    val = {"states": B, "gpu_ms": total / len(per), "states_per_s": B / (total / len(per) * 1e-3)}
+    if ref is not None:
+        sample = 65536
+        t0 = time.perf_counter()
+        for b in range(sample):
+            ref.check_state(rho[b])
+        dt = time.perf_counter() - t0
+        val["ref_states_per_s_sample"] = sample / dt
+        val["ref_note"] = f"lb::check_state on {sample} states through ctypes (one call per state)"
+    rows["check_state"] = val
+    return rows
 
 
 def grape_table(lbg):

@@ -261,6 +261,13 @@ class Reference:
                                    _ptr(ops), _ptr(rho0), _ptr(out), C.byref(b), C.byref(c)), "grape_chain")
         return out, b.value, c.value
 
+    def check_state(self, rho, tol=1e-8):
+        """lb::check_state (validate.cpp:10-30). Returns (passed, trace_err, herm_err, min_diag)."""
+        rho = np.ascontiguousarray(rho, np.complex128)
+        te, he, md = C.c_double(), C.c_double(), C.c_double()
+        rc = self.lib.ref_check_state(_ptr(rho), rho.shape[0], tol, C.byref(te), C.byref(he), C.byref(md))
+        return rc == 0, te.value, he.value, md.value
+
     def sweep_batch(self, deltas, scales, steps=500, threads=1):
         """Config 4 through the reference. Returns (pops (B,9), ens_sum (9,9), seconds)."""
         deltas = np.ascontiguousarray(deltas, np.float64)

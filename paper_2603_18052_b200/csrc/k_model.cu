@@ -6,6 +6,7 @@
 
 #include "common.cuh"
 #include "internal.hpp"
+#include "small_expm.cuh"
 
 namespace lbg {
 
@@ -151,6 +152,17 @@ __global__ void check_state_init(unsigned long long* keys) {
 }
 
 // one matvec out[i] = sum_j P[i][j] v[j] (the raw-pointer shim), ascending j
+// exp(scale * a) for n <= 16 in one CTA (small_expm.cuh)
+__global__ void __launch_bounds__(kSmallNN) small_expm_kernel(const double2* __restrict__ a, int n, double scale,
+                                                              int sq, SmallCoef co, double2* __restrict__ out) {
+  __shared__ double2 A[kSmallNN], A2[kSmallNN], A3[kSmallNN], A4[kSmallNN], T[kSmallNN];
+  const int e = threadIdx.x;
+  if (e < n * n) A[e] = make_double2(a[e].x * scale, a[e].y * scale);
+  __syncthreads();
+  small_taylor(A, A2, A3, A4, T, n, co.c, sq);
+  if (e < n * n) out[e] = T[e];
+}
+
 // SoA planes <-> AoS (interleaved) for the AoS-only latency kernels
 __global__ void planes_to_aos_kernel(const double* __restrict__ re, const double* __restrict__ im, long long count,
                                      double2* __restrict__ out) {
@@ -232,6 +244,13 @@ void expm_dev(const double* a, size_t n, double dt, double* out, double* work, c
     if (sq > 64) throw runtime_error("expm: norm of a*dt requires more than 64 squarings");
   }
   const double scale = dt * std::ldexp(1.0, -sq);
+  if (n <= size_t(kSmallN)) {  // one launch instead of eleven
+    SmallCoef co;
+    for (int k = 0; k <= 16; ++k) co.c[k] = inv_fact(k);
+    small_expm_kernel<<<1, kSmallNN, 0, s>>>(reinterpret_cast<const double2*>(a), int(n), scale, sq, co, P);
+    LBG_CHECK_LAUNCH("small_expm_kernel");
+    return;
+  }
   scale_kernel<<<blocks_for(nn, 256), 256, 0, s>>>(A1, reinterpret_cast<const double2*>(a), scale, nn);
   LBG_CHECK_LAUNCH("scale_kernel");
   const int ni = int(n);

@@ -18,6 +18,7 @@
 
 #include "common.cuh"
 #include "internal.hpp"
+#include "small_expm.cuh"
 
 namespace lbg {
 
@@ -150,26 +151,12 @@ __global__ void __launch_bounds__(96) sweep_step_kernel(const double2* __restric
 // memory. Same construction as the batched path (sweep_assemble_kernel +
 // Taylor-16 / Paterson-Stockmeyer), with the squaring count chosen per segment
 // on the device (no host round trip for the norm).
-constexpr int kSmallN = 16;
-__device__ __forceinline__ double2 small_mm(const double2* __restrict__ X, const double2* __restrict__ Y, int n,
-                                            int r, int c) {
-  double re = 0.0, im = 0.0;
-  for (int k = 0; k < n; ++k) {
-    const double2 a = X[r * n + k], b = Y[k * n + c];
-    re = fma(a.x, b.x, re);
-    re = fma(-a.y, b.y, re);
-    im = fma(a.x, b.y, im);
-    im = fma(a.y, b.x, im);
-  }
-  return make_double2(re, im);
-}
-
 __global__ void __launch_bounds__(kSmallN * kSmallN) grape_small_build_kernel(
     const double2* __restrict__ dis, const double2* __restrict__ h0, const double2* __restrict__ hc,
     const double* __restrict__ amps, int d, double dt, double theta, const double* __restrict__ cf,
     double2* __restrict__ props) {
   constexpr int NN = kSmallN * kSmallN;
-  __shared__ double2 A[NN], A2[NN], A3[NN], A4[NN], T[NN], U[NN];
+  __shared__ double2 A[NN], A2[NN], A3[NN], A4[NN], T[NN];
   __shared__ double colsum[kSmallN];
   __shared__ int s_sq;
   const int n = d * d, e = threadIdx.x, seg = blockIdx.x;
@@ -209,44 +196,8 @@ __global__ void __launch_bounds__(kSmallN * kSmallN) grape_small_build_kernel(
   const double sc = ldexp(1.0, -sq);
   if (own) A[e] = make_double2(A[e].x * sc, A[e].y * sc);
   __syncthreads();
-  auto combo = [&](double2 x, double c0, double c1, double c2, double c3) {
-    double2 v = x;
-    if (r == c) v.x += c0;
-    v.x += c1 * A[e].x; v.y += c1 * A[e].y;
-    v.x += c2 * A2[e].x; v.y += c2 * A2[e].y;
-    v.x += c3 * A3[e].x; v.y += c3 * A3[e].y;
-    return v;
-  };
-  if (own) A2[e] = small_mm(A, A, n, r, c);
-  __syncthreads();
-  if (own) {
-    A3[e] = small_mm(A2, A, n, r, c);
-    A4[e] = small_mm(A2, A2, n, r, c);
-  }
-  __syncthreads();
-  if (own) {  // T = c12 I + c13 A + c14 A2 + c15 A3 + c16 A4
-    double2 v = combo(make_double2(0.0, 0.0), cf[12], cf[13], cf[14], cf[15]);
-    v.x += cf[16] * A4[e].x;
-    v.y += cf[16] * A4[e].y;
-    T[e] = v;
-  }
-  __syncthreads();
-  for (int j = 2; j >= 0; --j) {  // T = A4 T + B_j
-    double2 v = make_double2(0.0, 0.0);
-    if (own) v = combo(small_mm(A4, T, n, r, c), cf[4 * j], cf[4 * j + 1], cf[4 * j + 2], cf[4 * j + 3]);
-    __syncthreads();
-    if (own) T[e] = v;
-    __syncthreads();
-  }
-  for (int q = 0; q < sq; ++q) {
-    double2 v = make_double2(0.0, 0.0);
-    if (own) v = small_mm(T, T, n, r, c);
-    __syncthreads();
-    if (own) T[e] = v;
-    __syncthreads();
-  }
+  small_taylor(A, A2, A3, A4, T, n, cf, sq);
   if (own) props[(long long)seg * n * n + e] = T[e];
-  (void)U;
 }
 
 double inv_fact(int k) {
