@@ -49,6 +49,11 @@ void launch_chain_segments(const double* props, std::size_t n, int64_t segments,
 bool smem_supported(std::size_t n);
 void launch_smem(const double* p_dev, std::size_t n, double* x_re, double* x_im, double* x_aos,
                  int64_t batch, int64_t steps, Layout layout, cudaStream_t s);
+// K1b-C — n = 81 on 2-CTA clusters, DSMEM exchange of a split n-tile (k_cluster.cu)
+bool cluster_supported(std::size_t n);
+bool cluster_preferred(std::size_t n, int64_t batch);
+void launch_smem_cluster(const double* p_dev, double* x_re, double* x_im, double* x_aos, int64_t batch,
+                         int64_t steps, Layout layout, cudaStream_t s);
 // K1c — any n, persistent DMMA tiles streamed from L2 (k_tiled.cu)
 std::size_t tiled_workspace(std::size_t n, int64_t batch);
 void launch_tiled_evolve(const double* p_dev, std::size_t n, double* x_re, double* x_im,
