@@ -54,7 +54,7 @@ WORKLOAD = {
     3: "c3: d=27 three transmons, shared P (729x729, 8.5 MB), 1,024 trajectories x 200 steps",
     4: "c4: d=9 sweep, per-trajectory L/P built on GPU, 65,536 trajectories x 500 steps",
 }
-KERNEL = {0: "chain_kernel", 1: "dfma9_kernel", 2: "smem_kernel", 3: "tiled_evolve_kernel",
+KERNEL = {0: "chain_kernel", 1: "dfma9_kernel", 2: "smem_cluster_kernel", 3: "tiled_evolve_kernel",
           4: "ptm_expm_kernel+ptm_step_kernel"}
 
 
