@@ -168,6 +168,17 @@ void evolve_dev(const double* p, size_t n, double* x_re, double* x_im, double* x
   }
 }
 
+}  // namespace
+
+// AoS complex stepping with automatic kernel choice, for other launchers
+// (the density mode's packed path, k_density.cu)
+void evolve_dev_aos(const double* p, size_t n, double* x_aos, int64_t batch, int64_t steps, void* work,
+                    cudaStream_t s) {
+  evolve_dev(p, n, nullptr, nullptr, x_aos, batch, steps, LBG_ALGO_AUTO, work, s, Layout::aos);
+}
+
+namespace {
+
 // ---- NCCL through dlopen (no link-time dependency) ----
 struct Nccl {
   void* h = nullptr;

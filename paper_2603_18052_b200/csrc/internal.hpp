@@ -67,6 +67,9 @@ bool rowsplit_supported(std::size_t n, int64_t batch);
 std::size_t rowsplit_workspace(std::size_t n, int64_t batch);
 void launch_rowsplit(const double* p, std::size_t n, double* x_aos, int64_t batch, int64_t steps,
                      void* work, cudaStream_t s);
+// automatic-choice AoS stepping (capi.cu)
+void evolve_dev_aos(const double* p, std::size_t n, double* x_aos, int64_t batch, int64_t steps, void* work,
+                    cudaStream_t s);
 // density-matrix mode: shared P applied to the real coordinates (k_density.cu)
 bool density_supported(std::size_t n);
 std::size_t density_workspace(std::size_t n, int64_t batch);

@@ -102,13 +102,9 @@ def test_density_zero_steps_and_empty(lbg, torch):
     assert run_density(lbg, torch, P, empty, 5).shape == (0, 3, 3)
 
 
-def test_density_rejects_large_n(lbg, torch):
+def test_density_rejects_bad_mode(lbg, torch):
     dev = torch.device("cuda")
-    P = torch.zeros((100, 100), dtype=torch.complex128, device=dev)
-    x = torch.zeros((2, 10, 10), dtype=torch.complex128, device=dev)
-    work = torch.empty(lbg.density_workspace(100, 2), dtype=torch.uint8, device=dev)
-    with pytest.raises(ValueError):
-        lbg.evolve_density_dev(P, x, 1, work)
+    work = torch.empty(lbg.density_workspace(9, 2), dtype=torch.uint8, device=dev)
     P9 = torch.eye(9, dtype=torch.complex128, device=dev)
     x3 = torch.zeros((2, 3, 3), dtype=torch.complex128, device=dev)
     with pytest.raises(ValueError):
@@ -140,3 +136,33 @@ def test_density_host_api_pipelined_full_size(lbg, oracle):
     assert tr <= TOL_INV and herm <= TOL_INV
     for b in (0, 1, 131071, 131072, 524288, B - 1):  # chunk boundaries
         assert np.abs(out[b] - oracle.evolve(P, rho0[b], S)).max() <= TOL_RHO, b
+
+
+@pytest.mark.parametrize("d,B", [(10, 7), (11, 40), (27, 6)])
+def test_density_packed_path_matches_complex(lbg, torch, oracle, d, B):
+    """n > 84: pairs of real vectors through the complex steppers"""
+    rng = np.random.default_rng(d)
+    n = d * d
+    if d == 27:
+        h, ops = lbg.config_model(3)
+        P = lbg.expm(lbg.build_lindbladian(h, ops), 0.1)
+        x = lbg.ginibre_batch(3, 0, B, d)
+        steps = 20
+    else:
+        P = np.zeros((n, n), np.complex128)
+        for c in rng.standard_normal(3):
+            A = (rng.standard_normal((d, d)) + 1j * rng.standard_normal((d, d))) / (2 * d)
+            P += c * np.kron(A, np.conj(A))
+        x = rng.standard_normal((B, d, d)) + 1j * rng.standard_normal((B, d, d))
+        steps = 5
+    want = lbg.evolve_batch(P, x, steps) if d == 27 else None
+    if want is None:
+        want = x.reshape(B, n).T
+        for _ in range(steps):
+            want = P @ want
+        want = want.T.reshape(B, d, d)
+    for mode in (("hermitian", "auto") if d == 27 else ("general", "auto")):
+        got = run_density(lbg, torch, P, x, steps, mode)
+        assert np.abs(got - want).max() <= 1e-12 * max(1.0, np.abs(want).max()), mode
+    if d == 27:
+        assert np.abs(got[0] - oracle.evolve(P, x[0], steps)).max() <= TOL_RHO
