@@ -58,7 +58,7 @@ Mat matmul(const Mat& a, const Mat& b, size_t d) {
     }
   }
   Mat m(d * d);
-  std::memcpy(m.data(), out.data(), out.size() * sizeof(double));
+  std::memcpy(static_cast<void*>(m.data()), out.data(), out.size() * sizeof(double));
   return m;
 }
 

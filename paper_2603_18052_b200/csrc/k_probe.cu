@@ -98,7 +98,7 @@ extern "C" int lbg_measure_machine_profile(lbg_machine_profile* out) {
     check_cuda(cudaGetDevice(&dev), "device");
     cudaDeviceProp prop{};
     check_cuda(cudaGetDeviceProperties(&prop, dev), "properties");
-    std::snprintf(out->name, sizeof out->name, "%s (%d SMs, sm_%d%d)", prop.name, prop.multiProcessorCount,
+    std::snprintf(out->name, sizeof out->name, "%.40s (%d SMs, sm_%d%d)", prop.name, prop.multiProcessorCount,
                   prop.major, prop.minor);
     double dmma = 0, dfma = 0;
     if (lbg_fp64_peak(&dmma, &dfma) != LBG_OK) throw cuda_error("fp64 peak probe failed");
