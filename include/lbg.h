@@ -95,6 +95,14 @@ int lbg_evolve_shared_p_soa_dev(const double* p, size_t n, double* x_re, double*
                                 void* stream);
 int lbg_evolve_shared_p_aos_dev(const double* p, size_t n, double* x, int64_t batch,
                                 int64_t steps, int algo, void* work, void* stream);
+/* the all-SoA form of the reference's Variant::soa (lb::Propagator::soa +
+ * VectorSoA states, propagate.cpp:85-92): P as split re / im planes too.
+ * work: lbg_evolve_planes_workspace(n, batch, algo) bytes (P is interleaved
+ * into it on the device). */
+size_t lbg_evolve_planes_workspace(size_t n, int64_t batch, int algo);
+int lbg_evolve_shared_p_planes_dev(const double* p_re, const double* p_im, size_t n, double* x_re,
+                                   double* x_im, int64_t batch, int64_t steps, int algo, void* work,
+                                   void* stream);
 /* host-buffer variant (end-to-end: H2D, steps, D2H; synchronous). rho0/out are
  * batch x d x d AoS density matrices; rho0 is validated like propagate.cpp:79. */
 int lbg_evolve_shared_p(const double* p, size_t d, const double* rho0, int64_t batch,

@@ -77,6 +77,9 @@ def lib() -> C.CDLL:
     L.lbg_evolve_shared_p_soa_dev.argtypes = [vp, _sz, vp, vp, C.c_int64, C.c_int64, C.c_int, vp, vp]
     L.lbg_evolve_shared_p_aos_dev.argtypes = [vp, _sz, vp, C.c_int64, C.c_int64, C.c_int, vp, vp]
     L.lbg_evolve_shared_p.argtypes = [_dp, _sz, _dp, C.c_int64, C.c_int64, _dp, C.c_int]
+    L.lbg_evolve_planes_workspace.argtypes = [_sz, C.c_int64, C.c_int]
+    L.lbg_evolve_planes_workspace.restype = _sz
+    L.lbg_evolve_shared_p_planes_dev.argtypes = [vp, vp, _sz, vp, vp, C.c_int64, C.c_int64, C.c_int, vp, vp]
     L.lbg_density_workspace.argtypes = [_sz, C.c_int64]
     L.lbg_density_workspace.restype = _sz
     L.lbg_evolve_density_dev.argtypes = [vp, _sz, vp, C.c_int64, C.c_int64, C.c_int, vp, vp]

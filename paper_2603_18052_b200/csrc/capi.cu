@@ -397,6 +397,24 @@ void host_evolve_impl(const double* p, size_t d, const double* rho0, int64_t bat
 
 extern "C" {
 
+size_t lbg_evolve_planes_workspace(size_t n, int64_t batch, int algo) {
+  return ((n * n * 16 + 255) & ~size_t(255)) + lbg_evolve_workspace(n, batch, algo);
+}
+
+int lbg_evolve_shared_p_planes_dev(const double* p_re, const double* p_im, size_t n, double* x_re, double* x_im,
+                                   int64_t batch, int64_t steps, int algo, void* work, void* stream) {
+  return guarded([&] {
+    if (!p_re || !p_im) throw invalid_argument("evolve: null propagator");
+    if (!work) throw invalid_argument("evolve: workspace required");
+    if (batch == 0 || steps == 0) return;
+    cudaStream_t s = as_stream(stream);
+    double* p = static_cast<double*>(work);
+    launch_planes_to_aos(p_re, p_im, (long long)n * (long long)n, p, s);
+    void* inner = static_cast<char*>(work) + ((n * n * 16 + 255) & ~size_t(255));
+    evolve_dev(p, n, x_re, x_im, nullptr, batch, steps, algo, inner, s, Layout::soa);
+  });
+}
+
 int lbg_evolve_shared_p(const double* p, size_t d, const double* rho0, int64_t batch, int64_t steps,
                         double* out, int algo) {
   return guarded([&] {

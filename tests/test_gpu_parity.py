@@ -7,8 +7,12 @@ GPU outputs. The GPU propagator uses Taylor-16/Paterson-Stockmeyer instead of
 the reference's Pade-13 (both accurate to unit roundoff), so P itself is
 compared at 1e-13 relative; the generator L is compared bit for bit.
 """
+import ctypes
+
 import numpy as np
 import pytest
+
+C_SZ = ctypes.c_size_t
 
 pytestmark = pytest.mark.gpu
 
@@ -420,3 +424,28 @@ def test_tiled_ragged_shapes_vs_torch(lbg, torch, n, B):
         want = want @ P.T
     torch.cuda.synchronize()
     assert (x - want).abs().max().item() <= 1e-13 * want.abs().max().item()
+
+
+@pytest.mark.parametrize("n,B", [(9, 3000), (81, 70), (81, 5), (729, 3)])
+def test_all_soa_planes_entry_point(lbg, torch, n, B):
+    """lbg_evolve_shared_p_planes_dev (P and the states as re / im planes, the
+    reference's Variant::soa) equals the AoS path"""
+    rng = np.random.default_rng(n + B)
+    P = (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) / (2 * n)
+    x = rng.standard_normal((B, n)) + 1j * rng.standard_normal((B, n))
+    dev = torch.device("cuda")
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    xa, pt = T(x), T(P)
+    w0 = torch.empty(max(lbg.evolve_workspace(n, B), 1), dtype=torch.uint8, device=dev)
+    lbg.evolve_batch_dev(pt, xa, 6, work=w0)
+    xr, xi = T(x.real), T(x.imag)
+    L = lbg.lib()
+    L.lbg_evolve_planes_workspace.restype = C_SZ
+    ws = L.lbg_evolve_planes_workspace(n, B, 0)
+    work = torch.empty(ws, dtype=torch.uint8, device=dev)
+    pr, pi = T(P.real), T(P.imag)  # keep the planes alive across the call
+    lbg._check(L.lbg_evolve_shared_p_planes_dev(lbg._tp(pr), lbg._tp(pi), n, lbg._tp(xr), lbg._tp(xi),
+                                                B, 6, 0, lbg._tp(work), None), "planes")
+    torch.cuda.synchronize()
+    got = xr.cpu().numpy() + 1j * xi.cpu().numpy()
+    assert np.abs(got - xa.cpu().numpy()).max() <= 1e-13 * max(1.0, np.abs(got).max())
