@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -32,6 +33,7 @@ int guarded(F&& f) {
     return LBG_EINVAL;
   } catch (const lbg::cuda_error& e) {
     g_err = e.what();
+    (void)cudaGetLastError();  // a non-sticky launch error must not surface in the next, unrelated call
     return LBG_ECUDA;
   } catch (const std::exception& e) {
     g_err = e.what();
@@ -88,9 +90,14 @@ struct EvolvePool {
     w[1].ensure(wb);
   }
 };
-EvolvePool& evolve_pool() {
-  static EvolvePool* pool = new EvolvePool;  // intentionally leaked: outlives CUDA teardown
-  return *pool;
+EvolvePool& evolve_pool() {  // one per device (buffers and streams belong to it)
+  static std::mutex mu;
+  static std::map<int, EvolvePool*>* pools = new std::map<int, EvolvePool*>;  // leaked: outlives CUDA teardown
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(mu);
+  EvolvePool*& p = (*pools)[dev];
+  if (!p) p = new EvolvePool;
+  return *p;
 }
 
 // reference is_hermitian (lindblad.cpp:13-20): relative 1e-12 on max |h|
@@ -214,6 +221,25 @@ void nccl_check(int rc, const char* what) {
 }  // namespace
 
 void note_launch(int n) { g_launches += n; }
+
+int current_device() {
+  int dev = 0;
+  check_cuda(cudaGetDevice(&dev), "get device");
+  return dev;
+}
+
+void ensure_max_dyn_smem(const void* fn, int bytes) {
+  // the attribute is an upper bound: only ever raise it (launches of one
+  // kernel with different sizes, in any order, all stay valid)
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int>* cur = new std::map<std::pair<const void*, int>, int>;
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(mu);
+  int& have = (*cur)[{fn, dev}];
+  if (bytes <= have) return;
+  check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "smem attr");
+  have = bytes;
+}
 
 }  // namespace lbg
 

@@ -115,6 +115,9 @@ void launch_ptm_sweep(std::size_t d, const double* h0, const double* hd, const d
                       double dt, const double* rho0, int64_t batch, int64_t steps, double* pops,
                       double* ens_sum, void* work, cudaStream_t s);
 
-int sm_count();
+int sm_count();       // of the current device
+int current_device();
+// cudaFuncAttributeMaxDynamicSharedMemorySize, set once per (kernel, device)
+void ensure_max_dyn_smem(const void* fn, int bytes);
 
 }  // namespace lbg

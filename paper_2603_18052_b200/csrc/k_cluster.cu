@@ -351,20 +351,10 @@ void launch_smem_cluster(const double* p_dev, double* x_re, double* x_im, double
   const double2* p2 = reinterpret_cast<const double2*>(p_dev);
   const dim3 grid(unsigned(2 * clusters));
   if (layout == Layout::soa) {
-    static bool a = [] {
-      check_cuda(cudaFuncSetAttribute(smem_cluster_kernel<Layout::soa>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(SMEM_BYTES)), "smem attr");
-      return true;
-    }();
-    (void)a;
+    ensure_max_dyn_smem((const void*)smem_cluster_kernel<Layout::soa>, int(SMEM_BYTES));
     smem_cluster_kernel<Layout::soa><<<grid, 32 * CWARPS, SMEM_BYTES, s>>>(p2, x_re, x_im, nullptr, batch, steps, pl);
   } else {
-    static bool a = [] {
-      check_cuda(cudaFuncSetAttribute(smem_cluster_kernel<Layout::aos>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(SMEM_BYTES)), "smem attr");
-      return true;
-    }();
-    (void)a;
+    ensure_max_dyn_smem((const void*)smem_cluster_kernel<Layout::aos>, int(SMEM_BYTES));
     smem_cluster_kernel<Layout::aos><<<grid, 32 * CWARPS, SMEM_BYTES, s>>>(p2, nullptr, nullptr, x_aos, batch, steps,
                                                                            pl);
   }

@@ -19,6 +19,7 @@
 // in pairs through the complex steppers (below), and K1b-R `smem_real_kernel`
 // (n <= 84: P_R resident in shared memory, real m8n8k4 DMMA, 32 vectors/CTA,
 // 8 warps balanced over the 4 SMSPs).
+#include <map>
 #include <mutex>
 
 #include "../../include/lbg.h"
@@ -211,9 +212,14 @@ struct SlotPool {
   bool init = false;
   int next = 0;
 };
-SlotPool& pool() {
-  static SlotPool p;
-  return p;
+SlotPool& pool() {  // per device: events and the constant bank belong to one device
+  static std::mutex mu;
+  static std::map<int, SlotPool*>* pools = new std::map<int, SlotPool*>;  // leaked: outlives CUDA teardown
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(mu);
+  SlotPool*& p = (*pools)[dev];
+  if (!p) p = new SlotPool;
+  return *p;
 }
 
 // ---- K1b-R: n <= 84, real DMMA, P_R in shared memory ---------------------------
@@ -327,9 +333,7 @@ template <int N, int MG>
 void launch_smem_real(const double* pr, int n, double* x, int64_t count, int64_t half, const int* flag,
                       int64_t steps, cudaStream_t s) {
   const RGeom g(n);
-  check_cuda(cudaFuncSetAttribute(smem_real_kernel<N, MG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(g.total)),
-             "smem attr");
+  ensure_max_dyn_smem((const void*)smem_real_kernel<N, MG>, int(g.total));
   smem_real_kernel<N, MG><<<unsigned((count + kVec - 1) / kVec), 32 * kWarpsR, g.total, s>>>(pr, n, x, count, half,
                                                                                              flag, steps);
   LBG_CHECK_LAUNCH("smem_real_kernel");

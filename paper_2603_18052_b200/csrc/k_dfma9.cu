@@ -11,6 +11,7 @@
 //
 // Replaces the reference hot loop step_soa_kernel (proj/src/kernels_variants.cpp:26-41)
 // driven by evolve (proj/src/propagate.cpp:85-92) for every trajectory.
+#include <map>
 #include <mutex>
 
 #include "common.cuh"
@@ -86,9 +87,14 @@ struct SlotPool {
   bool init = false;
   int next = 0;
 };
-SlotPool& pool() {
-  static SlotPool p;
-  return p;
+SlotPool& pool() {  // per device: events and the constant bank belong to one device
+  static std::mutex mu;
+  static std::map<int, SlotPool*>* pools = new std::map<int, SlotPool*>;  // leaked: outlives CUDA teardown
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(mu);
+  SlotPool*& p = (*pools)[dev];
+  if (!p) p = new SlotPool;
+  return *p;
 }
 
 }  // namespace

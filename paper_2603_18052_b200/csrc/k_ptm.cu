@@ -377,12 +377,7 @@ void launch_ptm_sweep(size_t d, const double* h0, const double* hd, const double
   rho_to_x_kernel<<<1, 96, 0, s>>>(reinterpret_cast<const double2*>(rho0), x0);
   LBG_CHECK_LAUNCH("rho_to_x_kernel");
   const size_t smem = size_t(3) * MAT * 8;
-  static bool attr = [&] {
-    check_cuda(cudaFuncSetAttribute(ptm_expm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
-               "smem attr");
-    return true;
-  }();
-  (void)attr;
+  ensure_max_dyn_smem((const void*)ptm_expm_kernel, int(smem));
   for (int64_t c0 = 0; c0 < batch; c0 += int64_t(chunk)) {
     const int cb = int(std::min<int64_t>(int64_t(chunk), batch - c0));
     ptm_expm_kernel<<<cb, THREADS, smem, s>>>(dr, reinterpret_cast<const double2*>(h0),

@@ -173,8 +173,7 @@ void launch_cta_chain(const double* p, size_t n, double* x_aos, int64_t batch, i
   const int ni = int(n);
   const int S = ni + ((4 - ni % 8) + 8) % 8;
   const size_t smem = (size_t(ni) * S + 2 * (ni + (kMaxCtaN + 3) / 4)) * sizeof(double2);
-  check_cuda(cudaFuncSetAttribute(cta_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
-             "smem attr");
+  ensure_max_dyn_smem((const void*)cta_chain_kernel, int(smem));
   const int threads = ((4 * ni + 31) / 32) * 32;
   cta_chain_kernel<<<unsigned(batch), threads, smem, s>>>(reinterpret_cast<const double2*>(p), ni,
                                                            reinterpret_cast<double2*>(x_aos), steps);
@@ -208,8 +207,7 @@ void launch_rowsplit(const double* p, size_t n, double* x_aos, int64_t batch, in
   const int grid = rowsplit_grid(n);
   const int rows_max = int((n + grid - 1) / grid);
   const size_t smem = (size_t(rows_max) * n + size_t(batch) * n) * sizeof(double2);
-  check_cuda(cudaFuncSetAttribute(rowsplit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
-             "smem attr");
+  ensure_max_dyn_smem((const void*)rowsplit_kernel, int(smem));
   const double2* p2 = reinterpret_cast<const double2*>(p);
   int ni = int(n), bi = int(batch);
   int64_t st = steps;

@@ -162,13 +162,11 @@ void launch_mg(const double* p, int n, double* x_re, double* x_im, double* x_aos
   const double2* p2 = reinterpret_cast<const double2*>(p);
   if (layout == Layout::soa) {
     auto k = smem_kernel<N, MG, Layout::soa>;
-    check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(g.total)),
-               "smem attr");
+    ensure_max_dyn_smem((const void*)k, int(g.total));
     k<<<blocks, 32 * kWarps, g.total, s>>>(p2, n, x_re, x_im, nullptr, batch, steps);
   } else {
     auto k = smem_kernel<N, MG, Layout::aos>;
-    check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(g.total)),
-               "smem attr");
+    ensure_max_dyn_smem((const void*)k, int(g.total));
     k<<<blocks, 32 * kWarps, g.total, s>>>(p2, n, nullptr, nullptr, x_aos, batch, steps);
   }
   LBG_CHECK_LAUNCH("smem_kernel");

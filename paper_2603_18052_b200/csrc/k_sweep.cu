@@ -311,8 +311,7 @@ void launch_sweep(size_t d, const double* h0, const double* hd, const double* hs
   const long long nn = (long long)n * n;
   check_cuda(cudaMemsetAsync(ens_sum, 0, size_t(n) * 16, s), "memset ens");
   const size_t smem = size_t(nn + 2 * n) * 16;
-  check_cuda(cudaFuncSetAttribute(sweep_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
-             "smem attr");
+  ensure_max_dyn_smem((const void*)sweep_step_kernel, int(smem));
   propagators_complex(d, h0, hd, hs, n_ops, ops, delta, scale, dt, batch, work, s,
                       [&](const double2* P, int64_t c0, int cb) {
                         sweep_step_kernel<<<cb, 96, smem, s>>>(P, nn, reinterpret_cast<const double2*>(rho0),

@@ -29,6 +29,8 @@
 #include <cuda.h>  // CUtensorMap (driver types only; the encoder comes via cudaGetDriverEntryPoint)
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 
 #include "common.cuh"
 #include "internal.hpp"
@@ -530,13 +532,13 @@ CUtensorMap complex_map(const double2* base, size_t rows, size_t cols, unsigned 
 }  // namespace
 
 int sm_count() {
-  static int count = [] {
-    int dev = 0, c = 0;
-    check_cuda(cudaGetDevice(&dev), "get device");
-    check_cuda(cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev), "sm count");
-    return c;
-  }();
-  return count;
+  static std::mutex mu;
+  static std::map<int, int>* counts = new std::map<int, int>;
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(mu);
+  int& c = (*counts)[dev];
+  if (c == 0) check_cuda(cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev), "sm count");
+  return c;
 }
 
 size_t tiled_ntiles(size_t n, int64_t batch) {
@@ -568,16 +570,10 @@ void launch_tiled_evolve(const double* p_dev, size_t n, double* x_re, double* x_
   convert<true>(x_re, x_im, x_aos, v0, ni, bi, layout, s);
   check_cuda(cudaMemsetAsync(ctl, 0, sizeof(StepCtl), s), "memset ctl");
 
-  static int occ = [] {
-    check_cuda(cudaFuncSetAttribute(tiled_evolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(StepGeo::kSmemBytes)),
-               "smem attr");
-    int o = 0;
-    check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, tiled_evolve_kernel, THREADS,
-                                                             StepGeo::kSmemBytes),
-               "occupancy");
-    return o;
-  }();
+  ensure_max_dyn_smem((const void*)tiled_evolve_kernel, int(StepGeo::kSmemBytes));
+  int occ = 0;
+  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tiled_evolve_kernel, THREADS, StepGeo::kSmemBytes),
+             "occupancy");
   const int ntiles = ((ni + BM - 1) / BM) * ((bi + StepGeo::BN - 1) / StepGeo::BN);
   int grid = std::min(occ * sm_count(), ntiles);
   if (grid < 1) grid = 1;
@@ -600,13 +596,7 @@ void launch_tiled_evolve(const double* p_dev, size_t n, double* x_re, double* x_
 
 void launch_zgemm(const double* a, const double* b, double* c, int n, int batch, long long stride_a,
                   long long stride_b, long long stride_c, cudaStream_t s) {
-  static bool init = [] {
-    check_cuda(cudaFuncSetAttribute(zgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(Geo<32>::kSmemBytes)),
-               "smem attr");
-    return true;
-  }();
-  (void)init;
+  ensure_max_dyn_smem((const void*)zgemm_kernel, int(Geo<32>::kSmemBytes));
   const long long nn = (long long)n * n;
   if ((stride_a != 0 && stride_a != nn) || (stride_b != 0 && stride_b != nn))
     throw invalid_argument("zgemm: batch strides must be 0 or n*n");
