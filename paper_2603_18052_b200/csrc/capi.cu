@@ -581,6 +581,7 @@ int lbg_run_bench(const lbg_bench_config* cfg, lbg_bench_result* out) {
 // ---- per-trajectory sweep (config 4) ----
 size_t lbg_sweep_workspace(size_t d, int64_t batch) {
   const size_t c = sweep_workspace(d, batch);
+  if (ptm_small_supported(d)) return std::max(c, ptm_small_workspace(d, batch));
   return ptm_sweep_supported(d) ? std::max(c, ptm_sweep_workspace(batch)) : c;
 }
 
@@ -599,7 +600,7 @@ int lbg_evolve_sweep_dev(size_t d, const double* h0, const double* hd, const dou
     bool real = false;
     if (mode == LBG_SWEEP_REAL || mode == LBG_SWEEP_AUTO) {
       bool herm = false;
-      if (ptm_sweep_supported(d)) {  // the real representation needs an exactly Hermitian rho0
+      if (ptm_sweep_supported(d) || ptm_small_supported(d)) {  // the real form needs an exactly Hermitian rho0
         std::vector<double> r(2 * d * d);
         check_cuda(cudaMemcpyAsync(r.data(), rho0, r.size() * 8, cudaMemcpyDeviceToHost, s), "D2H rho0");
         check_cuda(cudaStreamSynchronize(s), "sync");
@@ -610,12 +611,14 @@ int lbg_evolve_sweep_dev(size_t d, const double* h0, const double* hd, const dou
                    r[2 * (i * d + j) + 1] == -r[2 * (j * d + i) + 1];
       }
       if (mode == LBG_SWEEP_REAL && !herm)
-        throw invalid_argument("sweep: real mode needs d == 9 and an exactly Hermitian rho0");
+        throw invalid_argument("sweep: real mode needs d in {2, 3, 9} and an exactly Hermitian rho0");
       real = herm;
     } else if (mode != LBG_SWEEP_COMPLEX) {
       throw invalid_argument("sweep: unknown mode");
     }
-    if (real)
+    if (real && ptm_small_supported(d))
+      launch_ptm_sweep_small(d, h0, hd, hs, n_ops, ops, delta, scale, dt, rho0, batch, steps, pops, ens_sum, work, s);
+    else if (real)
       launch_ptm_sweep(d, h0, hd, hs, n_ops, ops, delta, scale, dt, rho0, batch, steps, pops, ens_sum, work, s);
     else
       launch_sweep(d, h0, hd, hs, n_ops, ops, delta, scale, dt, rho0, batch, steps, pops, ens_sum, work, s);

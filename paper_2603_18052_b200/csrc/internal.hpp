@@ -115,6 +115,14 @@ void launch_ptm_sweep(std::size_t d, const double* h0, const double* hd, const d
                       double dt, const double* rho0, int64_t batch, int64_t steps, double* pops,
                       double* ens_sum, void* work, cudaStream_t s);
 
+// d <= 3 sweeps: warp-per-trajectory build, thread-per-trajectory stepping (k_ptm_small.cu)
+bool ptm_small_supported(std::size_t d);
+std::size_t ptm_small_workspace(std::size_t d, int64_t batch);
+void launch_ptm_sweep_small(std::size_t d, const double* h0, const double* hd, const double* hs,
+                            std::size_t n_ops, const double* ops, const double* delta, const double* scale,
+                            double dt, const double* rho0, int64_t batch, int64_t steps, double* pops,
+                            double* ens_sum, void* work, cudaStream_t s);
+
 int sm_count();       // of the current device
 int current_device();
 // cudaFuncAttributeMaxDynamicSharedMemorySize, set once per (kernel, device)

@@ -449,3 +449,41 @@ def test_all_soa_planes_entry_point(lbg, torch, n, B):
     torch.cuda.synchronize()
     got = xr.cpu().numpy() + 1j * xi.cpu().numpy()
     assert np.abs(got - xa.cpu().numpy()).max() <= 1e-13 * max(1.0, np.abs(got).max())
+
+
+@pytest.mark.parametrize("d,B", [(2, 1000), (3, 65536), (3, 33)])
+def test_small_d_sweep_real_vs_complex_and_oracle(lbg, torch, oracle, d, B):
+    """per-trajectory P at d <= 3 (warp-per-trajectory build, thread-per-trajectory
+    steps) against the complex path and, for sampled trajectories, the oracle"""
+    rng = np.random.default_rng(d * 7 + B)
+    dev = torch.device("cuda")
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    if d == 3:
+        h0, ops = lbg.config_model(0)
+    else:
+        h0 = np.array([[0.3, 0.1 - 0.05j], [0.1 + 0.05j, -0.2]], complex)
+        ops = np.array([[[0, 0.05], [0, 0]]], complex)
+    hd = np.diag(np.arange(d)).astype(complex)
+    hs = np.zeros((d, d), complex)
+    for i in range(d - 1):
+        hs[i, i + 1] = hs[i + 1, i] = 0.02 * np.sqrt(i + 1)
+    delta, scale = rng.uniform(-0.03, 0.03, B), rng.uniform(0.9, 1.1, B)
+    r0 = np.zeros((d, d), complex)
+    r0[0, 0] = 1.0
+    S = 200
+    outs = {}
+    for mode in ("real", "complex"):
+        pops = torch.zeros(B, d, dtype=torch.float64, device=dev)
+        ens = torch.zeros(d, d, dtype=torch.complex128, device=dev)
+        work = torch.empty(lbg.sweep_workspace(d, B), dtype=torch.uint8, device=dev)
+        lbg.evolve_sweep_dev(T(h0), T(hd), T(hs), T(ops), T(delta), T(scale), 0.1, T(r0), S, pops, ens, work,
+                             mode=mode)
+        torch.cuda.synchronize()
+        outs[mode] = (pops.cpu().numpy(), ens.cpu().numpy())
+    assert np.abs(outs["real"][0] - outs["complex"][0]).max() <= TOL_RHO
+    assert np.abs(outs["real"][1] - outs["complex"][1]).max() <= TOL_RHO * B
+    assert abs(np.trace(outs["real"][1]).real - B) <= 1e-9 * B
+    for b in (0, B // 2, B - 1):
+        P = oracle.expm(oracle.build_lindbladian(h0 + delta[b] * hd + scale[b] * hs, ops), 0.1)
+        want = np.diag(oracle.evolve(P, r0, S)).real
+        assert np.abs(outs["real"][0][b] - want).max() <= TOL_RHO, b
