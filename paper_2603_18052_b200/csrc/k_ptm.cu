@@ -275,29 +275,37 @@ __global__ void __launch_bounds__(THREADS, 1)
 // 81-term dot product runs as 12 independent chains (depth 7) and the loads of
 // x are issued in 4 blocks (compiler barrier) to keep the register count at
 // 3 CTAs per SM.
-constexpr int STEP_THREADS = 96;
+// Three trajectories per CTA: 8 warps hold 3 x 81 = 243 rows (13 idle lanes),
+// i.e. two 224-register warps per sub-partition — all a sub-partition's 16K
+// registers can carry — so an SM steps 3 trajectories at once instead of the 2
+// that 3-warp one-trajectory CTAs reach (their third warp would not fit).
+constexpr int STEP_TRAJ = 3;
+constexpr int STEP_THREADS = 256;
 constexpr int NACC = 12;
-__global__ void __maxnreg__(224) ptm_step_kernel(const double* __restrict__ p_r,
-                                                                  const double* __restrict__ x0,
-                                                                  int64_t steps, double* __restrict__ pops,
-                                                                  double* __restrict__ ens_x) {
-  __shared__ __align__(16) double xs[2][88];
+__global__ void __maxnreg__(224)
+    ptm_step_kernel(const double* __restrict__ p_r, const double* __restrict__ x0, int64_t count, int64_t steps,
+                    double* __restrict__ pops, double* __restrict__ ens_x) {
+  __shared__ __align__(16) double xs[2][STEP_TRAJ][88];
   const int tid = threadIdx.x;
-  const int row = tid < N ? tid : N - 1;  // idle lanes shadow the last row
-  const double* pb = p_r + size_t(blockIdx.x) * N * N + size_t(row) * N;
+  const int tt = tid < STEP_TRAJ * N ? tid / N : STEP_TRAJ - 1;   // trajectory within the CTA
+  const int row = tid < STEP_TRAJ * N ? tid - tt * N : N - 1;      // idle lanes shadow the last row
+  const int64_t b = int64_t(blockIdx.x) * STEP_TRAJ + tt;
+  const bool live = b < count;
+  const double* pb = p_r + size_t(live ? b : 0) * N * N + size_t(row) * N;
   double p[N];
 #pragma unroll
   for (int j = 0; j < N; ++j) p[j] = pb[j];
-  for (int e = tid; e < 88; e += STEP_THREADS) {
-    xs[0][e] = e < N ? x0[e] : 0.0;
-    xs[1][e] = 0.0;
+  for (int e = tid; e < STEP_TRAJ * 88; e += STEP_THREADS) {
+    const int c = e % 88;
+    xs[0][e / 88][c] = c < N ? x0[c] : 0.0;
+    xs[1][e / 88][c] = 0.0;
   }
   __syncthreads();
-  const int slot = tid < N ? tid : N;  // idle lanes write a dummy slot
+  const int slot = tid < STEP_TRAJ * N ? row : N;  // idle lanes write a dummy slot
   int cur = 0;
 #pragma unroll 1
   for (int64_t s = 0; s < steps; ++s) {
-    const double* x = xs[cur];
+    const double* x = xs[cur][tt];
     double acc[NACC];
 #pragma unroll
     for (int a = 0; a < NACC; ++a) acc[a] = 0.0;
@@ -313,13 +321,14 @@ __global__ void __maxnreg__(224) ptm_step_kernel(const double* __restrict__ p_r,
     for (int w = 1; w < NACC; w *= 2)
 #pragma unroll
       for (int a = 0; a + w < NACC; a += 2 * w) acc[a] += acc[a + w];
-    const double y = acc[0];
-    xs[cur ^ 1][slot] = y;
+    xs[cur ^ 1][tt][slot] = acc[0];
     __syncthreads();
     cur ^= 1;
   }
-  if (tid < D) pops[size_t(blockIdx.x) * D + tid] = xs[cur][tid * D + tid];
-  if (tid < N) atomicAdd(&ens_x[tid], xs[cur][tid]);
+  if (tid < STEP_TRAJ * N && live) {
+    if (row < D) pops[size_t(b) * D + row] = xs[cur][tt][row * D + row];
+    atomicAdd(&ens_x[row], xs[cur][tt][row]);
+  }
 }
 
 // complex rho (d x d) <-> real coordinates
@@ -385,7 +394,8 @@ void launch_ptm_sweep(size_t d, const double* h0, const double* hd, const double
                                               reinterpret_cast<const double2*>(hs), delta + c0, scale + c0,
                                               dt, pr);
     LBG_CHECK_LAUNCH("ptm_expm_kernel");
-    ptm_step_kernel<<<cb, STEP_THREADS, 0, s>>>(pr, x0, steps, pops + c0 * int64_t(D), ens_x);
+    ptm_step_kernel<<<unsigned((cb + STEP_TRAJ - 1) / STEP_TRAJ), STEP_THREADS, 0, s>>>(
+        pr, x0, cb, steps, pops + c0 * int64_t(D), ens_x);
     LBG_CHECK_LAUNCH("ptm_step_kernel");
   }
   x_to_rho_kernel<<<1, 96, 0, s>>>(ens_x, reinterpret_cast<double2*>(ens_sum));
