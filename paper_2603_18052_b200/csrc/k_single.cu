@@ -26,9 +26,13 @@ namespace {
 constexpr int kMaxCtaN = 96;
 
 // ---------------------------------------------------------------- K2b ------
-__global__ void __launch_bounds__(4 * kMaxCtaN) cta_chain_kernel(const double2* __restrict__ p, int n,
+// NT > 0: n known at compile time (n = 81: exact quarter rows, no predicates,
+// constant addresses); NT == 0: runtime n
+template <int NT>
+__global__ void __launch_bounds__(4 * kMaxCtaN) cta_chain_kernel(const double2* __restrict__ p, int n_rt,
                                                                 double2* __restrict__ x, int64_t steps) {
   extern __shared__ __align__(16) double2 sm2[];
+  const int n = NT > 0 ? NT : n_rt;
   const int S = n + ((4 - n % 8) + 8) % 8;  // row stride = 4 (mod 8) complex
   double2* ps = sm2;
   constexpr int VPAD = (kMaxCtaN + 3) / 4;  // quarter rows may read up to QMAX past n
@@ -36,7 +40,7 @@ __global__ void __launch_bounds__(4 * kMaxCtaN) cta_chain_kernel(const double2* 
   double2* vb = va + n + VPAD;
   const int tid = threadIdx.x;
   const int i = tid >> 2, q = tid & 3;
-  const int Q = (n + 3) / 4;
+  const int Q = NT > 0 ? (NT + 3) / 4 : (n + 3) / 4;
   double2* xb = x + size_t(blockIdx.x) * n;
   for (int e = tid; e < n * S; e += blockDim.x) {
     const int r = e / S, c = e - r * S;
@@ -47,7 +51,8 @@ __global__ void __launch_bounds__(4 * kMaxCtaN) cta_chain_kernel(const double2* 
   const bool active = i < n;
   const int j0 = q * Q;
   // this thread's quarter row of P, register resident for all steps
-  constexpr int QMAX = (kMaxCtaN + 3) / 4;
+  constexpr int QMAX = NT > 0 ? (NT + 3) / 4 : (kMaxCtaN + 3) / 4;
+  constexpr int NC = NT > 0 ? 8 : 4;  // independent FMA chains per re / im (DFMA latency 23 cycles)
   double2 pr[QMAX];
 #pragma unroll
   for (int jj = 0; jj < QMAX; ++jj) {
@@ -58,20 +63,28 @@ __global__ void __launch_bounds__(4 * kMaxCtaN) cta_chain_kernel(const double2* 
 #pragma unroll 1
   for (int64_t s = 0; s < steps; ++s) {
     vq = va + j0;
-    double ar[4] = {0.0, 0.0, 0.0, 0.0}, ai[4] = {0.0, 0.0, 0.0, 0.0};
+    double ar[NC], ai[NC];
 #pragma unroll
-    for (int jj = 0; jj < QMAX; ++jj) {  // 8 independent FMA chains (DFMA latency 23 cycles)
-      if (jj < Q) {
+    for (int c = 0; c < NC; ++c) ar[c] = ai[c] = 0.0;
+#pragma unroll
+    for (int jj = 0; jj < QMAX; ++jj) {  // 2 NC independent FMA chains
+      if (NT > 0 || jj < Q) {
         const double2 a = pr[jj], v = vq[jj];
-        const int c = jj & 3;
+        const int c = jj % NC;
         ar[c] = fma(a.x, v.x, ar[c]);
         ar[c] = fma(-a.y, v.y, ar[c]);
         ai[c] = fma(a.x, v.y, ai[c]);
         ai[c] = fma(a.y, v.x, ai[c]);
       }
     }
-    double re = (ar[0] + ar[1]) + (ar[2] + ar[3]);
-    double im = (ai[0] + ai[1]) + (ai[2] + ai[3]);
+#pragma unroll
+    for (int w = 1; w < NC; w *= 2)
+#pragma unroll
+      for (int c = 0; c + w < NC; c += 2 * w) {
+        ar[c] += ar[c + w];
+        ai[c] += ai[c + w];
+      }
+    double re = ar[0], im = ai[0];
     re += __shfl_xor_sync(0xffffffffu, re, 1);
     im += __shfl_xor_sync(0xffffffffu, im, 1);
     re += __shfl_xor_sync(0xffffffffu, re, 2);
@@ -173,10 +186,16 @@ void launch_cta_chain(const double* p, size_t n, double* x_aos, int64_t batch, i
   const int ni = int(n);
   const int S = ni + ((4 - ni % 8) + 8) % 8;
   const size_t smem = (size_t(ni) * S + 2 * (ni + (kMaxCtaN + 3) / 4)) * sizeof(double2);
-  ensure_max_dyn_smem((const void*)cta_chain_kernel, int(smem));
+  ensure_max_dyn_smem((const void*)cta_chain_kernel<0>, int(smem));
   const int threads = ((4 * ni + 31) / 32) * 32;
-  cta_chain_kernel<<<unsigned(batch), threads, smem, s>>>(reinterpret_cast<const double2*>(p), ni,
-                                                           reinterpret_cast<double2*>(x_aos), steps);
+  if (ni == 81) {
+    ensure_max_dyn_smem((const void*)cta_chain_kernel<81>, int(smem));
+    cta_chain_kernel<81><<<unsigned(batch), threads, smem, s>>>(reinterpret_cast<const double2*>(p), ni,
+                                                                reinterpret_cast<double2*>(x_aos), steps);
+  } else {
+    cta_chain_kernel<0><<<unsigned(batch), threads, smem, s>>>(reinterpret_cast<const double2*>(p), ni,
+                                                               reinterpret_cast<double2*>(x_aos), steps);
+  }
   LBG_CHECK_LAUNCH("cta_chain_kernel");
 }
 
