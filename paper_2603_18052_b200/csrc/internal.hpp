@@ -63,6 +63,8 @@ void launch_tiled_evolve(const double* p_dev, std::size_t n, double* x_re, doubl
 bool cta_chain_supported(std::size_t n);
 void launch_cta_chain(const double* p, std::size_t n, double* x_aos, int64_t batch, int64_t steps,
                       cudaStream_t s);
+void launch_cta_chain_segments(const double* props, std::size_t n, int64_t segments, int64_t sps,
+                               double* x_aos, cudaStream_t s);
 bool rowsplit_supported(std::size_t n, int64_t batch);
 std::size_t rowsplit_workspace(std::size_t n, int64_t batch);
 void launch_rowsplit(const double* p, std::size_t n, double* x_aos, int64_t batch, int64_t steps,

@@ -27,10 +27,13 @@ constexpr int kMaxCtaN = 96;
 
 // ---------------------------------------------------------------- K2b ------
 // NT > 0: n known at compile time (n = 81: exact quarter rows, no predicates,
-// constant addresses); NT == 0: runtime n
+// constant addresses); NT == 0: runtime n. `segments` > 1 is the GRAPE chain
+// in one launch: segment g applies props[g] for sps steps, and the next
+// segment's P streams into shared memory (cp.async) while the current one runs.
 template <int NT>
-__global__ void __launch_bounds__(4 * kMaxCtaN) cta_chain_kernel(const double2* __restrict__ p, int n_rt,
-                                                                double2* __restrict__ x, int64_t steps) {
+__global__ void __launch_bounds__(4 * kMaxCtaN) cta_chain_kernel(const double2* __restrict__ props, int n_rt,
+                                                                double2* __restrict__ x, int64_t segments,
+                                                                int64_t sps) {
   extern __shared__ __align__(16) double2 sm2[];
   const int n = NT > 0 ? NT : n_rt;
   const int S = n + ((4 - n % 8) + 8) % 8;  // row stride = 4 (mod 8) complex
@@ -42,58 +45,66 @@ __global__ void __launch_bounds__(4 * kMaxCtaN) cta_chain_kernel(const double2* 
   const int i = tid >> 2, q = tid & 3;
   const int Q = NT > 0 ? (NT + 3) / 4 : (n + 3) / 4;
   double2* xb = x + size_t(blockIdx.x) * n;
-  for (int e = tid; e < n * S; e += blockDim.x) {
-    const int r = e / S, c = e - r * S;
-    ps[e] = c < n ? p[size_t(r) * n + c] : make_double2(0.0, 0.0);
-  }
+  auto stage = [&](const double2* p) {  // P (n x n) -> padded shared memory, asynchronously
+    for (int e = tid; e < n * S; e += blockDim.x) {
+      const int r = e / S, c = e - r * S;
+      cp_async16(ps + e, p + size_t(r) * n + (c < n ? c : 0), c < n);
+    }
+    cp_async_commit();
+  };
+  stage(props);
   for (int e = tid; e < 2 * (n + VPAD); e += blockDim.x) va[e] = e < n ? xb[e] : make_double2(0.0, 0.0);
-  __syncthreads();
   const bool active = i < n;
   const int j0 = q * Q;
-  // this thread's quarter row of P, register resident for all steps
   constexpr int QMAX = NT > 0 ? (NT + 3) / 4 : (kMaxCtaN + 3) / 4;
   constexpr int NC = NT > 0 ? 8 : 4;  // independent FMA chains per re / im (DFMA latency 23 cycles)
-  double2 pr[QMAX];
-#pragma unroll
-  for (int jj = 0; jj < QMAX; ++jj) {
-    const int j = j0 + jj;
-    pr[jj] = (active && jj < Q && j < n) ? ps[size_t(i) * S + j] : make_double2(0.0, 0.0);
-  }
-  const double2* vq = nullptr;
+  double2 pr[QMAX];  // this thread's quarter row of P, register resident for a whole segment
 #pragma unroll 1
-  for (int64_t s = 0; s < steps; ++s) {
-    vq = va + j0;
-    double ar[NC], ai[NC];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) ar[c] = ai[c] = 0.0;
-#pragma unroll
-    for (int jj = 0; jj < QMAX; ++jj) {  // 2 NC independent FMA chains
-      if (NT > 0 || jj < Q) {
-        const double2 a = pr[jj], v = vq[jj];
-        const int c = jj % NC;
-        ar[c] = fma(a.x, v.x, ar[c]);
-        ar[c] = fma(-a.y, v.y, ar[c]);
-        ai[c] = fma(a.x, v.y, ai[c]);
-        ai[c] = fma(a.y, v.x, ai[c]);
-      }
-    }
-#pragma unroll
-    for (int w = 1; w < NC; w *= 2)
-#pragma unroll
-      for (int c = 0; c + w < NC; c += 2 * w) {
-        ar[c] += ar[c + w];
-        ai[c] += ai[c + w];
-      }
-    double re = ar[0], im = ai[0];
-    re += __shfl_xor_sync(0xffffffffu, re, 1);
-    im += __shfl_xor_sync(0xffffffffu, im, 1);
-    re += __shfl_xor_sync(0xffffffffu, re, 2);
-    im += __shfl_xor_sync(0xffffffffu, im, 2);
-    if (active && q == 0) vb[i] = make_double2(re, im);
+  for (int64_t seg = 0; seg < segments; ++seg) {
+    cp_async_wait<0>();
     __syncthreads();
-    double2* t = va;
-    va = vb;
-    vb = t;
+#pragma unroll
+    for (int jj = 0; jj < QMAX; ++jj) {
+      const int j = j0 + jj;
+      pr[jj] = (active && jj < Q && j < n) ? ps[size_t(i) * S + j] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();  // everyone holds its row before the buffer is refilled
+    if (seg + 1 < segments) stage(props + (seg + 1) * size_t(n) * n);
+#pragma unroll 1
+    for (int64_t s = 0; s < sps; ++s) {
+      const double2* vq = va + j0;
+      double ar[NC], ai[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) ar[c] = ai[c] = 0.0;
+#pragma unroll
+      for (int jj = 0; jj < QMAX; ++jj) {  // 2 NC independent FMA chains
+        if (NT > 0 || jj < Q) {
+          const double2 a = pr[jj], v = vq[jj];
+          const int c = jj % NC;
+          ar[c] = fma(a.x, v.x, ar[c]);
+          ar[c] = fma(-a.y, v.y, ar[c]);
+          ai[c] = fma(a.x, v.y, ai[c]);
+          ai[c] = fma(a.y, v.x, ai[c]);
+        }
+      }
+#pragma unroll
+      for (int w = 1; w < NC; w *= 2)
+#pragma unroll
+        for (int c = 0; c + w < NC; c += 2 * w) {
+          ar[c] += ar[c + w];
+          ai[c] += ai[c + w];
+        }
+      double re = ar[0], im = ai[0];
+      re += __shfl_xor_sync(0xffffffffu, re, 1);
+      im += __shfl_xor_sync(0xffffffffu, im, 1);
+      re += __shfl_xor_sync(0xffffffffu, re, 2);
+      im += __shfl_xor_sync(0xffffffffu, im, 2);
+      if (active && q == 0) vb[i] = make_double2(re, im);
+      __syncthreads();
+      double2* t = va;
+      va = vb;
+      vb = t;
+    }
   }
   for (int e = tid; e < n; e += blockDim.x) xb[e] = va[e];
 }
@@ -180,23 +191,35 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 bool cta_chain_supported(size_t n) { return n >= 1 && n <= size_t(kMaxCtaN); }
 
-void launch_cta_chain(const double* p, size_t n, double* x_aos, int64_t batch, int64_t steps, cudaStream_t s) {
-  if (batch <= 0 || steps <= 0) return;
+static void cta_launch(const double* props, size_t n, double* x_aos, int64_t batch, int64_t segments, int64_t sps,
+                       cudaStream_t s) {
   if (!cta_chain_supported(n)) throw invalid_argument("cta chain kernel supports n <= 96");
   const int ni = int(n);
   const int S = ni + ((4 - ni % 8) + 8) % 8;
   const size_t smem = (size_t(ni) * S + 2 * (ni + (kMaxCtaN + 3) / 4)) * sizeof(double2);
-  ensure_max_dyn_smem((const void*)cta_chain_kernel<0>, int(smem));
   const int threads = ((4 * ni + 31) / 32) * 32;
+  const double2* p2 = reinterpret_cast<const double2*>(props);
+  double2* x2 = reinterpret_cast<double2*>(x_aos);
   if (ni == 81) {
     ensure_max_dyn_smem((const void*)cta_chain_kernel<81>, int(smem));
-    cta_chain_kernel<81><<<unsigned(batch), threads, smem, s>>>(reinterpret_cast<const double2*>(p), ni,
-                                                                reinterpret_cast<double2*>(x_aos), steps);
+    cta_chain_kernel<81><<<unsigned(batch), threads, smem, s>>>(p2, ni, x2, segments, sps);
   } else {
-    cta_chain_kernel<0><<<unsigned(batch), threads, smem, s>>>(reinterpret_cast<const double2*>(p), ni,
-                                                               reinterpret_cast<double2*>(x_aos), steps);
+    ensure_max_dyn_smem((const void*)cta_chain_kernel<0>, int(smem));
+    cta_chain_kernel<0><<<unsigned(batch), threads, smem, s>>>(p2, ni, x2, segments, sps);
   }
   LBG_CHECK_LAUNCH("cta_chain_kernel");
+}
+
+void launch_cta_chain(const double* p, size_t n, double* x_aos, int64_t batch, int64_t steps, cudaStream_t s) {
+  if (batch <= 0 || steps <= 0) return;
+  cta_launch(p, n, x_aos, batch, 1, steps, s);
+}
+
+// GRAPE chain of one trajectory over all segments in one launch
+void launch_cta_chain_segments(const double* props, size_t n, int64_t segments, int64_t sps, double* x_aos,
+                               cudaStream_t s) {
+  if (segments <= 0 || sps <= 0) return;
+  cta_launch(props, n, x_aos, 1, segments, sps, s);
 }
 
 // one CTA per SM (at most one per row); each holds ceil(n/grid) rows of P

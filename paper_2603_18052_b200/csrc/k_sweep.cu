@@ -363,6 +363,10 @@ void launch_grape(size_t d, const double* h0, const double* hc, const double* ze
                                    "D2D P");
                       });
   if (ev_build_end) check_cuda(cudaEventRecord(ev_build_end, s), "event");
+  if (cta_chain_supported(n) && !chain_supported(n)) {  // d <= 9: the whole chain in one launch
+    launch_cta_chain_segments(reinterpret_cast<const double*>(props), n, segments, steps_per_segment, x, s);
+    return;
+  }
   for (int64_t j = 0; j < segments; ++j) {
     const double* pj = reinterpret_cast<const double*>(props + j * nn);
     if (chain_supported(n))
