@@ -557,8 +557,7 @@ def density_entry(torch, lbg, R, cfg, peak):
     total, per, launches = R.time_passes(lambda: lbg.evolve_density_dev(pt, xt, S, work, stream=R.stream), 3, 1)
     ms = total / len(per)
     rate = B * S / (ms * 1e-3)
-    packed = d * d > 84  # pairs of real vectors through the complex stepper: 4 d^4 executed flops each
-    executed = rate * (4 if packed else 2) * d ** 4 / 1e12
+    executed = rate * 2 * d ** 4 / 1e12
     # end to end through the host-buffer call lbg_evolve_density (pinned buffers)
     import ctypes as C
     pin = torch.empty(B * d * d * 2, dtype=torch.float64).pin_memory()
@@ -587,7 +586,7 @@ def density_entry(torch, lbg, R, cfg, peak):
                     "call": "lbg_evolve_density (host buffers, synchronous); median of 5"},
             "ms_per_pass": ms, "gpu_launches_per_pass": launches // len(per),
             "kernel": ("dfma9r_kernel" if d * d == 9 else
-                       "tiled_evolve_kernel (packed real pairs)" if packed else "smem_real_kernel"),
+                       "tiled_evolve_kernel<real>" if d * d > 84 else "smem_real_kernel"),
             "roofline": {"bound": "fp64", "executed_tflops": executed, "peak": peak, "unit": "TFLOP/s",
                          "frac": executed / peak},
             "note": "real coordinates of the Hermitian rho (2 d^4 flops per traj-step); the headline "

@@ -120,9 +120,9 @@ int lbg_evolve_shared_p(const double* p, size_t d, const double* rho0, int64_t b
  * H only; LBG_DENSITY_GENERAL always propagates both; LBG_DENSITY_AUTO detects
  * H' != 0 on the device and skips the H' set when it is zero (no host sync).
  * P must preserve Hermiticity (every Lindblad propagator does). Any d: up to
- * d*d = 84 on real-arithmetic kernels (n^2 FMAs per step), beyond through the
- * complex steppers with two real vectors packed per complex one (2 n^2; AUTO
- * reads the device flag there, one 4-byte sync). P: n x n AoS (device), rho: batch x d x d AoS
+ * d*d = 84 on the real register / shared-memory kernels, beyond on the real
+ * variant of the K1c tile engine (n^2 FMAs per step everywhere; AUTO reads the
+ * device flag there, one 4-byte sync). P: n x n AoS (device), rho: batch x d x d AoS
  * (device, in place), work: lbg_density_workspace(d*d, batch) bytes.
  * ------------------------------------------------------------------------ */
 #define LBG_DENSITY_HERMITIAN 0

@@ -59,6 +59,10 @@ std::size_t tiled_workspace(std::size_t n, int64_t batch);
 void launch_tiled_evolve(const double* p_dev, std::size_t n, double* x_re, double* x_im,
                          double* x_aos, int64_t batch, int64_t steps, Layout layout, void* work,
                          cudaStream_t s);
+// K1c-R — the same engine on real matrices (density mode beyond n = 84)
+std::size_t tiled_real_workspace(std::size_t n, int64_t batch);
+void launch_tiled_evolve_real(const double* p_dev, std::size_t n, double* x, int64_t batch, int64_t steps,
+                              void* work, cudaStream_t s);
 // K2b / K2c — latency kernels for one or a few trajectories (k_single.cu)
 bool cta_chain_supported(std::size_t n);
 void launch_cta_chain(const double* p, std::size_t n, double* x_aos, int64_t batch, int64_t steps,

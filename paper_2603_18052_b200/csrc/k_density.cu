@@ -15,8 +15,8 @@
 // one. A step is n^2 real FMAs instead of 4 n^2 (8 d^4 -> 2 d^4 flops).
 //
 // Kernels: K1a-R `dfma9r_kernel` (n = 9: P_R in the constant bank, 81 DFMA per
-// trajectory-step, one trajectory per thread), for n > 84 real vectors packed
-// in pairs through the complex steppers (below), and K1b-R `smem_real_kernel`
+// trajectory-step, one trajectory per thread), for n > 84 the real-arithmetic
+// variant of the K1c tile engine (k_tiled.cu), and K1b-R `smem_real_kernel`
 // (n <= 84: P_R resident in shared memory, real m8n8k4 DMMA, 32 vectors/CTA,
 // 8 warps balanced over the 4 SMSPs).
 #include <map>
@@ -103,51 +103,6 @@ __global__ void real_to_rho_kernel(const double* __restrict__ x, const double* _
     r.y += a.x;
   }
   rho[e] = r;
-}
-
-// ---- n > 84: real vectors packed in pairs into complex ones ---------------------
-// z_j = x_{2j} + i x_{2j+1} and P_R stored as a complex matrix with zero
-// imaginary part: P_R z_j = P_R x_{2j} + i P_R x_{2j+1} exactly, so the complex
-// steppers (K1c / K2c) propagate two real vectors per complex one (half the
-// flops of the complex path; the products with the zero imaginary part are
-// exact zeros).
-__global__ void p_to_real_c_kernel(const double2* __restrict__ p, int d, double2* __restrict__ prc) {
-  const int n = d * d;
-  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (e >= (long long)n * n) return;
-  const int q = int(e / n), s = int(e - (long long)q * n);
-  const int si = s / d, sj = s - si * d;
-  double2 c;
-  if (si == sj) {
-    c = p[e];
-  } else {
-    const double2 a = p[e], bt = p[(long long)q * n + sj * d + si];
-    c = si < sj ? make_double2(a.x + bt.x, a.y + bt.y) : make_double2(a.y - bt.y, bt.x - a.x);
-  }
-  const int qi = q / d, qj = q - qi * d;
-  prc[e] = make_double2(real_coord(c, qi, qj), 0.0);
-}
-
-__global__ void pack_pairs_kernel(const double* __restrict__ x, long long nvec, int n, double2* __restrict__ z) {
-  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const long long pairs = (nvec + 1) / 2;
-  if (e >= pairs * n) return;
-  const long long j = e / n;
-  const int k = int(e - j * n);
-  const double a = x[(2 * j) * n + k];
-  const double b = 2 * j + 1 < nvec ? x[(2 * j + 1) * n + k] : 0.0;
-  z[e] = make_double2(a, b);
-}
-
-__global__ void unpack_pairs_kernel(const double2* __restrict__ z, long long nvec, int n, double* __restrict__ x) {
-  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const long long pairs = (nvec + 1) / 2;
-  if (e >= pairs * n) return;
-  const long long j = e / n;
-  const int k = int(e - j * n);
-  const double2 v = z[e];
-  x[(2 * j) * n + k] = v.x;
-  if (2 * j + 1 < nvec) x[(2 * j + 1) * n + k] = v.y;
 }
 
 // ---- K1a-R: n = 9 --------------------------------------------------------------
@@ -343,16 +298,15 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 }  // namespace
 
-constexpr size_t kDirectMaxN = 84;  // real kernels (K1a-R / K1b-R) up to here, packed pairs beyond
+constexpr size_t kDirectMaxN = 84;  // K1a-R / K1b-R up to here, the real K1c tile engine beyond
 
 bool density_supported(size_t n) { return n >= 1; }
 
 size_t density_workspace(size_t n, int64_t batch) {
   const size_t base = align_up(n * n * 8) + align_up(2 * size_t(batch) * n * 8) + 256;
   if (n <= kDirectMaxN) return base;
-  // + P_R as complex, the packed pairs (2 batch vectors at most -> batch pairs), the stepper's workspace
-  return base + align_up(n * n * 16) + align_up(size_t(batch) * n * 16) +
-         align_up(lbg_evolve_workspace(n, batch, LBG_ALGO_AUTO));
+  // + the real tile engine's workspace for up to 2 batch vectors
+  return base + align_up(tiled_real_workspace(n, 2 * batch));
 }
 
 // x: count real vectors of length n (in place)
@@ -400,7 +354,7 @@ void launch_density(const double* p, size_t d, double* rho, int64_t batch, int64
   if (!density_supported(n)) throw invalid_argument("density mode: empty state");
   if (mode < kDensityHermitian || mode > kDensityAuto) throw invalid_argument("density: unknown mode");
   if (batch <= 0) return;
-  const bool packed_auto = n > kDirectMaxN && mode == kDensityAuto;  // decided after one flag read (below)
+  const bool tiled_auto = n > kDirectMaxN && mode == kDensityAuto;  // decided after one flag read (below)
   char* w = static_cast<char*>(work);
   double* pr = reinterpret_cast<double*>(w);
   double* x = reinterpret_cast<double*>(w + align_up(n * n * 8));
@@ -410,10 +364,8 @@ void launch_density(const double* p, size_t d, double* rho, int64_t batch, int64
   int* live = mode == kDensityAuto ? flag : nullptr;
   if (live) check_cuda(cudaMemsetAsync(live, 0, sizeof(int), s), "memset flag");
   const long long nn = (long long)n * n, ne = (long long)batch * n;
-  if (n <= kDirectMaxN) {
-    p_to_real_kernel<<<unsigned((nn + 255) / 256), 256, 0, s>>>(reinterpret_cast<const double2*>(p), int(d), pr);
-    LBG_CHECK_LAUNCH("p_to_real_kernel");
-  }
+  p_to_real_kernel<<<unsigned((nn + 255) / 256), 256, 0, s>>>(reinterpret_cast<const double2*>(p), int(d), pr);
+  LBG_CHECK_LAUNCH("p_to_real_kernel");
   rho_to_real_kernel<<<unsigned((ne + 255) / 256), 256, 0, s>>>(reinterpret_cast<const double2*>(rho), int(d),
                                                                 batch, x, general ? xa : nullptr, live);
   LBG_CHECK_LAUNCH("rho_to_real_kernel");
@@ -423,24 +375,15 @@ void launch_density(const double* p, size_t d, double* rho, int64_t batch, int64
     step_real(pr, n, x, general ? 2 * batch : batch, batch, live, steps, s);
   } else {
     bool gen = general;
-    if (packed_auto) {  // the complex steppers cannot skip on a device flag: read it (one 4-byte sync)
+    if (tiled_auto) {  // read the flag (one 4-byte sync): the tile engine takes its vector count from the host
       int h = 0;
       check_cuda(cudaMemcpyAsync(&h, live, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H flag");
       check_cuda(cudaStreamSynchronize(s), "sync flag");
       gen = h != 0;
     }
-    char* w2 = w + align_up(n * n * 8) + align_up(2 * size_t(batch) * n * 8) + 256;
-    double2* prc = reinterpret_cast<double2*>(w2);
-    double2* z = reinterpret_cast<double2*>(w2 + align_up(n * n * 16));
-    void* inner = w2 + align_up(n * n * 16) + align_up(size_t(batch) * n * 16);
-    const long long nvec = gen ? 2 * batch : batch, pairs = (nvec + 1) / 2;
-    p_to_real_c_kernel<<<unsigned((nn + 255) / 256), 256, 0, s>>>(reinterpret_cast<const double2*>(p), int(d), prc);
-    LBG_CHECK_LAUNCH("p_to_real_c_kernel");
-    pack_pairs_kernel<<<unsigned((pairs * n + 255) / 256), 256, 0, s>>>(x, nvec, int(n), z);
-    LBG_CHECK_LAUNCH("pack_pairs_kernel");
-    evolve_dev_aos(reinterpret_cast<const double*>(prc), n, reinterpret_cast<double*>(z), pairs, steps, inner, s);
-    unpack_pairs_kernel<<<unsigned((pairs * n + 255) / 256), 256, 0, s>>>(z, nvec, int(n), x);
-    LBG_CHECK_LAUNCH("unpack_pairs_kernel");
+    void* inner = w + align_up(n * n * 8) + align_up(2 * size_t(batch) * n * 8) + 256;
+    const int64_t nvec = gen ? 2 * batch : batch;
+    launch_tiled_evolve_real(pr, n, x, nvec, steps, inner, s);  // K1c on real arithmetic
   }
   real_to_rho_kernel<<<unsigned((ne + 255) / 256), 256, 0, s>>>(x, general ? xa : nullptr, int(d), batch,
                                                                 reinterpret_cast<double2*>(rho), live);

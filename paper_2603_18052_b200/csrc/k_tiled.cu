@@ -48,14 +48,24 @@ constexpr int A_ELEMS = BM * SA;
 // the stepper (twice the tiles per step -> half the step-tail granularity).
 // Each consumer warp owns MI m8-tiles x NI n8-tiles; the 8 warps form a
 // WM x WN grid. SB = BN + 4 = 4 (mod 8) keeps B fragment loads conflict free.
-template <int BN_>
+// REAL: the same engine on real matrices (density mode beyond n = 84): 64-row
+// x BN tiles, K chunk 32, A stride 36 = 4 (mod 16) and B stride BN + 8 =
+// 8 (mod 16) doubles (conflict-free m8n8k4 fragments), the same byte size per
+// stage as the complex geometry.
+template <int BN_, bool REAL_ = false, int BK_ = BK>
 struct Geo {
-  static constexpr int BN = BN_, NI = 2, WN = BN_ / (8 * NI), WM = CWARPS / WN, MI = (BM / 4) / WM;
-  static constexpr int SB = BN_ + 4;
-  static constexpr int B_ELEMS = BK * SB;
-  static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;  // double2 units
+  static constexpr bool REAL = REAL_;
+  static constexpr int CPX = REAL ? 1 : 2;         // doubles per element
+  static constexpr int BMg = REAL ? 64 : BM;       // rows per tile
+  static constexpr int BKg = BK_;                  // K chunk (elements)
+  static constexpr int SAg = REAL ? BKg + 4 : SA;  // A row stride (elements)
+  static constexpr int BN = BN_, NI = 2, WN = BN_ / (8 * NI), WM = CWARPS / WN;
+  static constexpr int MI = (REAL ? BMg / 8 : BMg / 4) / WM;
+  static constexpr int SB = REAL ? BN_ + 8 : BN_ + 4;  // B row stride (elements)
+  static constexpr int A_ELEMS = BMg * SAg * CPX / 2, B_ELEMS = BKg * SB * CPX / 2;  // double2 units
+  static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
   static constexpr size_t kSmemBytes = size_t(STAGES) * STAGE_ELEMS * sizeof(double2) + 256;
-  static_assert(WN * WM == CWARPS && MI * WM * 4 == BM, "tile geometry");
+  static_assert(WN * WM == CWARPS && MI * WM * (REAL ? 8 : 4) == BMg, "tile geometry");
 };
 
 // ---- mbarrier / bulk-copy primitives (PTX) ----------------------------------
@@ -159,10 +169,11 @@ __device__ __forceinline__ void produce_range_tma(const Ring& r, const Problem& 
                                                   int a_row0 = 0, int b_row0 = 0) {
   constexpr int BN = G::BN, STAGE_ELEMS = G::STAGE_ELEMS;
   constexpr unsigned kBytes = unsigned(STAGE_ELEMS) * 16u;  // full boxes, OOB fill included
+  constexpr int BK = G::BKg;
   const int nk = (p.K + BK - 1) / BK;
   for (long long it = it0; it < it1; ++it) {
     const int t = int(it / nk), kc = int(it - (long long)t * nk);
-    const int m0 = (t % tiles_m) * BM, n0 = (t / tiles_m) * BN;
+    const int m0 = (t % tiles_m) * G::BMg, n0 = (t / tiles_m) * BN;
     const long long tb = (long long)t * nk;
     const int lo = int(max(it0 - tb, 0ll)), hi = int(min(it1 - 1 - tb, (long long)nk - 1));
     mbar_wait(&r.empty[stage], phase ^ 1u);
@@ -173,8 +184,8 @@ __device__ __forceinline__ void produce_range_tma(const Ring& r, const Problem& 
       r.hdr[4 * stage + 2] = lo;
       r.hdr[4 * stage + 3] = hi;
       mbar_arrive_tx(&r.full[stage], kBytes);
-      tma_g2s_2d(as, map_a, 2 * kc * BK, a_row0 + m0, &r.full[stage]);
-      tma_g2s_2d(as + A_ELEMS, map_b, 2 * n0, b_row0 + kc * BK, &r.full[stage]);
+      tma_g2s_2d(as, map_a, G::CPX * kc * BK, a_row0 + m0, &r.full[stage]);
+      tma_g2s_2d(as + G::A_ELEMS, map_b, G::CPX * n0, b_row0 + kc * BK, &r.full[stage]);
     }
     __syncwarp();
     advance(stage, phase);
@@ -207,11 +218,16 @@ template <class G>
 __device__ __forceinline__ void consume(const Ring& r, const Problem& p, int tiles_m, int& stage,
                                        unsigned& phase, int warp, int lane, const SplitK* sk) {
   constexpr int BN = G::BN, SB = G::SB, STAGE_ELEMS = G::STAGE_ELEMS, MI = G::MI, NI = G::NI;
+  constexpr int BK = G::BKg;
   const AFragLane af(lane);
   const int wm = warp / G::WN, wn = warp % G::WN;
   const int nk = (p.K + BK - 1) / BK;
-  const int a_off = 2 * ((wm * MI * 4 + af.di) * SA + af.dj) + af.comp;
-  const int b_off = 2 * (((lane & 3) >> 1) * SB + wn * NI * 8 + (lane >> 2)) + (lane & 1);
+  const int gq = lane >> 2, tq = lane & 3;
+  // fragment bases in doubles: complex real-form (common.cuh) or plain real
+  const int a_off = G::REAL ? (wm * MI * 8 + gq) * G::SAg + tq
+                            : 2 * ((wm * MI * 4 + af.di) * SA + af.dj) + af.comp;
+  const int b_off = G::REAL ? tq * SB + wn * NI * 8 + gq
+                            : 2 * (((lane & 3) >> 1) * SB + wn * NI * 8 + (lane >> 2)) + (lane & 1);
   double acc[MI][NI][2] = {};
   bool row_ok[MI];
 #pragma unroll
@@ -228,17 +244,17 @@ __device__ __forceinline__ void consume(const Ring& r, const Problem& p, int til
       return;
     }
     if (kc == lo) {
-      m0 = (tile % tiles_m) * BM;
+      m0 = (tile % tiles_m) * G::BMg;
       n0 = (tile / tiles_m) * BN;
 #pragma unroll
       for (int mi = 0; mi < MI; ++mi) {
-        row_ok[mi] = m0 + (wm * MI + mi) * 4 + af.di < p.M;
+        row_ok[mi] = G::REAL ? m0 + (wm * MI + mi) * 8 + gq < p.M : m0 + (wm * MI + mi) * 4 + af.di < p.M;
 #pragma unroll
         for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
       }
     }
     const double* ad = reinterpret_cast<const double*>(r.data + stage * STAGE_ELEMS) + a_off;
-    const double* bd = reinterpret_cast<const double*>(r.data + stage * STAGE_ELEMS + A_ELEMS) + b_off;
+    const double* bd = reinterpret_cast<const double*>(r.data + stage * STAGE_ELEMS + G::A_ELEMS) + b_off;
     const int k0 = kc * BK;
     bool all_rows = true;
 #pragma unroll
@@ -246,7 +262,22 @@ __device__ __forceinline__ void consume(const Ring& r, const Problem& p, int til
     // row_ok depends on the lane's fragment row: the path choice must be
     // warp-uniform, mma.sync needs all 32 lanes converged
     all_rows = __all_sync(0xffffffffu, all_rows);
-    if (k0 + BK <= p.K && all_rows) {
+    if constexpr (G::REAL) {
+      // rows >= M and k >= K arrive zero-filled by the TMA: no masking needed
+      (void)all_rows;
+#pragma unroll
+      for (int ks = 0; ks < BK / 4; ++ks) {
+        double a[MI], b[NI];
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi) a[mi] = ad[mi * 8 * G::SAg + 4 * ks];
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) b[ni] = bd[4 * ks * SB + ni * 8];
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+      }
+    } else if (k0 + BK <= p.K && all_rows) {
 #pragma unroll
       for (int ks = 0; ks < BK / 2; ++ks) {
         double a[MI], b[NI];
@@ -314,7 +345,20 @@ __device__ __forceinline__ void consume(const Ring& r, const Problem& p, int til
           acc[mi][ni][1] += q.y;
         }
     }
-    {  // tile done: registers -> global
+    if constexpr (G::REAL) {  // tile done: registers -> global (row g, columns 2t, 2t+1)
+      double* C = reinterpret_cast<double*>(p.C);
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) {
+          const int i = m0 + (wm * MI + mi) * 8 + gq;
+          const int col = n0 + (wn * NI + ni) * 8 + 2 * tq;
+          if (i < p.M) {
+            if (col < p.N) C[(long long)i * p.ldc + col] = acc[mi][ni][0];
+            if (col + 1 < p.N) C[(long long)i * p.ldc + col + 1] = acc[mi][ni][1];
+          }
+        }
+    } else {  // tile done: registers -> global
 #pragma unroll
       for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
@@ -375,6 +419,7 @@ __global__ void __launch_bounds__(THREADS) zgemm_kernel(const double2* __restric
 // 32-wide tiles: 16-wide halves the step-tail granularity but doubles the
 // row copies per MMA and measured 2x slower at config 3 (copy-issue bound).
 using StepGeo = Geo<32>;
+using StepGeoR = Geo<32, true, 64>;  // real arithmetic (density mode); measured: <64,true,32> 11.2, <64,true,64> 8.34, this 8.32 ms at c3
 struct StepCtl {
   unsigned int tile_ctr[2];
   unsigned int barrier;
@@ -397,21 +442,21 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int tar
   __syncthreads();
 }
 
+template <class G>
 __global__ void __launch_bounds__(THREADS) tiled_evolve_kernel(const double2* __restrict__ P, int n,
                                                                double2* v0, double2* v1,
-                                                               int batch, int64_t steps,
+                                                               int batch, int ldv, int64_t steps,
                                                                StepCtl* ctl, double2* part,
                                                                unsigned int* flags,
                                                                const __grid_constant__ CUtensorMap map_p,
                                                                const __grid_constant__ CUtensorMap map_v0,
                                                                const __grid_constant__ CUtensorMap map_v1) {
-  using G = StepGeo;
   constexpr int BN = G::BN;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const Ring r = carve<G>(smem_raw);
   init_ring(r);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tiles_m = (n + BM - 1) / BM, tiles_n = (batch + BN - 1) / BN;
+  const int tiles_m = (n + G::BMg - 1) / G::BMg, tiles_n = (batch + BN - 1) / BN;
   const int ntiles = tiles_m * tiles_n;
   double2* cur = v0;
   double2* nxt = v1;
@@ -420,10 +465,10 @@ __global__ void __launch_bounds__(THREADS) tiled_evolve_kernel(const double2* __
   // stream-K: this CTA's fixed, contiguous share of the step's (tile, K chunk)
   // iterations; grid <= ntiles keeps every range >= one tile, so a tile is
   // split across at most two CTAs
-  const long long nk = (n + BK - 1) / BK, work = (long long)ntiles * nk;
+  const long long nk = (n + G::BKg - 1) / G::BKg, work = (long long)ntiles * nk;
   const long long it0 = work * blockIdx.x / gridDim.x, it1 = work * (blockIdx.x + 1) / gridDim.x;
   for (int64_t s = 0; s < steps; ++s) {
-    const Problem p{P, n, cur, batch, nxt, batch, n, batch, n};
+    const Problem p{P, n, cur, ldv, nxt, ldv, n, batch, n};
     if (warp == CWARPS) {
       // generic-proxy stores of the previous step -> async-proxy (bulk copy) reads
       asm volatile("fence.proxy.async.global;\n" ::: "memory");
@@ -541,15 +586,117 @@ int sm_count() {
   return c;
 }
 
-size_t tiled_ntiles(size_t n, int64_t batch) {
-  return ((n + BM - 1) / BM) * ((size_t(batch) + StepGeo::BN - 1) / StepGeo::BN);
+template <class G>
+size_t ntiles_of(size_t n, int64_t batch) {
+  return ((n + G::BMg - 1) / G::BMg) * ((size_t(batch) + G::BN - 1) / G::BN);
 }
-constexpr size_t kSlot = size_t(CWARPS) * 32 * StepGeo::MI * StepGeo::NI;  // double2 per split tile
+template <class G>
+constexpr size_t slot_of() {  // double2 per split tile
+  return size_t(CWARPS) * 32 * G::MI * G::NI;
+}
+// real rows must be 16-byte aligned for the TMA: even leading dimensions
+inline size_t even(size_t x) { return x + (x & 1); }
+template <class G>
+size_t ldv_of(int64_t batch) {
+  return G::REAL ? even(size_t(batch)) : size_t(batch);
+}
+template <class G>
+size_t workspace_of(size_t n, int64_t batch) {
+  const size_t nt = ntiles_of<G>(n, batch);
+  const size_t vbytes = size_t(G::CPX) * 8 * n * ldv_of<G>(batch);
+  return 2 * align_up(vbytes) + align_up(sizeof(StepCtl)) + align_up(nt * slot_of<G>() * sizeof(double2)) +
+         align_up(nt * sizeof(unsigned int));
+}
 
-size_t tiled_workspace(size_t n, int64_t batch) {
-  const size_t nt = tiled_ntiles(n, batch);
-  return 2 * align_up(sizeof(double2) * n * size_t(batch)) + align_up(sizeof(StepCtl)) +
-         align_up(nt * kSlot * sizeof(double2)) + align_up(nt * sizeof(unsigned int));
+size_t tiled_workspace(size_t n, int64_t batch) { return workspace_of<StepGeo>(n, batch); }
+size_t tiled_real_workspace(size_t n, int64_t batch) {
+  return workspace_of<StepGeoR>(n, batch) + align_up(8 * n * even(n));  // + an even-stride copy of P_R
+}
+
+// rows x cols real row-major matrix with leading dimension ld (even); box box_rows x box_cols
+CUtensorMap real_map(const double* base, size_t rows, size_t cols, size_t ld, unsigned box_rows, unsigned box_cols) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+  const cuuint64_t strides[1] = {cuuint64_t(ld * sizeof(double))};
+  const cuuint32_t box[2] = {cuuint32_t(box_cols), cuuint32_t(box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult rc = encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims,
+                                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (rc != CUDA_SUCCESS) throw cuda_error("cuTensorMapEncodeTiled failed (" + std::to_string(int(rc)) + ")");
+  return m;
+}
+
+// real state layout conversion: x[b][k] (batch x n) <-> V[k][b]
+template <bool ToV>
+__global__ void convert_real_kernel(double* __restrict__ x, double* __restrict__ v, int n, int batch, int ldv) {
+  __shared__ double tile[32][33];
+  const int kb = blockIdx.x * 32, bb = blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  if (ToV) {
+    for (int r = ty; r < 32; r += 8) {
+      const int b = bb + r, k = kb + tx;
+      tile[r][tx] = (b < batch && k < n) ? x[(long long)b * n + k] : 0.0;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+      const int k = kb + r, b = bb + tx;
+      if (k < n && b < batch) v[(long long)k * ldv + b] = tile[tx][r];
+    }
+  } else {
+    for (int r = ty; r < 32; r += 8) {
+      const int k = kb + r, b = bb + tx;
+      tile[r][tx] = (k < n && b < batch) ? v[(long long)k * ldv + b] : 0.0;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+      const int b = bb + r, k = kb + tx;
+      if (b < batch && k < n) x[(long long)b * n + k] = tile[tx][r];
+    }
+  }
+}
+
+// persistent cooperative stepping for geometry G; v0 already holds V[k][b]
+template <class G>
+void run_tiled(const double* p_dev, size_t ldp, size_t n, int64_t batch, int64_t steps, void* work, cudaStream_t s) {
+  char* w = static_cast<char*>(work);
+  const size_t ldv = ldv_of<G>(batch);
+  const size_t vbytes = size_t(G::CPX) * 8 * n * ldv;
+  double2* v0 = reinterpret_cast<double2*>(w);
+  double2* v1 = reinterpret_cast<double2*>(w + align_up(vbytes));
+  StepCtl* ctl = reinterpret_cast<StepCtl*>(w + 2 * align_up(vbytes));
+  const size_t nt = ntiles_of<G>(n, batch);
+  double2* part = reinterpret_cast<double2*>(reinterpret_cast<char*>(ctl) + align_up(sizeof(StepCtl)));
+  unsigned int* flags =
+      reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(part) + align_up(nt * slot_of<G>() * sizeof(double2)));
+  check_cuda(cudaMemsetAsync(flags, 0, nt * sizeof(unsigned int), s), "memset flags");
+  check_cuda(cudaMemsetAsync(ctl, 0, sizeof(StepCtl), s), "memset ctl");
+  if (steps <= 0) return;
+  const auto kern = tiled_evolve_kernel<G>;
+  ensure_max_dyn_smem((const void*)kern, int(G::kSmemBytes));
+  int occ = 0;
+  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, THREADS, G::kSmemBytes), "occupancy");
+  int grid = std::min<int>(occ * sm_count(), int(nt));
+  if (grid < 1) grid = 1;
+  const double2* p2 = reinterpret_cast<const double2*>(p_dev);
+  int ni = int(n), bi = int(batch), li = int(ldv);
+  int64_t st = steps;
+  // A = P (n x n), B = the state V[k][b] (n x batch); boxes BMg x SAg and BK x SB elements
+  CUtensorMap map_p, map_v0, map_v1;
+  if constexpr (G::REAL) {
+    map_p = real_map(p_dev, n, n, ldp, G::BMg, G::SAg);
+    map_v0 = real_map(reinterpret_cast<const double*>(v0), n, size_t(batch), ldv, G::BKg, G::SB);
+    map_v1 = real_map(reinterpret_cast<const double*>(v1), n, size_t(batch), ldv, G::BKg, G::SB);
+  } else {
+    map_p = complex_map(p2, n, n, BM, SA);
+    map_v0 = complex_map(v0, n, size_t(batch), BK, G::SB);
+    map_v1 = complex_map(v1, n, size_t(batch), BK, G::SB);
+  }
+  void* args[] = {(void*)&p2, (void*)&ni, (void*)&v0, (void*)&v1, (void*)&bi, (void*)&li, (void*)&st,
+                  (void*)&ctl, (void*)&part, (void*)&flags, (void*)&map_p, (void*)&map_v0, (void*)&map_v1};
+  check_cuda(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(THREADS), args, G::kSmemBytes, s),
+             "tiled_evolve_kernel (cooperative)");
+  note_launch();
 }
 
 void launch_tiled_evolve(const double* p_dev, size_t n, double* x_re, double* x_im, double* x_aos,
@@ -557,41 +704,37 @@ void launch_tiled_evolve(const double* p_dev, size_t n, double* x_re, double* x_
   if (batch <= 0) return;
   if (batch > (1ll << 30) || n > (1u << 20)) throw invalid_argument("tiled: shape too large");
   if (!work) throw invalid_argument("tiled: workspace required");
-  char* w = static_cast<char*>(work);
-  double2* v0 = reinterpret_cast<double2*>(w);
-  double2* v1 = reinterpret_cast<double2*>(w + align_up(sizeof(double2) * n * size_t(batch)));
-  StepCtl* ctl = reinterpret_cast<StepCtl*>(w + 2 * align_up(sizeof(double2) * n * size_t(batch)));
-  const size_t nt = tiled_ntiles(n, batch);
-  double2* part = reinterpret_cast<double2*>(reinterpret_cast<char*>(ctl) + align_up(sizeof(StepCtl)));
-  unsigned int* flags =
-      reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(part) + align_up(nt * kSlot * sizeof(double2)));
-  check_cuda(cudaMemsetAsync(flags, 0, nt * sizeof(unsigned int), s), "memset flags");
+  double2* v0 = reinterpret_cast<double2*>(work);
+  double2* v1 = reinterpret_cast<double2*>(static_cast<char*>(work) + align_up(sizeof(double2) * n * size_t(batch)));
   const int ni = int(n), bi = int(batch);
   convert<true>(x_re, x_im, x_aos, v0, ni, bi, layout, s);
-  check_cuda(cudaMemsetAsync(ctl, 0, sizeof(StepCtl), s), "memset ctl");
-
-  ensure_max_dyn_smem((const void*)tiled_evolve_kernel, int(StepGeo::kSmemBytes));
-  int occ = 0;
-  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tiled_evolve_kernel, THREADS, StepGeo::kSmemBytes),
-             "occupancy");
-  const int ntiles = ((ni + BM - 1) / BM) * ((bi + StepGeo::BN - 1) / StepGeo::BN);
-  int grid = std::min(occ * sm_count(), ntiles);
-  if (grid < 1) grid = 1;
-  const double2* p2 = reinterpret_cast<const double2*>(p_dev);
-  int64_t st = steps;
-  // A = P (n x n), B = the state V[k][b] (n x batch); boxes of BM x SA and BK x SB complex
-  CUtensorMap map_p = complex_map(p2, n, n, BM, SA);
-  CUtensorMap map_v0 = complex_map(v0, n, size_t(batch), BK, StepGeo::SB);
-  CUtensorMap map_v1 = complex_map(v1, n, size_t(batch), BK, StepGeo::SB);
-  void* args[] = {(void*)&p2, (void*)&ni, (void*)&v0, (void*)&v1, (void*)&bi, (void*)&st, (void*)&ctl,
-                  (void*)&part, (void*)&flags, (void*)&map_p, (void*)&map_v0, (void*)&map_v1};
-  if (steps > 0) {
-    check_cuda(cudaLaunchCooperativeKernel((const void*)tiled_evolve_kernel, dim3(grid), dim3(THREADS),
-                                           args, StepGeo::kSmemBytes, s),
-               "tiled_evolve_kernel (cooperative)");
-    note_launch();
-  }
+  run_tiled<StepGeo>(p_dev, n, n, batch, steps, work, s);
   convert<false>(x_re, x_im, x_aos, (steps & 1) ? v1 : v0, ni, bi, layout, s);
+}
+
+// real: x (batch x n real, [b][k]) stepped in place by the real n x n P_R
+void launch_tiled_evolve_real(const double* p_dev, size_t n, double* x, int64_t batch, int64_t steps, void* work,
+                              cudaStream_t s) {
+  if (batch <= 0) return;
+  if (batch > (1ll << 30) || n > (1u << 20)) throw invalid_argument("tiled: shape too large");
+  if (!work) throw invalid_argument("tiled: workspace required");
+  const size_t ldv = ldv_of<StepGeoR>(batch), ldp = even(n);
+  double* v0 = static_cast<double*>(work);
+  double* v1 = reinterpret_cast<double*>(static_cast<char*>(work) + align_up(8 * n * ldv));
+  const double* pt = p_dev;
+  if (ldp != n) {  // odd n: an even-stride copy of P_R (TMA rows are 16-byte aligned)
+    double* pp = reinterpret_cast<double*>(static_cast<char*>(work) + workspace_of<StepGeoR>(n, batch));
+    check_cuda(cudaMemsetAsync(pp, 0, 8 * n * ldp, s), "memset");
+    check_cuda(cudaMemcpy2DAsync(pp, ldp * 8, p_dev, n * 8, n * 8, n, cudaMemcpyDeviceToDevice, s), "P_R copy");
+    pt = pp;
+  }
+  const int ni = int(n), bi = int(batch), li = int(ldv);
+  const dim3 grid((ni + 31) / 32, (bi + 31) / 32), block(32, 8);
+  convert_real_kernel<true><<<grid, block, 0, s>>>(x, v0, ni, bi, li);
+  LBG_CHECK_LAUNCH("convert_real_kernel");
+  run_tiled<StepGeoR>(pt, ldp, n, batch, steps, work, s);
+  convert_real_kernel<false><<<grid, block, 0, s>>>(x, (steps & 1) ? v1 : v0, ni, bi, li);
+  LBG_CHECK_LAUNCH("convert_real_kernel");
 }
 
 void launch_zgemm(const double* a, const double* b, double* c, int n, int batch, long long stride_a,

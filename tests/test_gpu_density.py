@@ -139,8 +139,8 @@ def test_density_host_api_pipelined_full_size(lbg, oracle):
 
 
 @pytest.mark.parametrize("d,B", [(10, 7), (11, 40), (27, 6)])
-def test_density_packed_path_matches_complex(lbg, torch, oracle, d, B):
-    """n > 84: pairs of real vectors through the complex steppers"""
+def test_density_real_tile_engine_matches_complex(lbg, torch, oracle, d, B):
+    """n > 84: the real-arithmetic K1c tile engine (odd n: even-stride copy of P_R)"""
     rng = np.random.default_rng(d)
     n = d * d
     if d == 27:
