@@ -66,6 +66,7 @@ struct Geo {
   static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
   static constexpr size_t kSmemBytes = size_t(STAGES) * STAGE_ELEMS * sizeof(double2) + 256;
   static_assert(WN * WM == CWARPS && MI * WM * (REAL ? 8 : 4) == BMg, "tile geometry");
+  static_assert(REAL || BK_ == BK, "complex tiles use the global K chunk (SA and the B box follow BK)");
 };
 
 // ---- mbarrier / bulk-copy primitives (PTX) ----------------------------------
