@@ -530,6 +530,7 @@ def extra_configs(torch, lbg, R, peak):
                 msc = total / len(per)
                 entry["complex_mode"] = {"value": B * S / (msc * 1e-3), "ms_per_pass": msc,
                                          "note": "reference-form complex d^2 x d^2 matrices (k_sweep.cu)"}
+            entry["cpu_reference"] = cpu_reference_entry(cfg, rate)
             out[f"c{cfg}"] = entry
         except Exception as e:  # noqa: BLE001
             out[f"c{cfg}"] = {"error": str(e)}
@@ -543,6 +544,33 @@ def extra_configs(torch, lbg, R, peak):
         out["propagator_build"] = expm_table(torch, lbg, R)
     except Exception as e:  # noqa: BLE001
         out["propagator_build"] = {"error": str(e)}
+    return out
+
+
+EXTRA_REF_SAMPLE = {0: 1, 2: 4096, 3: 128, 4: 512}
+
+
+def cpu_reference_entry(cfg, gpu_rate):
+    """The reference (lb::evolve native-fast SoA; c4 with make_model +
+    build_lindbladian + expm per trajectory) on the box's host threads, beside
+    each extra config; c4 also reports build and steps apart."""
+    threads = os.cpu_count() or 1
+    sample = EXTRA_REF_SAMPLE[cfg]
+    try:
+        value, times = cpu_reference_rate(cfg, sample, threads, reps=1, warmup=0)
+    except Exception as e:  # noqa: BLE001
+        return {"unavailable": str(e)}
+    d, _, S = CONFIGS[cfg]
+    out = {"value": value, "unit": "traj-steps/s", "cores": threads, "kind": "reference",
+           "sample": f"{sample} trajectories x {S} steps, {threads} std::threads, {times[0]:.2f} s",
+           "gpu_over_cpu": gpu_rate / value}
+    if cfg == 4:
+        from oracle.bindings import Oracle, Reference
+        o, r = Oracle(), Reference()
+        dl = np.array([o.sweep_params(42, b)[0] for b in range(sample)])
+        sc = np.array([o.sweep_params(42, b)[1] for b in range(sample)])
+        _, _, build_s = r.sweep_batch(dl, sc, steps=0, threads=threads)
+        out["build_s"], out["steps_s"] = build_s, max(times[0] - build_s, 0.0)
     return out
 
 
