@@ -652,9 +652,16 @@ int lbg_grape_chain(size_t d, const double* h0, const double* hc, const double* 
     if (!(chk[0] <= 1e-8 && chk[1] <= 1e-8 && chk[2] >= -1e-8))
       throw invalid_argument("evolve: initial state fails physical-state checks");
     const size_t dd = d * d;
+    // the real transfer-matrix form needs an exactly Hermitian rho0 (k_grape_real.cu)
+    bool real = grape_real_supported(d);
+    for (size_t i = 0; real && i < d; ++i)
+      for (size_t j = 0; j < d; ++j)
+        real = real && rho0[2 * (i * d + j)] == rho0[2 * (j * d + i)] &&
+               rho0[2 * (i * d + j) + 1] == -rho0[2 * (j * d + i) + 1];
     std::vector<double> zeros(size_t(segments), 0.0);
     DevBuf dh0(dd * 16), dhc(dd * 16), dz(dd * 16), dops(n_ops * dd * 16 + 16), damp(size_t(segments) * 8),
-        dzs(size_t(segments) * 8), dx(dd * 16), dw(grape_workspace(d, segments));
+        dzs(size_t(segments) * 8), dx(dd * 16),
+        dw(real ? grape_real_workspace(d, segments) : grape_workspace(d, segments));
     check_cuda(cudaMemcpy(dh0.p, h0, dd * 16, cudaMemcpyHostToDevice), "H2D");
     check_cuda(cudaMemcpy(dhc.p, hc, dd * 16, cudaMemcpyHostToDevice), "H2D");
     check_cuda(cudaMemset(dz.p, 0, dd * 16), "memset");
@@ -667,9 +674,13 @@ int lbg_grape_chain(size_t d, const double* h0, const double* hc, const double* 
     check_cuda(cudaEventCreate(&e1), "event");
     check_cuda(cudaEventCreate(&e2), "event");
     check_cuda(cudaEventRecord(e0, nullptr), "event");
-    launch_grape(d, dh0.as<double>(), dhc.as<double>(), dz.as<double>(), n_ops, dops.as<double>(),
-                 damp.as<double>(), dzs.as<double>(), segments, steps_per_segment, dt, dx.as<double>(), dw.p,
-                 nullptr, e1);
+    if (real)
+      launch_grape_real(d, dh0.as<double>(), dhc.as<double>(), dz.as<double>(), n_ops, dops.as<double>(),
+                        damp.as<double>(), segments, steps_per_segment, dt, dx.as<double>(), dw.p, nullptr, e1);
+    else
+      launch_grape(d, dh0.as<double>(), dhc.as<double>(), dz.as<double>(), n_ops, dops.as<double>(),
+                   damp.as<double>(), dzs.as<double>(), segments, steps_per_segment, dt, dx.as<double>(), dw.p,
+                   nullptr, e1);
     check_cuda(cudaEventRecord(e2, nullptr), "event");
     check_cuda(cudaEventSynchronize(e2), "sync");
     float b = 0.f, c = 0.f;

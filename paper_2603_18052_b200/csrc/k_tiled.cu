@@ -390,24 +390,28 @@ __device__ __forceinline__ void init_ring(const Ring& r) {
 // n rows); a box reaching past row n of matrix b reads rows of matrix b+1 —
 // A rows >= n only feed outputs that are never stored, and B rows k >= n meet
 // A columns k >= n, which the TMA zero-fills — so the product is exact.
-__global__ void __launch_bounds__(THREADS) zgemm_kernel(const double2* __restrict__ A,
-                                                        const double2* __restrict__ B,
-                                                        double2* __restrict__ C, int n,
-                                                        long long sa, long long sb, long long sc,
-                                                        const __grid_constant__ CUtensorMap map_a,
-                                                        const __grid_constant__ CUtensorMap map_b) {
-  using G = Geo<32>;
+// G complex (zgemm) or REAL (dgemm on matrices with leading dimension ld; the
+// batch strides sa / sb / sc are in elements)
+template <class G>
+__global__ void __launch_bounds__(THREADS) gemm_kernel(const double2* __restrict__ A,
+                                                       const double2* __restrict__ B,
+                                                       double2* __restrict__ C, int n, int ld,
+                                                       long long sa, long long sb, long long sc,
+                                                       const __grid_constant__ CUtensorMap map_a,
+                                                       const __grid_constant__ CUtensorMap map_b) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const Ring r = carve<G>(smem_raw);
   init_ring(r);
   const int b = blockIdx.z, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const Problem p{A + b * sa, n, B + b * sb, n, C + b * sc, n, n, n, n};
-  const int tiles_m = (n + BM - 1) / BM;
+  // element offsets in units of double2: complex element = 1, real element = 1/2
+  auto off = [&](long long e) { return G::REAL ? e / 2 : e; };
+  const Problem p{A + off(b * sa), ld, B + off(b * sb), ld, C + off(b * sc), ld, n, n, n};
+  const int tiles_m = (n + G::BMg - 1) / G::BMg;
   const int tile = blockIdx.y * tiles_m + blockIdx.x;
   int stage = 0;
   unsigned phase = 0;
   if (warp == CWARPS) {
-    const long long nk = (n + BK - 1) / BK;
+    const long long nk = (n + G::BKg - 1) / G::BKg;
     produce_range_tma<G>(r, p, &map_a, &map_b, tiles_m, tile * nk, (tile + 1) * nk, stage, phase, lane,
                          sa ? b * n : 0, sb ? b * n : 0);
     produce_end(r, stage, phase, lane);
@@ -740,7 +744,7 @@ void launch_tiled_evolve_real(const double* p_dev, size_t n, double* x, int64_t 
 
 void launch_zgemm(const double* a, const double* b, double* c, int n, int batch, long long stride_a,
                   long long stride_b, long long stride_c, cudaStream_t s) {
-  ensure_max_dyn_smem((const void*)zgemm_kernel, int(Geo<32>::kSmemBytes));
+  ensure_max_dyn_smem((const void*)gemm_kernel<Geo<32>>, int(Geo<32>::kSmemBytes));
   const long long nn = (long long)n * n;
   if ((stride_a != 0 && stride_a != nn) || (stride_b != 0 && stride_b != nn))
     throw invalid_argument("zgemm: batch strides must be 0 or n*n");
@@ -749,11 +753,31 @@ void launch_zgemm(const double* a, const double* b, double* c, int n, int batch,
                                         size_t(n), BM, SA);
   const CUtensorMap map_b = complex_map(reinterpret_cast<const double2*>(b), size_t(n) * (stride_b ? batch : 1),
                                         size_t(n), BK, Geo<32>::SB);
-  zgemm_kernel<<<grid, THREADS, Geo<32>::kSmemBytes, s>>>(reinterpret_cast<const double2*>(a),
-                                                 reinterpret_cast<const double2*>(b),
-                                                 reinterpret_cast<double2*>(c), n, stride_a, stride_b,
-                                                 stride_c, map_a, map_b);
+  gemm_kernel<Geo<32>><<<grid, THREADS, Geo<32>::kSmemBytes, s>>>(reinterpret_cast<const double2*>(a),
+                                                                   reinterpret_cast<const double2*>(b),
+                                                                   reinterpret_cast<double2*>(c), n, n, stride_a,
+                                                                   stride_b, stride_c, map_a, map_b);
   LBG_CHECK_LAUNCH("zgemm_kernel");
+}
+
+// real batched GEMM C[b] = A[b] B[b] (n x n, leading dimension ld even, batch
+// strides 0 or n*ld doubles)
+void launch_dgemm(const double* a, const double* b, double* c, int n, int ld, int batch, long long stride_a,
+                  long long stride_b, long long stride_c, cudaStream_t s) {
+  using G = StepGeoR;
+  ensure_max_dyn_smem((const void*)gemm_kernel<G>, int(G::kSmemBytes));
+  const long long nl = (long long)n * ld;
+  if ((ld & 1) || ld < n) throw invalid_argument("dgemm: leading dimension must be even and >= n");
+  if ((stride_a != 0 && stride_a != nl) || (stride_b != 0 && stride_b != nl) || (stride_c & 1))
+    throw invalid_argument("dgemm: batch strides must be 0 or n*ld");
+  const dim3 grid((n + G::BMg - 1) / G::BMg, (n + G::BN - 1) / G::BN, batch);
+  const CUtensorMap map_a = real_map(a, size_t(n) * (stride_a ? batch : 1), size_t(n), size_t(ld), G::BMg, G::SAg);
+  const CUtensorMap map_b = real_map(b, size_t(n) * (stride_b ? batch : 1), size_t(n), size_t(ld), G::BKg, G::SB);
+  gemm_kernel<G><<<grid, THREADS, G::kSmemBytes, s>>>(reinterpret_cast<const double2*>(a),
+                                                      reinterpret_cast<const double2*>(b),
+                                                      reinterpret_cast<double2*>(c), n, ld, stride_a, stride_b,
+                                                      stride_c, map_a, map_b);
+  LBG_CHECK_LAUNCH("dgemm_kernel");
 }
 
 }  // namespace lbg
