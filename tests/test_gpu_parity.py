@@ -408,6 +408,38 @@ def test_grape_constant_pulse_equals_evolve(lbg):
         lbg.grape_chain(h0, np.zeros((2, 2)), [0.5], 4, 0.01, dis, rho0)
 
 
+@pytest.mark.parametrize("d", [11, 27])
+def test_grape_real_form_matches_complex(lbg, reference, d):
+    """n > 96: an exactly Hermitian rho0 takes the real transfer-matrix path
+    (k_grape_real.cu, odd n = 121 exercises the padded leading dimension); a
+    rho0 off Hermitian by one ulp takes the complex path. Both agree with each
+    other and with the constant-pulse evolve route."""
+    rng = np.random.default_rng(d)
+    if d == 27:
+        h0, hc, op, amps, dt, rho0 = reference.grape_inputs(d, 3)
+    else:
+        r = rng.uniform(-1, 1, (d, d)) + 1j * rng.uniform(-1, 1, (d, d))
+        h0 = 0.5 * (r + r.conj().T)
+        r = rng.uniform(-1, 1, (d, d)) + 1j * rng.uniform(-1, 1, (d, d))
+        hc = 0.5 * (r + r.conj().T)
+        op = [0.3 * np.diag(np.sqrt(np.arange(1, d)), 1).astype(complex)]
+        amps, dt = list(rng.uniform(-1, 1, 4)), 0.01
+        rho0 = np.zeros((d, d), complex)
+        rho0[d - 1, d - 1] = 1.0
+    amps = list(amps)
+    got_r, _ = lbg.grape_chain(h0, hc, amps, 8, dt, op, rho0)
+    r2 = np.array(rho0, dtype=complex)
+    r2[0, 1] += 1e-15
+    got_c, _ = lbg.grape_chain(h0, hc, amps, 8, dt, op, r2)
+    assert np.abs(got_r - got_c).max() <= TOL_RHO
+    tr, herm = invariants(got_r)
+    assert tr <= TOL_INV and herm <= TOL_INV
+    # constant pulse: the real chain equals expm + evolve of the one generator
+    got, _ = lbg.grape_chain(h0, hc, [amps[0]] * 3, 5, dt, op, rho0)
+    P = lbg.expm(lbg.build_lindbladian(h0 + amps[0] * hc, op), dt)
+    assert np.abs(got - lbg.evolve(P, rho0, 15)).max() <= TOL_RHO
+
+
 @pytest.mark.parametrize("n,B", [(17, 16), (33, 5), (81, 8), (97, 40), (130, 333)])
 def test_tiled_ragged_shapes_vs_torch(lbg, torch, n, B):
     """Regression: odd n (ragged last K chunk and last M tile) through the TMA /
