@@ -22,12 +22,11 @@
 //   three 88x92 padded matrices in shared memory, A and A^2 also kept at each
 //   thread's own accumulator positions so the Horner epilogues never re-read
 //   them. Writes P_R (n x n) to global memory.
-// K3 (ptm_step_kernel): one CTA per trajectory; P_R register resident (one
-//   row of 81 doubles per thread), x in shared memory; per step 81 FMAs in 12
-//   chains on broadcast loads, one barrier. The SM register file (P_R = 13k
-//   registers per trajectory) caps residency at 2 trajectories per SM, which
-//   bounds this kernel (ncu: 6 warps/SM, FP64 pipe ~40%, "wait" stalls).
-//   Epilogue: populations + ensemble sum.
+// K3 (ptm_step_kernel): three trajectories per CTA; P_R register resident
+//   (a 4 x 21 block per thread), x in shared memory; per step 84 FMAs in 12
+//   chains, a 4-lane shuffle reduce-scatter, one barrier. The SM register file
+//   (P_R = 13k registers per trajectory) caps residency at 3 trajectories per
+//   SM. Epilogue: populations + ensemble sum.
 #include <algorithm>
 #include <cmath>
 
@@ -267,67 +266,94 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 // K3: x <- P_R x for `steps` steps, P_R register resident.
-// One thread per row of P_R: the whole 81-double row lives in registers, so a
-// step is 81 FMAs on broadcast loads of x, one store and one 3-warp barrier —
-// no cross-thread reduction. ~200 registers x 96 threads lets 3 trajectories
-// share an SM; the FP64 pipe, not latency, bounds the step.
-// DFMA latency is 23 cycles on B200 (profiles/r01_latency_probe.json), so the
-// 81-term dot product runs as 12 independent chains (depth 7) and the loads of
-// x are issued in 4 blocks (compiler barrier) to keep the register count at
-// 3 CTAs per SM.
-// Three trajectories per CTA: 8 warps hold 3 x 81 = 243 rows (13 idle lanes),
-// i.e. two 224-register warps per sub-partition — all a sub-partition's 16K
-// registers can carry — so an SM steps 3 trajectories at once instead of the 2
-// that 3-warp one-trajectory CTAs reach (their third warp would not fit).
+// P_R is padded to 84 x 84 and cut into 4-row x 21-column blocks: one block
+// (84 doubles) per thread, the 4 column blocks of a row group in 4 adjacent
+// lanes. A step is 84 FMAs on 11 loads of the thread's 21 x values (earlier
+// design — one 81-double row per thread — issued 41 broadcast loads per step
+// and was shared-memory-wavefront bound: ncu 0.82 wavefronts/cycle, FP64 pipe
+// 40%, profiles/r01_ncu_ptm_step_rowthread.json), then a 2-round butterfly
+// reduce-scatter over the 4 lanes leaves each lane one finished row, one store
+// and one barrier.
+// DFMA latency is 23 cycles on B200 (profiles/r01_latency_probe.json): the 4
+// row sums run as 12 independent chains of depth 7.
+// Three trajectories per CTA: 63 groups of 4 lanes = 252 of 256 threads, two
+// 224-register warps per sub-partition — all its 16K registers can carry.
+// x lives in shared memory padded per column block (stride 22: 16-byte aligned
+// pairs, the 4 blocks on disjoint banks).
 constexpr int STEP_TRAJ = 3;
 constexpr int STEP_THREADS = 256;
-constexpr int NACC = 12;
+constexpr int SR = 4, SC = 21, SGROUPS = 21, XB = 22, XS = 4 * XB;
+__device__ __forceinline__ int xpos(int c) { return (c / SC) * XB + c % SC; }
 __global__ void __maxnreg__(224)
     ptm_step_kernel(const double* __restrict__ p_r, const double* __restrict__ x0, int64_t count, int64_t steps,
                     double* __restrict__ pops, double* __restrict__ ens_x) {
-  __shared__ __align__(16) double xs[2][STEP_TRAJ][88];
+  __shared__ __align__(16) double xs[2][STEP_TRAJ][XS];
   const int tid = threadIdx.x;
-  const int tt = tid < STEP_TRAJ * N ? tid / N : STEP_TRAJ - 1;   // trajectory within the CTA
-  const int row = tid < STEP_TRAJ * N ? tid - tt * N : N - 1;      // idle lanes shadow the last row
+  const int grp = tid >> 2, cb = tid & 3;
+  const bool active = grp < STEP_TRAJ * SGROUPS;  // the 4 spare lanes shadow the last group
+  const int tt = active ? grp / SGROUPS : STEP_TRAJ - 1;
+  const int rg = active ? grp - tt * SGROUPS : SGROUPS - 1;
   const int64_t b = int64_t(blockIdx.x) * STEP_TRAJ + tt;
   const bool live = b < count;
-  const double* pb = p_r + size_t(live ? b : 0) * N * N + size_t(row) * N;
-  double p[N];
+  const double* pb = p_r + size_t(live ? b : 0) * N * N;
+  double p[SR][SC];
 #pragma unroll
-  for (int j = 0; j < N; ++j) p[j] = pb[j];
-  for (int e = tid; e < STEP_TRAJ * 88; e += STEP_THREADS) {
-    const int c = e % 88;
-    xs[0][e / 88][c] = c < N ? x0[c] : 0.0;
-    xs[1][e / 88][c] = 0.0;
+  for (int i = 0; i < SR; ++i)
+#pragma unroll
+    for (int k = 0; k < SC; ++k) {
+      const int r = rg * SR + i, c = cb * SC + k;
+      p[i][k] = (r < N && c < N) ? pb[r * N + c] : 0.0;
+    }
+  for (int e = tid; e < STEP_TRAJ * XS; e += STEP_THREADS) {
+    const int t = e / XS, q = e - t * XS, c = (q / XB) * SC + q % XB;
+    xs[0][t][q] = (q % XB < SC && c < N) ? x0[c] : 0.0;
+    xs[1][t][q] = 0.0;
   }
   __syncthreads();
-  const int slot = tid < STEP_TRAJ * N ? row : N;  // idle lanes write a dummy slot
+  const int row = rg * SR + cb;  // the row this lane finishes
+  const bool writer = active && row < N;
+  const int slot = xpos(row);
+  const bool hi2 = cb & 2, hi1 = cb & 1;
   int cur = 0;
 #pragma unroll 1
   for (int64_t s = 0; s < steps; ++s) {
-    const double* x = xs[cur][tt];
-    double acc[NACC];
+    const double* x = xs[cur][tt] + cb * XB;
+    double acc[SR][2];
 #pragma unroll
-    for (int a = 0; a < NACC; ++a) acc[a] = 0.0;
+    for (int i = 0; i < SR; ++i) acc[i][0] = acc[i][1] = 0.0;
 #pragma unroll
-    for (int j = 0; j + 1 < N; j += 2) {
-      if (j % 20 == 0) asm volatile("" ::: "memory");  // bound how far loads are hoisted
-      const double2 v = *reinterpret_cast<const double2*>(x + j);
-      acc[j % NACC] = fma(p[j], v.x, acc[j % NACC]);
-      acc[(j + 1) % NACC] = fma(p[j + 1], v.y, acc[(j + 1) % NACC]);
+    for (int k = 0; k + 1 < SC; k += 2) {
+      if (k % 10 == 0) asm volatile("" ::: "memory");  // bound how far loads are hoisted
+      const double2 v = *reinterpret_cast<const double2*>(x + k);
+#pragma unroll
+      for (int i = 0; i < SR; ++i) {
+        acc[i][0] = fma(p[i][k], v.x, acc[i][0]);
+        acc[i][1] = fma(p[i][k + 1], v.y, acc[i][1]);
+      }
     }
-    acc[(N - 1) % NACC] = fma(p[N - 1], x[N - 1], acc[(N - 1) % NACC]);
+    {
+      const double v = x[SC - 1];
 #pragma unroll
-    for (int w = 1; w < NACC; w *= 2)
+      for (int i = 0; i < SR; ++i) acc[i][0] = fma(p[i][SC - 1], v, acc[i][0]);
+    }
+    double r4[SR];
 #pragma unroll
-      for (int a = 0; a + w < NACC; a += 2 * w) acc[a] += acc[a + w];
-    xs[cur ^ 1][tt][slot] = acc[0];
+    for (int i = 0; i < SR; ++i) r4[i] = acc[i][0] + acc[i][1];
+    // butterfly reduce-scatter over the 4 column-block lanes: lane cb keeps row cb
+    double k0 = hi2 ? r4[2] : r4[0], k1 = hi2 ? r4[3] : r4[1];
+    const double s0 = hi2 ? r4[0] : r4[2], s1 = hi2 ? r4[1] : r4[3];
+    k0 += __shfl_xor_sync(0xffffffffu, s0, 2);
+    k1 += __shfl_xor_sync(0xffffffffu, s1, 2);
+    double kk = hi1 ? k1 : k0;
+    kk += __shfl_xor_sync(0xffffffffu, hi1 ? k0 : k1, 1);
+    if (writer) xs[cur ^ 1][tt][slot] = kk;
     __syncthreads();
     cur ^= 1;
   }
-  if (tid < STEP_TRAJ * N && live) {
-    if (row < D) pops[size_t(b) * D + row] = xs[cur][tt][row * D + row];
-    atomicAdd(&ens_x[row], xs[cur][tt][row]);
+  if (writer && live) {
+    const double v = xs[cur][tt][slot];
+    if (row % (D + 1) == 0) pops[size_t(b) * D + row / (D + 1)] = v;
+    atomicAdd(&ens_x[row], v);
   }
 }
 
