@@ -323,6 +323,38 @@ def test_sweep_modes_agree_at_full_size(lbg, torch):
     assert np.abs(er - ec).max() <= TOL_RHO
 
 
+@pytest.mark.parametrize("dt", [0.07, 0.12, 0.6])
+def test_sweep_real_expm_branches(lbg, torch, dt):
+    """k_ptm.cu expm branches: ||A||_1 ~ 0.23 / 0.41 / 2.0 take Taylor degree 12,
+    degree 14, and degree 14 with two squarings; a ragged batch (not a multiple
+    of the 3 trajectories per step CTA) and a full Hermitian rho0. The real
+    path must agree with the reference-form complex path."""
+    dev = torch.device("cuda")
+    B, S = 301, 40
+    h0, hd, hs = lbg.config_sweep_terms()
+    _, ops = lbg.config_model(4)
+    delta, scale = lbg.sweep_params(7, B)
+    rng = np.random.default_rng(5)
+    g = rng.normal(size=(9, 9)) + 1j * rng.normal(size=(9, 9))
+    rho0 = g @ g.conj().T
+    rho0 = rho0 / np.trace(rho0).real
+    rho0 = 0.5 * (rho0 + rho0.conj().T)  # exactly Hermitian
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    out = {}
+    for mode in ("real", "complex"):
+        pops = torch.zeros(B, 9, dtype=torch.float64, device=dev)
+        ens = torch.zeros(9, 9, dtype=torch.complex128, device=dev)
+        work = torch.empty(lbg.sweep_workspace(9, B), dtype=torch.uint8, device=dev)
+        lbg.evolve_sweep_dev(T(h0), T(hd), T(hs), T(ops), T(delta), T(scale), dt, T(rho0), S, pops, ens, work,
+                             mode=mode)
+        torch.cuda.synchronize()
+        out[mode] = (pops.cpu().numpy(), ens.cpu().numpy())
+    assert np.abs(out["real"][0] - out["complex"][0]).max() <= TOL_RHO
+    assert np.abs(out["real"][1] - out["complex"][1]).max() <= TOL_RHO * B
+    tr, herm = invariants(out["real"][1] / B)
+    assert tr <= TOL_INV and herm <= TOL_INV
+
+
 def test_sweep_real_mode_rejects_non_hermitian(lbg, torch):
     dev = torch.device("cuda")
     h0, hd, hs = lbg.config_sweep_terms()
