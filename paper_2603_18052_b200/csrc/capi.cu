@@ -653,7 +653,7 @@ int lbg_grape_chain(size_t d, const double* h0, const double* hc, const double* 
       throw invalid_argument("evolve: initial state fails physical-state checks");
     const size_t dd = d * d;
     // the real transfer-matrix form needs an exactly Hermitian rho0 (k_grape_real.cu)
-    bool real = grape_real_supported(d);
+    bool real = grape_real_supported(d) || ptm_grape_supported(d);
     for (size_t i = 0; real && i < d; ++i)
       for (size_t j = 0; j < d; ++j)
         real = real && rho0[2 * (i * d + j)] == rho0[2 * (j * d + i)] &&
@@ -661,7 +661,8 @@ int lbg_grape_chain(size_t d, const double* h0, const double* hc, const double* 
     std::vector<double> zeros(size_t(segments), 0.0);
     DevBuf dh0(dd * 16), dhc(dd * 16), dz(dd * 16), dops(n_ops * dd * 16 + 16), damp(size_t(segments) * 8),
         dzs(size_t(segments) * 8), dx(dd * 16),
-        dw(real ? grape_real_workspace(d, segments) : grape_workspace(d, segments));
+        dw(real ? (ptm_grape_supported(d) ? ptm_grape_workspace(segments) : grape_real_workspace(d, segments))
+                : grape_workspace(d, segments));
     check_cuda(cudaMemcpy(dh0.p, h0, dd * 16, cudaMemcpyHostToDevice), "H2D");
     check_cuda(cudaMemcpy(dhc.p, hc, dd * 16, cudaMemcpyHostToDevice), "H2D");
     check_cuda(cudaMemset(dz.p, 0, dd * 16), "memset");
@@ -674,7 +675,10 @@ int lbg_grape_chain(size_t d, const double* h0, const double* hc, const double* 
     check_cuda(cudaEventCreate(&e1), "event");
     check_cuda(cudaEventCreate(&e2), "event");
     check_cuda(cudaEventRecord(e0, nullptr), "event");
-    if (real)
+    if (real && ptm_grape_supported(d))
+      launch_ptm_grape(dh0.as<double>(), dhc.as<double>(), dz.as<double>(), n_ops, dops.as<double>(),
+                       damp.as<double>(), segments, steps_per_segment, dt, dx.as<double>(), dw.p, nullptr, e1);
+    else if (real)
       launch_grape_real(d, dh0.as<double>(), dhc.as<double>(), dz.as<double>(), n_ops, dops.as<double>(),
                         damp.as<double>(), segments, steps_per_segment, dt, dx.as<double>(), dw.p, nullptr, e1);
     else

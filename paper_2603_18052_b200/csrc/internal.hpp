@@ -111,6 +111,12 @@ void launch_grape(std::size_t d, const double* h0, const double* hc, const doubl
                   std::size_t n_ops, const double* ops, const double* amps, const double* zeros,
                   int64_t segments, int64_t steps_per_segment, double dt, double* x, void* work,
                   cudaStream_t s, cudaEvent_t ev_build_end);
+// GRAPE chain for d = 9 in the real form (Hermitian rho0) (k_ptm.cu)
+bool ptm_grape_supported(std::size_t d);
+std::size_t ptm_grape_workspace(int64_t segments);
+void launch_ptm_grape(const double* h0, const double* hc, const double* zero_h, std::size_t n_ops, const double* ops,
+                      const double* amps, int64_t segments, int64_t steps_per_segment, double dt, double* rho,
+                      void* work, cudaStream_t s, cudaEvent_t ev_build_end);
 // GRAPE chain in the real transfer-matrix form (Hermitian rho0, n > 96) (k_grape_real.cu)
 bool grape_real_supported(std::size_t d);
 std::size_t grape_real_workspace(std::size_t d, int64_t segments);

@@ -440,14 +440,15 @@ def test_grape_constant_pulse_equals_evolve(lbg):
         lbg.grape_chain(h0, np.zeros((2, 2)), [0.5], 4, 0.01, dis, rho0)
 
 
-@pytest.mark.parametrize("d", [11, 27])
+@pytest.mark.parametrize("d", [9, 11, 27])
 def test_grape_real_form_matches_complex(lbg, reference, d):
-    """n > 96: an exactly Hermitian rho0 takes the real transfer-matrix path
-    (k_grape_real.cu, odd n = 121 exercises the padded leading dimension); a
+    """d = 9 (k_ptm.cu launch_ptm_grape) and n > 96 (k_grape_real.cu, odd n = 121
+    exercises the padded leading dimension): an exactly Hermitian rho0 takes the
+    real transfer-matrix path; a
     rho0 off Hermitian by one ulp takes the complex path. Both agree with each
     other and with the constant-pulse evolve route."""
     rng = np.random.default_rng(d)
-    if d == 27:
+    if d in (9, 27):
         h0, hc, op, amps, dt, rho0 = reference.grape_inputs(d, 3)
     else:
         r = rng.uniform(-1, 1, (d, d)) + 1j * rng.uniform(-1, 1, (d, d))
