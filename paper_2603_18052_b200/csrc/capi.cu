@@ -73,15 +73,19 @@ struct Grow {
     cap = bytes;
   }
 };
+constexpr int kMaxChunks = 16;
 struct EvolvePool {
   std::mutex mu;
   Grow p, x, chk, w[2];
-  cudaStream_t st[2] = {nullptr, nullptr};
-  cudaEvent_t ev_p = nullptr;
+  cudaStream_t st[4] = {nullptr, nullptr, nullptr, nullptr};  // H2D, compute x2, D2H
+  cudaEvent_t ev_h[kMaxChunks] = {}, ev_c[kMaxChunks] = {};
   void ensure(size_t pb, size_t xb, size_t cb, size_t wb) {
     if (!st[0]) {
       for (auto& s : st) check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
-      check_cuda(cudaEventCreateWithFlags(&ev_p, cudaEventDisableTiming), "event");
+      for (int i = 0; i < kMaxChunks; ++i) {
+        check_cuda(cudaEventCreateWithFlags(&ev_h[i], cudaEventDisableTiming), "event");
+        check_cuda(cudaEventCreateWithFlags(&ev_c[i], cudaEventDisableTiming), "event");
+      }
     }
     p.ensure(pb);
     x.ensure(xb);
@@ -375,10 +379,12 @@ int lbg_evolve_shared_p_aos_dev(const double* p, size_t n, double* x, int64_t ba
 
 namespace {
 // Host-buffer evolve shared by lbg_evolve_shared_p and lbg_evolve_density.
-// Pipeline: the batch is cut into chunks that alternate between two streams,
-// so chunk k's H2D, chunk k-1's steps and chunk k-2's D2H overlap (copy
-// engines and SMs run concurrently). `single` forces one chunk (the
-// cooperative tiled kernel is never run concurrently with itself).
+// Three-stage pipeline over chunks of the batch: H2D on one stream, validation
+// + steps on two compute streams (alternating chunks, so one chunk's kernel
+// tail overlaps the next chunk's start), D2H on a fourth, chained by events —
+// the copy engines run both directions underneath the compute and only the
+// first chunk's H2D and the last chunk's D2H are exposed. `single` forces one
+// chunk (the cooperative tiled kernel).
 template <class WorkBytes, class Step>
 void host_evolve_impl(const double* p, size_t d, const double* rho0, int64_t batch, double* out, bool single,
                       WorkBytes work_bytes, Step step) {
@@ -387,7 +393,10 @@ void host_evolve_impl(const double* p, size_t d, const double* rho0, int64_t bat
   if (batch == 0) return;
   const size_t n = d * d;
   const int64_t min_chunk = 32768;
-  constexpr int64_t max_chunks = 16;  // measured at c1: 4 -> 21.2, 8 -> 20.6, 16 -> 20.2, 32 -> 21.1 ms per call
+  // measured at c1 (ms per call): 4 -> 21.1, 8 -> 20.4, 16 -> 21.6-27 (+ outliers); one compute stream
+  // instead of two: 21.2 at 8 (kernel tails no longer overlap)
+  constexpr int64_t max_chunks = 8;
+  static_assert(max_chunks <= kMaxChunks, "events per chunk");
   const int nchunks = (single || batch < 2 * min_chunk) ? 1 : int(std::min<int64_t>(max_chunks, batch / min_chunk));
   const int64_t chunk = (batch + nchunks - 1) / nchunks;
   EvolvePool& pool = evolve_pool();
@@ -396,26 +405,30 @@ void host_evolve_impl(const double* p, size_t d, const double* rho0, int64_t bat
   double* dp = static_cast<double*>(pool.p.ptr);
   double* dx = static_cast<double*>(pool.x.ptr);
   double* dchk = static_cast<double*>(pool.chk.ptr);
-  check_cuda(cudaMemcpyAsync(dp, p, n * n * 16, cudaMemcpyHostToDevice, pool.st[0]), "H2D P");
-  check_cuda(cudaEventRecord(pool.ev_p, pool.st[0]), "event");
-  check_cuda(cudaStreamWaitEvent(pool.st[1], pool.ev_p, 0), "wait");
+  cudaStream_t sh = pool.st[0], sd = pool.st[3];
+  check_cuda(cudaMemcpyAsync(dp, p, n * n * 16, cudaMemcpyHostToDevice, sh), "H2D P");
+  int used = 0;
   for (int c = 0; c < nchunks; ++c) {
     const int64_t b0 = c * chunk, nb = std::min<int64_t>(chunk, batch - b0);
     if (nb <= 0) break;
-    cudaStream_t s = pool.st[c & 1];
     double* xc = dx + size_t(b0) * n * 2;
     const size_t bytes = size_t(nb) * n * 16;
-    check_cuda(cudaMemcpyAsync(xc, rho0 + size_t(b0) * n * 2, bytes, cudaMemcpyHostToDevice, s), "H2D rho0");
+    check_cuda(cudaMemcpyAsync(xc, rho0 + size_t(b0) * n * 2, bytes, cudaMemcpyHostToDevice, sh), "H2D rho0");
+    check_cuda(cudaEventRecord(pool.ev_h[c], sh), "event");
+    cudaStream_t sc = pool.st[1 + (c & 1)];
+    check_cuda(cudaStreamWaitEvent(sc, pool.ev_h[c], 0), "wait");
     // propagate.cpp:79 — every rho0 must pass check_state at 1e-8
-    launch_check_state(xc, d, nb, dchk + 3 * c, s);
-    step(dp, xc, nb, pool.w[c & 1].ptr, s);
-    check_cuda(cudaMemcpyAsync(out + size_t(b0) * n * 2, xc, bytes, cudaMemcpyDeviceToHost, s), "D2H rho");
+    launch_check_state(xc, d, nb, dchk + 3 * c, sc);
+    step(dp, xc, nb, pool.w[c & 1].ptr, sc);
+    check_cuda(cudaEventRecord(pool.ev_c[c], sc), "event");
+    check_cuda(cudaStreamWaitEvent(sd, pool.ev_c[c], 0), "wait");
+    check_cuda(cudaMemcpyAsync(out + size_t(b0) * n * 2, xc, bytes, cudaMemcpyDeviceToHost, sd), "D2H rho");
+    used = c + 1;
   }
-  std::vector<double> chk(size_t(nchunks) * 3);
-  check_cuda(cudaMemcpyAsync(chk.data(), dchk, chk.size() * 8, cudaMemcpyDeviceToHost, pool.st[1]), "D2H");
-  check_cuda(cudaStreamSynchronize(pool.st[0]), "sync");
-  check_cuda(cudaStreamSynchronize(pool.st[1]), "sync");
-  for (int c = 0; c < nchunks; ++c)
+  std::vector<double> chk(size_t(used) * 3);
+  check_cuda(cudaMemcpyAsync(chk.data(), dchk, chk.size() * 8, cudaMemcpyDeviceToHost, sd), "D2H");
+  check_cuda(cudaStreamSynchronize(sd), "sync");
+  for (int c = 0; c < used; ++c)
     if (!(chk[3 * c] <= 1e-8 && chk[3 * c + 1] <= 1e-8 && chk[3 * c + 2] >= -1e-8))
       throw invalid_argument("evolve: initial state fails physical-state checks");
 }
