@@ -681,7 +681,12 @@ void run_tiled(const double* p_dev, size_t ldp, size_t n, int64_t batch, int64_t
   ensure_max_dyn_smem((const void*)kern, int(G::kSmemBytes));
   int occ = 0;
   check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, THREADS, G::kSmemBytes), "occupancy");
-  int grid = std::min<int>(occ * sm_count(), int(nt));
+  // stream-K needs grid <= ntiles; when fewer tiles than resident slots exist,
+  // a whole multiple of the SM count keeps every SM's share equal (384 real
+  // tiles at c3 on 444 slots: 384 CTAs = 3 tiles on some SMs, 2 on others)
+  const int sms = sm_count();
+  int grid = std::min<int>(occ * sms, int(nt));
+  if (grid < occ * sms && grid >= sms) grid -= grid % sms;
   if (grid < 1) grid = 1;
   const double2* p2 = reinterpret_cast<const double2*>(p_dev);
   int ni = int(n), bi = int(batch), li = int(ldv);
