@@ -434,6 +434,53 @@ void host_evolve_impl(const double* p, size_t d, const double* rho0, int64_t bat
 }
 }  // namespace
 
+namespace {
+// 1-norm (max column sum) of a d x d complex matrix (interleaved doubles)
+double norm1(const double* a, size_t d) {
+  double best = 0.0;
+  for (size_t c = 0; c < d; ++c) {
+    double sum = 0.0;
+    for (size_t r = 0; r < d; ++r) sum += std::hypot(a[2 * (r * d + c)], a[2 * (r * d + c) + 1]);
+    best = std::max(best, sum);
+  }
+  return best;
+}
+// A-priori bound on the squarings the real-form GRAPE build needs (Taylor-16,
+// theta = 0.79): ||L||_1 <= 2 max_j ||h0 + a_j hc||_1 + sum_k (||A_k||_1^2 +
+// ||A_k^dag A_k||_1) by the Kronecker norm identity, and every real-form entry
+// combines two complex entries, so ||L_R||_1 <= 2 ||L||_1.
+int grape_squaring_bound(size_t d, const double* h0, const double* hc, const double* amps, int64_t segments,
+                         size_t n_ops, const double* ops, double dt) {
+  double hmax = 0.0;
+  const double n0 = norm1(h0, d), nc = norm1(hc, d);
+  for (int64_t j = 0; j < segments; ++j) hmax = std::max(hmax, n0 + std::fabs(amps[j]) * nc);
+  double dis = 0.0;
+  std::vector<double> ada(2 * d * d);
+  for (size_t k = 0; k < n_ops; ++k) {
+    const double* a = ops + k * 2 * d * d;
+    for (size_t i = 0; i < d; ++i)
+      for (size_t j = 0; j < d; ++j) {
+        double re = 0.0, im = 0.0;  // (A^dag A)_ij = sum_r conj(A_ri) A_rj
+        for (size_t r = 0; r < d; ++r) {
+          const double xr = a[2 * (r * d + i)], xi = -a[2 * (r * d + i) + 1];
+          const double yr = a[2 * (r * d + j)], yi = a[2 * (r * d + j) + 1];
+          re += xr * yr - xi * yi;
+          im += xr * yi + xi * yr;
+        }
+        ada[2 * (i * d + j)] = re;
+        ada[2 * (i * d + j) + 1] = im;
+      }
+    const double na = norm1(a, d);
+    dis += na * na + norm1(ada.data(), d);
+  }
+  const double bound = 2.0 * std::fabs(dt) * (2.0 * hmax + dis);
+  if (!std::isfinite(bound)) throw invalid_argument("grape_chain: non-finite generator");
+  const int sq = bound > 0.79 ? int(std::ceil(std::log2(bound / 0.79))) : 0;
+  if (sq > 64) throw runtime_error("expm: norm requires more than 64 squarings");
+  return sq;
+}
+}  // namespace
+
 extern "C" {
 
 size_t lbg_evolve_planes_workspace(size_t n, int64_t batch, int algo) {
@@ -693,7 +740,8 @@ int lbg_grape_chain(size_t d, const double* h0, const double* hc, const double* 
                        damp.as<double>(), segments, steps_per_segment, dt, dx.as<double>(), dw.p, nullptr, e1);
     else if (real)
       launch_grape_real(d, dh0.as<double>(), dhc.as<double>(), dz.as<double>(), n_ops, dops.as<double>(),
-                        damp.as<double>(), segments, steps_per_segment, dt, dx.as<double>(), dw.p, nullptr, e1);
+                        damp.as<double>(), segments, steps_per_segment, dt, dx.as<double>(),
+                        grape_squaring_bound(d, h0, hc, amplitudes, segments, n_ops, ops, dt), dw.p, nullptr, e1);
     else
       launch_grape(d, dh0.as<double>(), dhc.as<double>(), dz.as<double>(), n_ops, dops.as<double>(),
                    damp.as<double>(), dzs.as<double>(), segments, steps_per_segment, dt, dx.as<double>(), dw.p,

@@ -87,8 +87,10 @@ void launch_density(const double* p, std::size_t d, double* rho, int64_t batch, 
 void launch_zgemm(const double* a, const double* b, double* c, int n, int batch,
                   long long stride_a, long long stride_b, long long stride_c, cudaStream_t s);
 // the same engine on real matrices: leading dimension ld (even, >= n), strides 0 or n * ld doubles
+// cond (device, optional): when cond_idx >= *cond the launch copies A into C instead
 void launch_dgemm(const double* a, const double* b, double* c, int n, int ld, int batch, long long stride_a,
-                  long long stride_b, long long stride_c, cudaStream_t s);
+                  long long stride_b, long long stride_c, cudaStream_t s, const int* cond = nullptr,
+                  int cond_idx = 0);
 
 // model kernels (k_model.cu)
 void launch_build_lindbladian(std::size_t d, const double* h, std::size_t n_ops,
@@ -122,8 +124,8 @@ bool grape_real_supported(std::size_t d);
 std::size_t grape_real_workspace(std::size_t d, int64_t segments);
 void launch_grape_real(std::size_t d, const double* h0, const double* hc, const double* zero_h,
                        std::size_t n_ops, const double* ops, const double* amps, int64_t segments,
-                       int64_t steps_per_segment, double dt, double* x_rho, void* work, cudaStream_t s,
-                       cudaEvent_t ev_build_end);
+                       int64_t steps_per_segment, double dt, double* x_rho, int squaring_bound, void* work,
+                       cudaStream_t s, cudaEvent_t ev_build_end);
 void launch_sweep(std::size_t d, const double* h0, const double* hd, const double* hs,
                   std::size_t n_ops, const double* ops, const double* delta, const double* scale,
                   double dt, const double* rho0, int64_t batch, int64_t steps, double* pops,

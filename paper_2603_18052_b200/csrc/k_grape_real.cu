@@ -82,24 +82,44 @@ __global__ void assemble_real_kernel(const double* __restrict__ dr, const double
   A[o] = dt * (dr[(long long)q * ld + s] + real_entry_rt(coh, d, q, s));
 }
 
-// per-matrix 1-norm (max column sum), max over the batch into *nmax (bits)
+// per-matrix 1-norm (max column sum), max over the batch into *nmax (bits).
+// Block (32 columns x 8 row groups), grid (column blocks, matrices): coalesced
+// rows, 8-way parallel column sums (a thread per whole column took 0.89 ms for
+// 20 matrices at n = 729 — a fifth of the build).
 __global__ void colsum_real_kernel(const double* __restrict__ A, int n, int ld, unsigned long long* __restrict__ nmax) {
-  const int b = blockIdx.x;
-  double best = 0.0;
-  for (int c = threadIdx.x; c < n; c += blockDim.x) {
-    double sum = 0.0;
-    for (int r = 0; r < n; ++r) sum += fabs(A[(long long)b * n * ld + (long long)r * ld + c]);
-    best = fmax(best, sum);
+  __shared__ double part[8][33];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int c = blockIdx.x * 32 + tx;
+  const double* m = A + (long long)blockIdx.y * n * ld;
+  double sum = 0.0;
+  if (c < n)
+    for (int r = ty; r < n; r += 8) sum += fabs(m[(long long)r * ld + c]);
+  part[ty][tx] = sum;
+  __syncthreads();
+  if (ty == 0) {
+    double tot = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) tot += part[k][tx];
+    for (int o = 16; o > 0; o >>= 1) tot = fmax(tot, __shfl_xor_sync(0xffffffffu, tot, o));
+    if (tx == 0) atomicMax(nmax, (unsigned long long)__double_as_longlong(tot));
   }
-  for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(nmax, (unsigned long long)__double_as_longlong(best));
 }
 
-__global__ void scale_real_kernel(double* __restrict__ A, int n, int ld, double sc) {
+// A *= 2^-sq with sq decided on the device (squarings_kernel)
+__global__ void scale_real_kernel(double* __restrict__ A, int n, int ld, const int* __restrict__ sq) {
+  const int q = *sq;
+  if (q == 0) return;
   const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (e >= (long long)n * n) return;
   const int r = int(e / n), c = int(e - (long long)r * n);
-  A[(long long)blockIdx.y * n * ld + (long long)r * ld + c] *= sc;
+  A[(long long)blockIdx.y * n * ld + (long long)r * ld + c] *= ldexp(1.0, -q);
+}
+
+// the common squaring count from the batch's max 1-norm (Taylor-16: theta = 0.79)
+__global__ void squarings_kernel(const unsigned long long* __restrict__ nmax, int sq_max, int* __restrict__ sq) {
+  const double nrm = __longlong_as_double((long long)*nmax);
+  int q = nrm > 0.79 ? int(ceil(log2(nrm / 0.79))) : 0;
+  *sq = q < sq_max ? q : sq_max;  // the host bound covers it; the clamp only guards rounding
 }
 
 // out = x + c0 I + c1 a1 + c2 a2 + c3 a3 + c4 a4   (any of x, a4 may be null)
@@ -210,7 +230,7 @@ size_t grape_real_workspace(size_t d, int64_t segments) {
 
 void launch_grape_real(size_t d, const double* h0, const double* hc, const double* zero_h, size_t n_ops,
                        const double* ops, const double* amps, int64_t segments, int64_t sps, double dt, double* x_rho,
-                       void* work, cudaStream_t s, cudaEvent_t ev_build_end) {
+                       int squaring_bound, void* work, cudaStream_t s, cudaEvent_t ev_build_end) {
   const int n = int(d * d), ld = even_ld(n), dd = int(d);
   const size_t mat = align_up(size_t(segments) * n * ld * 8);
   char* w = static_cast<char*>(work);
@@ -228,6 +248,7 @@ void launch_grape_real(size_t d, const double* h0, const double* hc, const doubl
   double* x1 = x0 + n;
   unsigned int* bar = reinterpret_cast<unsigned int*>(x1 + n);
   unsigned long long* nmax = reinterpret_cast<unsigned long long*>(bar + 4);
+  int* sqd = reinterpret_cast<int*>(nmax + 1);
   // matrices start zeroed (the leading-dimension padding is never written)
   check_cuda(cudaMemsetAsync(mats, 0, 7 * mat, s), "memset");
   launch_build_lindbladian(d, zero_h, n_ops, ops, reinterpret_cast<double*>(dis), s);
@@ -238,21 +259,17 @@ void launch_grape_real(size_t d, const double* h0, const double* hc, const doubl
   assemble_real_kernel<<<eg, 256, 0, s>>>(dr, reinterpret_cast<const double2*>(h0),
                                           reinterpret_cast<const double2*>(hc), amps, dd, ld, dt, A);
   LBG_CHECK_LAUNCH("assemble_real_kernel");
-  // one norm pass fixes a common squaring count (Taylor-16: theta = 0.79)
+  // one norm pass fixes a common squaring count (Taylor-16: theta = 0.79) on the
+  // device; the host launches sq_max conditional products from an a-priori
+  // bound, each a plain copy when beyond the device count — no host round trip
   check_cuda(cudaMemsetAsync(nmax, 0, 8, s), "memset");
-  colsum_real_kernel<<<unsigned(segments), 256, 0, s>>>(A, n, ld, nmax);
+  colsum_real_kernel<<<dim3(unsigned((n + 31) / 32), unsigned(segments)), dim3(32, 8), 0, s>>>(A, n, ld, nmax);
   LBG_CHECK_LAUNCH("colsum_real_kernel");
-  unsigned long long bits = 0;
-  check_cuda(cudaMemcpyAsync(&bits, nmax, 8, cudaMemcpyDeviceToHost, s), "D2H norm");
-  check_cuda(cudaStreamSynchronize(s), "sync norm");
-  double nrm;
-  std::memcpy(&nrm, &bits, 8);
-  if (!std::isfinite(nrm)) throw invalid_argument("grape_chain: non-finite generator");
-  int sq = 0;
-  if (nrm > 0.79) sq = int(std::ceil(std::log2(nrm / 0.79)));
-  if (sq > 64) throw runtime_error("expm: norm requires more than 64 squarings");
-  if (sq > 0) {
-    scale_real_kernel<<<eg, 256, 0, s>>>(A, n, ld, std::ldexp(1.0, -sq));
+  const int sq_max = squaring_bound;
+  squarings_kernel<<<1, 1, 0, s>>>(nmax, sq_max, sqd);
+  LBG_CHECK_LAUNCH("squarings_kernel");
+  if (sq_max > 0) {
+    scale_real_kernel<<<eg, 256, 0, s>>>(A, n, ld, sqd);
     LBG_CHECK_LAUNCH("scale_real_kernel");
   }
   double c[17];
@@ -268,15 +285,15 @@ void launch_grape_real(size_t d, const double* h0, const double* hc, const doubl
   LBG_CHECK_LAUNCH("combo_real_kernel");
   for (int j = 2; j >= 0; --j) {  // T = A4 T + B_j
     mm(A4, T, M);
-    double* dst = (j == 0 && sq == 0) ? P : T;
+    double* dst = (j == 0 && sq_max == 0) ? P : T;
     combo_real_kernel<<<eg, 256, 0, s>>>(dst, M, A, A2, A3, nullptr, c[4 * j], c[4 * j + 1], c[4 * j + 2],
                                          c[4 * j + 3], 0.0, n, ld);
     LBG_CHECK_LAUNCH("combo_real_kernel");
   }
   double* cur = T;
-  for (int i = 0; i < sq; ++i) {
-    double* dst = (i == sq - 1) ? P : (cur == T ? M : T);
-    mm(cur, cur, dst);
+  for (int i = 0; i < sq_max; ++i) {  // T -> M -> T ... ending in P; copies past the device count
+    double* dst = (i == sq_max - 1) ? P : (cur == T ? M : T);
+    launch_dgemm(cur, cur, dst, n, ld, bs, st, st, st, s, sqd, i);
     cur = dst;
   }
   if (ev_build_end) check_cuda(cudaEventRecord(ev_build_end, s), "event");

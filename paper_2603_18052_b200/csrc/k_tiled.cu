@@ -398,13 +398,26 @@ __global__ void __launch_bounds__(THREADS) gemm_kernel(const double2* __restrict
                                                        double2* __restrict__ C, int n, int ld,
                                                        long long sa, long long sb, long long sc,
                                                        const __grid_constant__ CUtensorMap map_a,
-                                                       const __grid_constant__ CUtensorMap map_b) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  const Ring r = carve<G>(smem_raw);
-  init_ring(r);
+                                                       const __grid_constant__ CUtensorMap map_b,
+                                                       const int* __restrict__ cond, int cond_idx) {
   const int b = blockIdx.z, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // element offsets in units of double2: complex element = 1, real element = 1/2
   auto off = [&](long long e) { return G::REAL ? e / 2 : e; };
+  if (cond && cond_idx >= *cond) {  // device-decided no-op product: C = A on this CTA's tile
+    const int tm = (n + G::BMg - 1) / G::BMg, t = blockIdx.y * tm + blockIdx.x;
+    const int m0 = (t % tm) * G::BMg, n0 = (t / tm) * G::BN;
+    const double* src = reinterpret_cast<const double*>(A + off(b * sa));
+    double* dst = reinterpret_cast<double*>(C + off(b * sc));
+    constexpr int W = G::CPX;  // doubles per element
+    for (int e = threadIdx.x; e < G::BMg * G::BN * W; e += blockDim.x) {
+      const int i = m0 + e / (G::BN * W), jd = n0 * W + e % (G::BN * W);
+      if (i < n && jd < n * W) dst[(long long)i * ld * W + jd] = src[(long long)i * ld * W + jd];
+    }
+    return;
+  }
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const Ring r = carve<G>(smem_raw);
+  init_ring(r);
   const Problem p{A + off(b * sa), ld, B + off(b * sb), ld, C + off(b * sc), ld, n, n, n};
   const int tiles_m = (n + G::BMg - 1) / G::BMg;
   const int tile = blockIdx.y * tiles_m + blockIdx.x;
@@ -761,14 +774,14 @@ void launch_zgemm(const double* a, const double* b, double* c, int n, int batch,
   gemm_kernel<Geo<32>><<<grid, THREADS, Geo<32>::kSmemBytes, s>>>(reinterpret_cast<const double2*>(a),
                                                                    reinterpret_cast<const double2*>(b),
                                                                    reinterpret_cast<double2*>(c), n, n, stride_a,
-                                                                   stride_b, stride_c, map_a, map_b);
+                                                                   stride_b, stride_c, map_a, map_b, nullptr, 0);
   LBG_CHECK_LAUNCH("zgemm_kernel");
 }
 
 // real batched GEMM C[b] = A[b] B[b] (n x n, leading dimension ld even, batch
 // strides 0 or n*ld doubles)
 void launch_dgemm(const double* a, const double* b, double* c, int n, int ld, int batch, long long stride_a,
-                  long long stride_b, long long stride_c, cudaStream_t s) {
+                  long long stride_b, long long stride_c, cudaStream_t s, const int* cond, int cond_idx) {
   using G = StepGeoR;
   ensure_max_dyn_smem((const void*)gemm_kernel<G>, int(G::kSmemBytes));
   const long long nl = (long long)n * ld;
@@ -781,7 +794,7 @@ void launch_dgemm(const double* a, const double* b, double* c, int n, int ld, in
   gemm_kernel<G><<<grid, THREADS, G::kSmemBytes, s>>>(reinterpret_cast<const double2*>(a),
                                                       reinterpret_cast<const double2*>(b),
                                                       reinterpret_cast<double2*>(c), n, ld, stride_a, stride_b,
-                                                      stride_c, map_a, map_b);
+                                                      stride_c, map_a, map_b, cond, cond_idx);
   LBG_CHECK_LAUNCH("dgemm_kernel");
 }
 

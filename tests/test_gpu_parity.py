@@ -473,6 +473,33 @@ def test_grape_real_form_matches_complex(lbg, reference, d):
     assert np.abs(got - lbg.evolve(P, rho0, 15)).max() <= TOL_RHO
 
 
+@pytest.mark.parametrize("dt", [0.002, 0.05, 0.4])
+def test_grape_real_squarings(lbg, dt):
+    """k_grape_real.cu: the squaring count is decided on the device under a host
+    bound (conditional products that copy past the device count). dt spans no
+    squaring with bound > 0, and several squarings; the real path must match the
+    complex one (rho0 off Hermitian by one ulp) and the expm + evolve route."""
+    d = 10
+    rng = np.random.default_rng(int(dt * 1000))
+    r = rng.uniform(-1, 1, (d, d)) + 1j * rng.uniform(-1, 1, (d, d))
+    h0 = 3.0 * (r + r.conj().T)
+    r = rng.uniform(-1, 1, (d, d)) + 1j * rng.uniform(-1, 1, (d, d))
+    hc = r + r.conj().T
+    ops = [0.5 * np.diag(np.sqrt(np.arange(1, d)), 1).astype(complex), 0.2 * np.diag(np.arange(d)).astype(complex)]
+    amps = list(rng.uniform(-1, 1, 5))
+    rho0 = np.zeros((d, d), complex)
+    rho0[d - 1, d - 1] = 0.6
+    rho0[0, 0] = 0.4
+    got_r, _ = lbg.grape_chain(h0, hc, amps, 6, dt, ops, rho0)
+    r2 = rho0.copy()
+    r2[0, 1] += 1e-15
+    got_c, _ = lbg.grape_chain(h0, hc, amps, 6, dt, ops, r2)
+    assert np.abs(got_r - got_c).max() <= TOL_RHO
+    got1, _ = lbg.grape_chain(h0, hc, [amps[0]], 6, dt, ops, rho0)
+    P = lbg.expm(lbg.build_lindbladian(h0 + amps[0] * hc, ops), dt)
+    assert np.abs(got1 - lbg.evolve(P, rho0, 6)).max() <= TOL_RHO
+
+
 @pytest.mark.parametrize("n,B", [(17, 16), (33, 5), (81, 8), (97, 40), (130, 333)])
 def test_tiled_ragged_shapes_vs_torch(lbg, torch, n, B):
     """Regression: odd n (ragged last K chunk and last M tile) through the TMA /
