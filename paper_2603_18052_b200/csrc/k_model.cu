@@ -143,6 +143,44 @@ __global__ void check_state_kernel(const double2* __restrict__ x, int d, long lo
   }
 }
 
+// the same per state with one WARP per state (d >= 6): lanes split the d^2
+// Hermiticity pairs; the trace is summed by lane 0 in the reference's order, so
+// the results are bit-identical to the thread-per-state kernel
+__global__ void check_state_warp_kernel(const double2* __restrict__ x, int d, long long batch,
+                                        unsigned long long* __restrict__ keys) {
+  const long long b = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  double tr_err = 0.0, herm = 0.0, mind = 1e300;
+  if (b < batch) {
+    const double2* r = x + b * d * d;
+    for (int e = lane; e < d * d; e += 32) {
+      const int i = e / d, j = e - i * d;
+      const double2 a = r[e], c = r[j * d + i];
+      herm = fmax(herm, hypot(a.x - c.x, a.y + c.y));
+    }
+    if (lane == 0) {
+      double tre = 0.0, tim = 0.0;
+      mind = r[0].x;
+      for (int i = 0; i < d; ++i) {
+        tre += r[i * d + i].x;
+        tim += r[i * d + i].y;
+        mind = fmin(mind, r[i * d + i].x);
+      }
+      tr_err = hypot(tre - 1.0, tim);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    tr_err = fmax(tr_err, __shfl_xor_sync(0xffffffffu, tr_err, o));
+    herm = fmax(herm, __shfl_xor_sync(0xffffffffu, herm, o));
+    mind = fmin(mind, __shfl_xor_sync(0xffffffffu, mind, o));
+  }
+  if (lane == 0) {
+    atomicMax(&keys[0], okey(tr_err));
+    atomicMax(&keys[1], okey(herm));
+    atomicMin(&keys[2], okey(mind));
+  }
+}
+
 __global__ void check_state_finish(const unsigned long long* __restrict__ keys, double* out3) {
   if (threadIdx.x < 3) out3[threadIdx.x] = ounkey(keys[threadIdx.x]);
 }
@@ -285,8 +323,15 @@ void launch_check_state(const double* x, size_t d, int64_t batch, double* out3, 
   check_state_init<<<1, 32, 0, s>>>(keys);
   LBG_CHECK_LAUNCH("check_state_init");
   if (batch > 0) {
-    check_state_kernel<<<blocks_for(batch, 256), 256, 0, s>>>(reinterpret_cast<const double2*>(x), int(d), batch, keys);
-    LBG_CHECK_LAUNCH("check_state_kernel");
+    if (d >= 6) {
+      check_state_warp_kernel<<<blocks_for(batch * 32, 256), 256, 0, s>>>(reinterpret_cast<const double2*>(x),
+                                                                         int(d), batch, keys);
+      LBG_CHECK_LAUNCH("check_state_warp_kernel");
+    } else {
+      check_state_kernel<<<blocks_for(batch, 256), 256, 0, s>>>(reinterpret_cast<const double2*>(x), int(d), batch,
+                                                                 keys);
+      LBG_CHECK_LAUNCH("check_state_kernel");
+    }
   }
   check_state_finish<<<1, 32, 0, s>>>(keys, out3);
   LBG_CHECK_LAUNCH("check_state_finish");

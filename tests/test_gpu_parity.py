@@ -579,3 +579,24 @@ def test_small_d_sweep_real_vs_complex_and_oracle(lbg, torch, oracle, d, B):
         P = oracle.expm(oracle.build_lindbladian(h0 + delta[b] * hd + scale[b] * hs, ops), 0.1)
         want = np.diag(oracle.evolve(P, r0, S)).real
         assert np.abs(outs["real"][0][b] - want).max() <= TOL_RHO, b
+
+
+@pytest.mark.parametrize("d,B", [(3, 1000), (9, 257), (27, 33)])
+def test_check_state_batched_vs_oracle(lbg, torch, oracle, d, B):
+    """K6 (thread per state for d < 6, warp per state above) == the reference's
+    check_state (validate.cpp:10-30) reduced over the batch, bit for bit."""
+    rng = np.random.default_rng(d)
+    g = rng.normal(size=(B, d, d)) + 1j * rng.normal(size=(B, d, d))
+    rho = g @ np.conj(np.swapaxes(g, 1, 2))
+    rho /= np.trace(rho, axis1=1, axis2=2)[:, None, None]
+    rho[B // 2, 0, d - 1] += 3e-9  # one slightly non-Hermitian state
+    rho[B // 3, 1, 1] -= 2e-9      # and one with a trace error
+    x = torch.from_numpy(np.ascontiguousarray(rho.reshape(B, d * d))).cuda()
+    out = torch.zeros(3, dtype=torch.float64, device="cuda")
+    lbg.check_state_batched_dev(x, d, out)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    want = [oracle.check_state(r) for r in rho]
+    assert got[0] == max(w["trace_error"] for w in want)
+    assert got[1] == max(w["hermiticity_error"] for w in want)
+    assert got[2] == min(w["min_diagonal"] for w in want)
