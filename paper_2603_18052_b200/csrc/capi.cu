@@ -393,12 +393,29 @@ void host_evolve_impl(const double* p, size_t d, const double* rho0, int64_t bat
   if (batch == 0) return;
   const size_t n = d * d;
   const int64_t min_chunk = 32768;
-  // measured at c1 (ms per call): 4 -> 21.1, 8 -> 20.4, 16 -> 21.6-27 (+ outliers); one compute stream
-  // instead of two: 21.2 at 8 (kernel tails no longer overlap)
-  constexpr int64_t max_chunks = 8;
+  // measured at c1 (ms per call), equal chunks: 4 -> 21.1, 8 -> 20.4, 16 -> 21.6-27 (+ outliers); one
+  // compute stream instead of two: 21.2 at 8 (kernel tails no longer overlap). Chunk sizes ramp
+  // 1, 2, 4, ..., 4, 2, 1 (10 chunks) so only a small first H2D and a small last D2H are exposed:
+  // 20.19 vs 20.48 ms for 8 equal chunks in the same run (1, 2, 4, 8 ramp over 12: no better).
+  constexpr int64_t max_chunks = 10;
   static_assert(max_chunks <= kMaxChunks, "events per chunk");
   const int nchunks = (single || batch < 2 * min_chunk) ? 1 : int(std::min<int64_t>(max_chunks, batch / min_chunk));
-  const int64_t chunk = (batch + nchunks - 1) / nchunks;
+  int64_t bounds[kMaxChunks + 1];
+  {
+    int64_t wsum = 0, wts[kMaxChunks];
+    for (int c = 0; c < nchunks; ++c) {
+      wts[c] = int64_t(1) << std::min(std::min(c, nchunks - 1 - c), 2);
+      wsum += wts[c];
+    }
+    int64_t acc = 0;
+    bounds[0] = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      acc += wts[c];
+      bounds[c + 1] = batch * acc / wsum;
+    }
+  }
+  int64_t chunk = 0;
+  for (int c = 0; c < nchunks; ++c) chunk = std::max(chunk, bounds[c + 1] - bounds[c]);
   EvolvePool& pool = evolve_pool();
   std::lock_guard<std::mutex> lk(pool.mu);
   pool.ensure(n * n * 16, size_t(batch) * n * 16, size_t(nchunks) * 3 * 8, work_bytes(chunk));
@@ -409,7 +426,7 @@ void host_evolve_impl(const double* p, size_t d, const double* rho0, int64_t bat
   check_cuda(cudaMemcpyAsync(dp, p, n * n * 16, cudaMemcpyHostToDevice, sh), "H2D P");
   int used = 0;
   for (int c = 0; c < nchunks; ++c) {
-    const int64_t b0 = c * chunk, nb = std::min<int64_t>(chunk, batch - b0);
+    const int64_t b0 = bounds[c], nb = bounds[c + 1] - bounds[c];
     if (nb <= 0) break;
     double* xc = dx + size_t(b0) * n * 2;
     const size_t bytes = size_t(nb) * n * 16;
