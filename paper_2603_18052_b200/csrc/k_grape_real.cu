@@ -158,15 +158,14 @@ constexpr int RT = 256;
 __device__ __forceinline__ void grid_sync_r(unsigned int* bar, unsigned int target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(bar, 1u);
+    // release-add (no separate membar) after the CTA barrier: cumulativity carries the
+    // other warps' stores; the acquire poll orders the reloads after it
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(bar) : "memory");
     while (true) {
       unsigned int v;
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(bar) : "memory");
       if (v >= target) break;
-      __nanosleep(32);
     }
-    __threadfence();
   }
   __syncthreads();
 }
@@ -301,6 +300,8 @@ void launch_grape_real(size_t d, const double* h0, const double* hc, const doubl
   rho_to_x_real_kernel<<<(n + 255) / 256, 256, 0, s>>>(reinterpret_cast<const double2*>(x_rho), dd, x0);
   LBG_CHECK_LAUNCH("rho_to_x_real_kernel");
   check_cuda(cudaMemsetAsync(bar, 0, 4, s), "memset");
+  // measured (50 x 32 steps at d = 27): 148 CTAs 1.90 ms, 96 1.96, 74 2.46, 37 3.20 — the
+  // per-CTA row work, not the barrier's participant count, sets the step time
   const int grid = std::min(sm_count(), n);
   const int rows_max = (n + grid - 1) / grid;
   const size_t smem = (size_t(rows_max) * n + n) * 8;

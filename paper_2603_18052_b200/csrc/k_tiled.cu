@@ -447,15 +447,14 @@ struct StepCtl {
 __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(bar, 1u);
+    // release-add after the CTA barrier (cumulativity carries the other warps'
+    // stores; no full membar), acquire poll (no trailing fence needed)
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(bar) : "memory");
     while (true) {
       unsigned int v;
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(bar) : "memory");
       if (v >= target) break;
-      __nanosleep(64);
     }
-    __threadfence();
   }
   __syncthreads();
 }
