@@ -320,10 +320,8 @@ __device__ __forceinline__ void consume(const Ring& r, const Problem& p, int til
         for (int ni = 0; ni < NI; ++ni)
           __stcg(dst + ((warp * MI + mi) * NI + ni) * 32 + lane, make_double2(acc[mi][ni][0], acc[mi][ni][1]));
       consumer_bar();
-      if (warp == 0 && lane == 0) {
-        __threadfence();
+      if (warp == 0 && lane == 0)  // release store: cumulative over the warps' partials (consumer barrier)
         asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(sk->flags + tile), "r"(sk->epoch) : "memory");
-      }
       continue;
     }
     if (sk && hi < nk - 1) {  // HEAD part: add the TAIL partial, then store
@@ -332,7 +330,6 @@ __device__ __forceinline__ void consume(const Ring& r, const Problem& p, int til
           unsigned v;
           asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(sk->flags + tile) : "memory");
           if (v == sk->epoch) break;
-          __nanosleep(32);
         }
       }
       consumer_bar();
