@@ -368,15 +368,17 @@ def run_ours(args):
         if torch.distributed.is_initialized():
             torch.distributed.barrier()
         calls = []
-        for _ in range(reps):
-            t0 = time.perf_counter()
-            call()
-            calls.append(time.perf_counter() - t0)
+        with Clocks(local) as eclk:  # clocks during the host-buffer calls too
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                call()
+                calls.append(time.perf_counter() - t0)
         e2e_s = max_over_ranks(torch, float(np.median(calls)))
         e2e = {"value": world * B * S / e2e_s, "unit": "traj-steps/s",
                "h2d_bytes_per_step": int(host_in.nbytes + Pc.nbytes), "d2h_bytes_per_step": int(host_out.nbytes),
                "ms_per_call": e2e_s * 1e3, "ms_per_call_all": [c * 1e3 for c in calls],
-               "call": "lbg_evolve_shared_p (host buffers, synchronous); median of the calls"}
+               "call": "lbg_evolve_shared_p (host buffers, synchronous); median of the calls",
+               "clocks": eclk.summary()}
     else:
         e2e = sweep.e2e(reps=2)
         e2e["value"] = e2e["value"] * world
