@@ -516,7 +516,8 @@ def extra_configs(torch, lbg, R, peak):
                                      "frac": exec_tf / peak,
                                      "counted": ("executed real-form flops: build 5 x 2 x 81^3 per trajectory + "
                                                  "steps 2 x 81^2 per traj-step"),
-                                     "reference_form_8d4_tflops": tf}
+                                     "reference_form_8d4_tflops": tf,
+                                     "reference_form_8d4_frac": tf / peak}
                 # report the build (K5 + K4) separately -> a steps=0 pass
                 case.args[-1] = 0
                 tb, pb, _ = R.time_passes(case.run, 3, 1)
