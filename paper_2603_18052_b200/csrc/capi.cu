@@ -322,7 +322,7 @@ int lbg_build_lindbladian(size_t d, const double* h, size_t n_ops, const double*
   });
 }
 
-size_t lbg_expm_workspace(size_t n) { return 6 * n * n * 16; }
+size_t lbg_expm_workspace(size_t n) { return expm_workspace(n); }
 
 int lbg_expm_dev(const double* a, size_t n, double dt, double* out, double* work, void* stream) {
   return guarded([&] {

@@ -95,6 +95,11 @@ void launch_dgemm(const double* a, const double* b, double* c, int n, int ld, in
 // model kernels (k_model.cu)
 void launch_build_lindbladian(std::size_t d, const double* h, std::size_t n_ops,
                               const double* ops, double* out, cudaStream_t s);
+constexpr std::size_t kExpmStreamN = 128;  // expm products on the stream-K engine from here
+std::size_t expm_workspace(std::size_t n);  // bytes (lbg_expm_workspace)
+// one complex GEMM C = A B (n x n) on the persistent stream-K engine (k_tiled.cu)
+std::size_t zgemm_stream_workspace(int n);
+void launch_zgemm_stream(const double* a, const double* b, double* c, int n, void* aux, cudaStream_t s);
 void expm_dev(const double* a, std::size_t n, double dt, double* out, double* work,
               cudaStream_t s);
 void launch_check_state(const double* x, std::size_t d, int64_t batch, double* out3,

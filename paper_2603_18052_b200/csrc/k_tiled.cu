@@ -671,14 +671,21 @@ __global__ void convert_real_kernel(double* __restrict__ x, double* __restrict__
 }
 
 // persistent cooperative stepping for geometry G; v0 already holds V[k][b]
+// stream-K control, split-tile partials and flags (after the two state buffers)
 template <class G>
-void run_tiled(const double* p_dev, size_t ldp, size_t n, int64_t batch, int64_t steps, void* work, cudaStream_t s) {
-  char* w = static_cast<char*>(work);
+size_t aux_workspace_of(size_t n, int64_t batch) {
+  const size_t nt = ntiles_of<G>(n, batch);
+  return align_up(sizeof(StepCtl)) + align_up(nt * slot_of<G>() * sizeof(double2)) + align_up(nt * sizeof(unsigned int));
+}
+
+// the persistent stream-K engine on caller-given state buffers: v0 holds V_0,
+// step s reads V_s and writes V_{s+1} into the other buffer (v1 after an odd
+// count). aux: aux_workspace_of<G>(n, batch) bytes.
+template <class G>
+void run_tiled_ext(const double* p_dev, size_t ldp, size_t n, int64_t batch, int64_t steps, double2* v0, double2* v1,
+                   void* aux, cudaStream_t s) {
   const size_t ldv = ldv_of<G>(batch);
-  const size_t vbytes = size_t(G::CPX) * 8 * n * ldv;
-  double2* v0 = reinterpret_cast<double2*>(w);
-  double2* v1 = reinterpret_cast<double2*>(w + align_up(vbytes));
-  StepCtl* ctl = reinterpret_cast<StepCtl*>(w + 2 * align_up(vbytes));
+  StepCtl* ctl = static_cast<StepCtl*>(aux);
   const size_t nt = ntiles_of<G>(n, batch);
   double2* part = reinterpret_cast<double2*>(reinterpret_cast<char*>(ctl) + align_up(sizeof(StepCtl)));
   unsigned int* flags =
@@ -716,6 +723,14 @@ void run_tiled(const double* p_dev, size_t ldp, size_t n, int64_t batch, int64_t
   check_cuda(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(THREADS), args, G::kSmemBytes, s),
              "tiled_evolve_kernel (cooperative)");
   note_launch();
+}
+
+template <class G>
+void run_tiled(const double* p_dev, size_t ldp, size_t n, int64_t batch, int64_t steps, void* work, cudaStream_t s) {
+  char* w = static_cast<char*>(work);
+  const size_t vbytes = size_t(G::CPX) * 8 * n * ldv_of<G>(batch);
+  run_tiled_ext<G>(p_dev, ldp, n, batch, steps, reinterpret_cast<double2*>(w),
+                   reinterpret_cast<double2*>(w + align_up(vbytes)), w + 2 * align_up(vbytes), s);
 }
 
 void launch_tiled_evolve(const double* p_dev, size_t n, double* x_re, double* x_im, double* x_aos,
@@ -772,6 +787,16 @@ void launch_zgemm(const double* a, const double* b, double* c, int n, int batch,
                                                                    reinterpret_cast<double2*>(c), n, n, stride_a,
                                                                    stride_b, stride_c, map_a, map_b, nullptr, 0);
   LBG_CHECK_LAUNCH("zgemm_kernel");
+}
+
+// one complex GEMM C = A B (n x n, AoS, C distinct from A and B) on the
+// persistent stream-K engine: a single product has n/32 x n/32 tiles, which
+// one-tile-per-CTA launches quantise into partial waves (n = 729: 529 tiles on
+// 444 slots = 2 waves at 60%); stream-K spreads them evenly.
+size_t zgemm_stream_workspace(int n) { return aux_workspace_of<StepGeo>(size_t(n), n); }
+void launch_zgemm_stream(const double* a, const double* b, double* c, int n, void* aux, cudaStream_t s) {
+  run_tiled_ext<StepGeo>(a, size_t(n), size_t(n), n, 1, reinterpret_cast<double2*>(const_cast<double*>(b)),
+                         reinterpret_cast<double2*>(c), aux, s);
 }
 
 // real batched GEMM C[b] = A[b] B[b] (n x n, leading dimension ld even, batch
