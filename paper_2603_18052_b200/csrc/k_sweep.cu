@@ -77,18 +77,25 @@ __global__ void combo_batched_kernel(double2* __restrict__ out, const double2* _
   out[o] = v;
 }
 
-// per-trajectory 1-norm (max column sum of moduli), max-reduced into *nmax
+// max over the batch of the 1-norms (max column sum of |A|): block = 32 columns
+// x 8 row groups of one matrix (coalesced rows, 8-way parallel column sums)
 __global__ void sweep_norm_kernel(const double2* __restrict__ A, int n, long long stride,
                                   unsigned long long* __restrict__ nmax) {
-  const int b = blockIdx.x;
-  double best = 0.0;
-  for (int c = threadIdx.x; c < n; c += blockDim.x) {
-    double s = 0.0;
-    for (int r = 0; r < n; ++r) s += hypot(A[b * stride + (long long)r * n + c].x, A[b * stride + (long long)r * n + c].y);
-    best = fmax(best, s);
+  __shared__ double part[8][33];
+  const int tx = threadIdx.x, ty = threadIdx.y, c = blockIdx.x * 32 + tx;
+  const double2* m = A + (long long)blockIdx.y * stride;
+  double sum = 0.0;
+  if (c < n)
+    for (int r = ty; r < n; r += 8) sum += hypot(m[(long long)r * n + c].x, m[(long long)r * n + c].y);
+  part[ty][tx] = sum;
+  __syncthreads();
+  if (ty == 0) {
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += part[k][tx];
+    for (int o = 16; o > 0; o >>= 1) t = fmax(t, __shfl_xor_sync(0xffffffffu, t, o));
+    if (tx == 0) atomicMax(nmax, (unsigned long long)__double_as_longlong(t));
   }
-  for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(nmax, (unsigned long long)__double_as_longlong(best));
 }
 
 // K3: one CTA per trajectory, P_b resident in shared memory (row stride n = 81
@@ -247,7 +254,7 @@ void propagators_complex(size_t d, const double* h0, const double* hd, const dou
         dis, reinterpret_cast<const double2*>(h0), reinterpret_cast<const double2*>(hd),
         reinterpret_cast<const double2*>(hs), delta + c0, scale + c0, int(d), dt, M[0], nn);
     LBG_CHECK_LAUNCH("sweep_assemble_kernel");
-    sweep_norm_kernel<<<cb, 128, 0, s>>>(M[0], n, nn, nmax);
+    sweep_norm_kernel<<<dim3(unsigned((n + 31) / 32), unsigned(cb)), dim3(32, 8), 0, s>>>(M[0], n, nn, nmax);
     LBG_CHECK_LAUNCH("sweep_norm_kernel");
   }
   unsigned long long bits = 0;
