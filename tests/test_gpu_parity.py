@@ -600,3 +600,29 @@ def test_check_state_batched_vs_oracle(lbg, torch, oracle, d, B):
     assert got[0] == max(w["trace_error"] for w in want)
     assert got[1] == max(w["hermiticity_error"] for w in want)
     assert got[2] == min(w["min_diagonal"] for w in want)
+
+
+def test_barrier_kernels_bitwise_deterministic(lbg, torch, reference):
+    """The grid-barrier / stream-K kernels (K1c complex and real, the real GRAPE
+    chain) reduce in a fixed order: two runs give identical bits. A broken
+    release/acquire barrier shows up here as run-to-run differences."""
+    d, B, S = 27, 256, 40
+    h, ops = lbg.config_model(3)
+    P = lbg.expm(lbg.build_lindbladian(h, ops), 0.1)
+    rho0 = lbg.ginibre_batch(3, 0, B, d)
+    a = lbg.evolve_batch(P, rho0, S, algo="tiled")
+    b = lbg.evolve_batch(P, rho0, S, algo="tiled")
+    assert np.array_equal(a, b)
+    dev = torch.device("cuda")
+    outs = []
+    for _ in range(2):
+        x = torch.from_numpy(rho0.copy()).to(dev)
+        work = torch.empty(lbg.density_workspace(d * d, B), dtype=torch.uint8, device=dev)
+        lbg.evolve_density_dev(torch.from_numpy(P).to(dev), x, S, work)
+        torch.cuda.synchronize()
+        outs.append(x.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
+    h0, hc, op, amps, dt, r0 = reference.grape_inputs(27, 4)
+    g1, _ = lbg.grape_chain(h0, hc, amps, 16, dt, op, r0)
+    g2, _ = lbg.grape_chain(h0, hc, amps, 16, dt, op, r0)
+    assert np.array_equal(g1, g2)
