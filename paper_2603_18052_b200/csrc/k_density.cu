@@ -19,6 +19,7 @@
 // variant of the K1c tile engine (k_tiled.cu), and K1b-R `smem_real_kernel`
 // (n <= 84: P_R resident in shared memory, real m8n8k4 DMMA, 32 vectors/CTA,
 // 8 warps balanced over the 4 SMSPs).
+#include <algorithm>
 #include <map>
 #include <mutex>
 
@@ -288,9 +289,19 @@ template <int N, int MG>
 void launch_smem_real(const double* pr, int n, double* x, int64_t count, int64_t half, const int* flag,
                       int64_t steps, cudaStream_t s) {
   const RGeom g(n);
-  ensure_max_dyn_smem((const void*)smem_real_kernel<N, MG>, int(g.total));
-  smem_real_kernel<N, MG><<<unsigned((count + kVec - 1) / kVec), 32 * kWarpsR, g.total, s>>>(pr, n, x, count, half,
-                                                                                             flag, steps);
+  // one CTA per SM: the 8 warps are balanced over the 4 sub-partitions for ONE
+  // CTA, and when the block scheduler stacks two live CTAs on an SM (observed
+  // under ncu: 64 SMs x 2 instead of 128 x 1, 4.35 vs 2.2 ms at config 2) they
+  // share its tensor pipes while other SMs idle. Asking for more than half the
+  // SM's shared memory pins the residency to one.
+  int dev = 0;
+  check_cuda(cudaGetDevice(&dev), "device");
+  int smem_sm = 0;
+  check_cuda(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev), "attr");
+  const size_t bytes = std::max(g.total, size_t(smem_sm / 2 + 1024));
+  ensure_max_dyn_smem((const void*)smem_real_kernel<N, MG>, int(bytes));
+  smem_real_kernel<N, MG><<<unsigned((count + kVec - 1) / kVec), 32 * kWarpsR, bytes, s>>>(pr, n, x, count, half,
+                                                                                          flag, steps);
   LBG_CHECK_LAUNCH("smem_real_kernel");
 }
 
