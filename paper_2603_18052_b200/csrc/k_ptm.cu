@@ -31,6 +31,7 @@
 //   SM. Epilogue: populations + ensemble sum.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.hpp"
@@ -300,6 +301,287 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+// K4, balanced: the DMMA tiles cover rows / columns / k 0..79 only (10 x 10
+// output tiles, 20 k-steps: 2,000 DMMAs per product instead of 11 x 11 x 21 =
+// 2,541, whose last m-tile, n-tile and k-step carry one real row / column / k
+// each), 20 warps = five per sub-partition own 5 tiles each (half an n-tile
+// column), so every sub-partition issues exactly 500 DMMAs per product (the
+// 11-warp kernel: 693 on three of them). The 81st row / column go to DFMA:
+// the k = 80 term is a rank-1 update on each lane's own tile entries, and the
+// 161 fringe entries (column 80, rows 0..79, and row 80) are dot products
+// split over 4 lanes (k = kq mod 4) and shuffle-reduced. Four 81 x 84
+// matrices (A, A^2, A^3, T: 213 KB) in shared memory; the Horner epilogues
+// read A and A^2 there, T is updated in place between two barriers.
+constexpr int RS2 = 84;                      // = 4 (mod 16): conflict-free DMMA fragments
+constexpr int MAT2 = N * RS2;                // doubles per matrix (81 rows)
+constexpr int E_WARPS = 20, E_THREADS = 32 * E_WARPS;
+constexpr int EMT = 5, EKT = 20;             // m-tiles per warp, DMMA k-steps (k < 80)
+constexpr int E_PARTS = 7, E_PROWS = 12;     // combine pass: 7 row parts x 81 columns
+constexpr int FRINGE = 2 * 80 + 1;           // column 80 (rows < 80) + row 80
+static_assert(E_PARTS * 81 <= E_THREADS && E_PARTS * E_PROWS >= N, "combine pass");
+static_assert(4 * MAT2 * 8 + E_PARTS * RS2 * 8 + 64 <= 232448, "shared memory");
+
+struct TaylorCoef {
+  double v[15];
+};
+constexpr TaylorCoef make_taylor() {
+  TaylorCoef c{};
+  c.v[0] = 1.0;
+  for (int k = 1; k < 15; ++k) c.v[k] = c.v[k - 1] / k;
+  return c;
+}
+__constant__ TaylorCoef c_taylor = make_taylor();
+
+__global__ void ptm_terms2_kernel(const double2* __restrict__ dis, const double2* __restrict__ h0,
+                                  const double2* __restrict__ hd, const double2* __restrict__ hs, double dt,
+                                  double* __restrict__ terms) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= MAT2) return;
+  const int q = e / RS2, s = e - q * RS2;
+  const bool in = s < N;
+  terms[e] = in ? dt * (real_entry([&](int p) { return dis[q * N + p]; }, q, s) +
+                        real_entry([&](int p) { return kron_c(h0, q, p); }, q, s))
+                : 0.0;
+  terms[MAT2 + e] = in ? dt * real_entry([&](int p) { return kron_c(hd, q, p); }, q, s) : 0.0;
+  terms[2 * MAT2 + e] = in ? dt * real_entry([&](int p) { return kron_c(hs, q, p); }, q, s) : 0.0;
+}
+
+struct Fringe {  // this lane's fringe dot products (the second only in warp 0)
+  int r[2], c[2];
+  bool own[2];   // lane kq == 0 of a valid dot: holds and stores the entry
+};
+__device__ __forceinline__ void fringe_rc(int d, int& r, int& c) {
+  if (d < 80) r = d, c = 80;
+  else r = 80, c = d - 80;
+}
+
+// (X Y) at this lane's tile entries (acc) and fringe entries (f)
+__device__ __forceinline__ void mm2(const double* __restrict__ X, const double* __restrict__ Y,
+                                    double (&acc)[EMT][2], double (&f)[2], const Fringe& fr, int w, int lane) {
+  const int g = lane >> 2, t = lane & 3, nt = w >> 1, mh = w & 1;
+#pragma unroll
+  for (int m = 0; m < EMT; ++m) acc[m][0] = acc[m][1] = 0.0;
+  const double* xa = X + (mh * EMT * 8 + g) * RS2 + t;
+  const double* yb = Y + t * RS2 + nt * 8 + g;
+#pragma unroll 4
+  for (int k = 0; k < EKT; ++k) {
+    const double b = yb[k * 4 * RS2];
+    double a[EMT];
+#pragma unroll
+    for (int m = 0; m < EMT; ++m) a[m] = xa[m * 8 * RS2 + k * 4];
+#pragma unroll
+    for (int m = 0; m < EMT; ++m) dmma(acc[m], a[m], b);
+  }
+  {  // k = 80: rank-1 update of the own entries
+    const double2 y = *reinterpret_cast<const double2*>(Y + 80 * RS2 + nt * 8 + 2 * t);
+#pragma unroll
+    for (int m = 0; m < EMT; ++m) {
+      const double x = X[((mh * EMT + m) * 8 + g) * RS2 + 80];
+      acc[m][0] = fma(x, y.x, acc[m][0]);
+      acc[m][1] = fma(x, y.y, acc[m][1]);
+    }
+  }
+  const int kq = lane & 3;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    if (i == 1 && w != 0) break;  // warp-uniform: only warp 0 has a second fringe dot
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    const double* xr = X + fr.r[i] * RS2;
+    const double* yc = Y + fr.c[i];
+#pragma unroll
+    for (int j = 0; j < 21; ++j) {  // k = kq + 4 j <= 80: 21 terms for kq = 0, 20 otherwise
+      const int k = kq + 4 * j;
+      if (j == 20 && kq != 0) break;
+      const double v = xr[k], y = yc[k * RS2];
+      if (j % 3 == 0)
+        s0 = fma(v, y, s0);
+      else if (j % 3 == 1)
+        s1 = fma(v, y, s1);
+      else
+        s2 = fma(v, y, s2);
+    }
+    double sum = (s0 + s1) + s2;
+    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+    f[i] = sum;
+  }
+}
+
+// acc = (with_acc ? acc : 0) + c0 I + c1 A + c2 A^2 at the own entries (A, A^2 from shared memory)
+__device__ __forceinline__ void epi2(double (&acc)[EMT][2], double (&f)[2], const Fringe& fr,
+                                     const double* __restrict__ SA, const double* __restrict__ SA2, double c0,
+                                     double c1, double c2, bool with_acc, int w, int lane) {
+  const int g = lane >> 2, t = lane & 3, nt = w >> 1, mh = w & 1;
+#pragma unroll
+  for (int m = 0; m < EMT; ++m) {
+    const int r = (mh * EMT + m) * 8 + g, col = nt * 8 + 2 * t;
+    const double2 a1 = *reinterpret_cast<const double2*>(SA + r * RS2 + col);
+    const double2 a2 = *reinterpret_cast<const double2*>(SA2 + r * RS2 + col);
+    double x0 = (with_acc ? acc[m][0] : 0.0) + c1 * a1.x + c2 * a2.x;
+    double x1 = (with_acc ? acc[m][1] : 0.0) + c1 * a1.y + c2 * a2.y;
+    if (r == col) x0 += c0;
+    if (r == col + 1) x1 += c0;
+    acc[m][0] = x0;
+    acc[m][1] = x1;
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    if (i == 1 && w != 0) break;
+    const int o = fr.r[i] * RS2 + fr.c[i];
+    double x = (with_acc ? f[i] : 0.0) + c1 * SA[o] + c2 * SA2[o];
+    if (fr.r[i] == fr.c[i]) x += c0;
+    f[i] = x;
+  }
+}
+
+__device__ __forceinline__ void store2(double* __restrict__ Z, const double (&acc)[EMT][2], const double (&f)[2],
+                                       const Fringe& fr, int w, int lane) {
+  const int g = lane >> 2, t = lane & 3, nt = w >> 1, mh = w & 1;
+#pragma unroll
+  for (int m = 0; m < EMT; ++m)
+    *reinterpret_cast<double2*>(Z + ((mh * EMT + m) * 8 + g) * RS2 + nt * 8 + 2 * t) =
+        make_double2(acc[m][0], acc[m][1]);
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+    if (fr.own[i]) Z[fr.r[i] * RS2 + fr.c[i]] = f[i];
+}
+
+__global__ void __launch_bounds__(E_THREADS, 1)
+    ptm_expm2_kernel(const double* __restrict__ terms, const double* __restrict__ delta,
+                     const double* __restrict__ scale, double* __restrict__ p_out) {
+  extern __shared__ __align__(16) double sm[];
+  double* SA = sm;
+  double* SA2 = sm + MAT2;
+  double* SA3 = sm + 2 * MAT2;
+  double* ST = sm + 3 * MAT2;
+  __shared__ double colpart[E_PARTS][RS2];
+  __shared__ int s_sq, s_deg12;
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int b = blockIdx.x;
+  // dt C0 / dt Cd / dt Cs -> SA / SA2 / SA3: three bulk async copies on one mbarrier
+  const unsigned sb32 = static_cast<unsigned>(__cvta_generic_to_shared(&bar));
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sb32));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sb32), "r"(unsigned(3 * MAT2 * 8))
+                 : "memory");
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+              static_cast<unsigned>(__cvta_generic_to_shared(sm + i * MAT2))),
+          "l"(terms + i * MAT2), "r"(unsigned(MAT2 * 8)), "r"(sb32)
+          : "memory");
+  }
+  const double db = delta[b], sb = scale[b];
+  // this lane's fringe dots: virtual lane v = tid (+ E_THREADS in warp 0), dot v / 4, k phase v % 4
+  Fringe fr;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int v = tid + i * E_THREADS, d = v >> 2;
+    const bool valid = d < FRINGE;
+    fringe_rc(valid ? d : 0, fr.r[i], fr.c[i]);
+    fr.own[i] = valid && (v & 3) == 0 && (i == 0 || w == 0);
+  }
+  __syncthreads();  // barrier initialised
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra WAIT_%=;\n}\n" ::"r"(
+          sb32)
+      : "memory");
+  // A = dt C0 + delta dt Cd + s dt Cs in place in SA, fused with the column sums of ||A||_1
+  if (tid < E_PARTS * 81) {
+    const int c = tid % 81, q0 = (tid / 81) * E_PROWS;
+    double cs = 0.0;
+#pragma unroll 2
+    for (int r = q0; r < q0 + E_PROWS && r < N; ++r) {
+      const int o = r * RS2 + c;
+      const double v = fma(sb, SA3[o], fma(db, SA2[o], SA[o]));
+      SA[o] = v;
+      cs += fabs(v);
+    }
+    colpart[tid / 81][c] = cs;
+  }
+  __syncthreads();
+  if (w == 0) {  // ||A||_1 -> squarings (per trajectory)
+    double nrm = 0.0;
+    for (int c = lane; c < N; c += 32) {
+      double cs = 0.0;
+#pragma unroll
+      for (int p = 0; p < E_PARTS; ++p) cs += colpart[p][c];
+      nrm = fmax(nrm, cs);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nrm = fmax(nrm, __shfl_xor_sync(0xffffffffu, nrm, o));
+    if (lane == 0) {
+      s_sq = nrm > kTheta14 ? int(ceil(log2(nrm / kTheta14))) : 0;
+      s_deg12 = nrm <= kTheta12;
+    }
+  }
+  __syncthreads();
+  const int sq = s_sq;
+  const bool deg12 = s_deg12;
+  if (sq > 0) {
+    const double sc = ldexp(1.0, -sq);
+    for (int e = tid; e < N * N; e += E_THREADS) {
+      const int q = e / N, s = e - q * N;
+      SA[q * RS2 + s] *= sc;
+    }
+    __syncthreads();
+  }
+  const double* cf = c_taylor.v;
+  double acc[EMT][2], f[2] = {0.0, 0.0};
+  mm2(SA, SA, acc, f, fr, w, lane);  // A^2
+  store2(SA2, acc, f, fr, w, lane);
+  __syncthreads();
+  mm2(SA2, SA, acc, f, fr, w, lane);  // A^3
+  store2(SA3, acc, f, fr, w, lane);
+  int j0;
+  if (deg12) {  // T = B3 + c12 A3 (B4 = c12 I: no product)
+#pragma unroll
+    for (int m = 0; m < EMT; ++m) acc[m][0] *= cf[12], acc[m][1] *= cf[12];
+    f[0] *= cf[12];
+    f[1] *= cf[12];
+    epi2(acc, f, fr, SA, SA2, cf[9], cf[10], cf[11], true, w, lane);
+    j0 = 2;
+  } else {  // T = B4
+    epi2(acc, f, fr, SA, SA2, cf[12], cf[13], cf[14], false, w, lane);
+    j0 = 3;
+  }
+  store2(ST, acc, f, fr, w, lane);
+  __syncthreads();
+#pragma unroll 1
+  for (int j = j0; j >= 0; --j) {  // T = B_j + A3 T
+    mm2(SA3, ST, acc, f, fr, w, lane);
+    epi2(acc, f, fr, SA, SA2, cf[3 * j], cf[3 * j + 1], cf[3 * j + 2], true, w, lane);
+    if (j > 0 || sq > 0) {
+      __syncthreads();  // every warp is done reading T
+      store2(ST, acc, f, fr, w, lane);
+      __syncthreads();
+    }
+  }
+  for (int i = 0; i < sq; ++i) {  // squarings
+    mm2(ST, ST, acc, f, fr, w, lane);
+    if (i + 1 < sq) {
+      __syncthreads();
+      store2(ST, acc, f, fr, w, lane);
+      __syncthreads();
+    }
+  }
+  // ---- P_R -> global (n x n, unpadded) ----
+  double* out = p_out + size_t(b) * N * N;
+  const int g = lane >> 2, t = lane & 3, nt = w >> 1, mh = w & 1;
+#pragma unroll
+  for (int m = 0; m < EMT; ++m) {  // rows of 81 doubles: odd rows are not 16-byte aligned
+    double* o = out + ((mh * EMT + m) * 8 + g) * N + nt * 8 + 2 * t;
+    o[0] = acc[m][0];
+    o[1] = acc[m][1];
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+    if (fr.own[i]) out[fr.r[i] * N + fr.c[i]] = f[i];
+}
+
 // K3: x <- P_R x for `steps` steps, P_R register resident.
 // P_R is padded to 84 x 84 and cut into 4-row x 21-column blocks: one block
 // (84 doubles) per thread, the 4 column blocks of a row group in 4 adjacent
@@ -485,6 +767,41 @@ __global__ void x_to_rho_kernel(const double* __restrict__ x, double2* __restric
     rho[p] = make_double2(x[j * D + i], -x[p]);
 }
 
+bool expm_v2() {  // A/B switch: LBG_PTM_EXPM=1 selects the 11-warp kernel
+  static const bool v2 = [] {
+    const char* e = std::getenv("LBG_PTM_EXPM");
+    return !(e && std::atoi(e) == 1);
+  }();
+  return v2;
+}
+void launch_terms(const double2* dis, const double* h0, const double* hd, const double* hs, double dt,
+                  double* terms, cudaStream_t s) {
+  const auto* H0 = reinterpret_cast<const double2*>(h0);
+  const auto* HD = reinterpret_cast<const double2*>(hd);
+  const auto* HS = reinterpret_cast<const double2*>(hs);
+  if (expm_v2()) {
+    ptm_terms2_kernel<<<(MAT2 + 255) / 256, 256, 0, s>>>(dis, H0, HD, HS, dt, terms);
+    LBG_CHECK_LAUNCH("ptm_terms2_kernel");
+  } else {
+    ptm_terms_kernel<<<(MAT + 255) / 256, 256, 0, s>>>(dis, H0, HD, HS, dt, terms);
+    LBG_CHECK_LAUNCH("ptm_terms_kernel");
+  }
+}
+void launch_expm(const double* terms, const double* delta, const double* scale, double* pr, int count,
+                 cudaStream_t s) {
+  if (expm_v2()) {
+    const size_t smem = size_t(4) * MAT2 * 8;
+    ensure_max_dyn_smem((const void*)ptm_expm2_kernel, int(smem));
+    ptm_expm2_kernel<<<count, E_THREADS, smem, s>>>(terms, delta, scale, pr);
+    LBG_CHECK_LAUNCH("ptm_expm2_kernel");
+  } else {
+    const size_t smem = size_t(3) * MAT * 8;
+    ensure_max_dyn_smem((const void*)ptm_expm_kernel, int(smem));
+    ptm_expm_kernel<<<count, THREADS, smem, s>>>(terms, delta, scale, pr);
+    LBG_CHECK_LAUNCH("ptm_expm_kernel");
+  }
+}
+
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 constexpr int64_t kChunk = 16384;
 
@@ -516,18 +833,12 @@ void launch_ptm_sweep(size_t d, const double* h0, const double* hd, const double
   check_cuda(cudaMemsetAsync(ens_x, 0, N * 8, s), "memset");
   check_cuda(cudaMemsetAsync(pr, 0, d * d * 16, s), "memset");
   launch_build_lindbladian(d, pr, n_ops, ops, reinterpret_cast<double*>(dis), s);
-  ptm_terms_kernel<<<(MAT + 255) / 256, 256, 0, s>>>(dis, reinterpret_cast<const double2*>(h0),
-                                                     reinterpret_cast<const double2*>(hd),
-                                                     reinterpret_cast<const double2*>(hs), dt, terms);
-  LBG_CHECK_LAUNCH("ptm_terms_kernel");
+  launch_terms(dis, h0, hd, hs, dt, terms, s);
   rho_to_x_kernel<<<1, 96, 0, s>>>(reinterpret_cast<const double2*>(rho0), x0);
   LBG_CHECK_LAUNCH("rho_to_x_kernel");
-  const size_t smem = size_t(3) * MAT * 8;
-  ensure_max_dyn_smem((const void*)ptm_expm_kernel, int(smem));
   for (int64_t c0 = 0; c0 < batch; c0 += int64_t(chunk)) {
     const int cb = int(std::min<int64_t>(int64_t(chunk), batch - c0));
-    ptm_expm_kernel<<<cb, THREADS, smem, s>>>(terms, delta + c0, scale + c0, pr);
-    LBG_CHECK_LAUNCH("ptm_expm_kernel");
+    launch_expm(terms, delta + c0, scale + c0, pr, cb, s);
     ptm_step_kernel<<<unsigned((cb + STEP_TRAJ - 1) / STEP_TRAJ), STEP_THREADS, 0, s>>>(
         pr, x0, cb, steps, pops + c0 * int64_t(D), ens_x);
     LBG_CHECK_LAUNCH("ptm_step_kernel");
@@ -558,14 +869,8 @@ void launch_ptm_grape(const double* h0, const double* hc, const double* zero_h, 
   double* zeros = reinterpret_cast<double*>(reinterpret_cast<char*>(terms) + align_up(size_t(3) * MAT * 8));
   check_cuda(cudaMemsetAsync(zeros, 0, size_t(segments) * 8, s), "memset");
   launch_build_lindbladian(size_t(D), zero_h, n_ops, ops, reinterpret_cast<double*>(dis), s);
-  ptm_terms_kernel<<<(MAT + 255) / 256, 256, 0, s>>>(dis, reinterpret_cast<const double2*>(h0),
-                                                     reinterpret_cast<const double2*>(hc),
-                                                     reinterpret_cast<const double2*>(zero_h), dt, terms);
-  LBG_CHECK_LAUNCH("ptm_terms_kernel");
-  const size_t smem = size_t(3) * MAT * 8;
-  ensure_max_dyn_smem((const void*)ptm_expm_kernel, int(smem));
-  ptm_expm_kernel<<<unsigned(segments), THREADS, smem, s>>>(terms, amps, zeros, pr);
-  LBG_CHECK_LAUNCH("ptm_expm_kernel");
+  launch_terms(dis, h0, hc, zero_h, dt, terms, s);
+  launch_expm(terms, amps, zeros, pr, int(segments), s);
   if (ev_build_end) check_cuda(cudaEventRecord(ev_build_end, s), "event");
   ptm_chain_kernel<<<1, CH_THREADS, 0, s>>>(pr, segments, sps, reinterpret_cast<double2*>(rho));
   LBG_CHECK_LAUNCH("ptm_chain_kernel");
