@@ -529,7 +529,8 @@ def extra_configs(torch, lbg, R, peak):
                     "ms": build_ms, "kernels": "ptm_expm_kernel (+ ptm_terms_kernel, once)",
                     "executed_tflops": build_flops / (build_ms * 1e-3) / 1e12,
                     "note": ("per trajectory: A = dt L_R from three precomputed affine terms, Taylor-12 "
-                             "Paterson-Stockmeyer, 5 real 81x81 DMMA matmuls")}
+                             "Paterson-Stockmeyer, 5 real 81x81 matmuls (10x10 DMMA tiles on k < 80 + DFMA "
+                             "fringe for row / column 80, 8 warps in 5x3 / 5x2 blocks)")}
                 entry["stepping"] = {
                     "ms": step_ms, "traj_steps_per_s": step_rate, "kernel": "ptm_step_kernel",
                     "executed_tflops": step_rate * 2 * 81 ** 2 / 1e12,

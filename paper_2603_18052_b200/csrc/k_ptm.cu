@@ -18,12 +18,12 @@
 // K4 (ptm_expm_kernel): one CTA per trajectory; A_R = dt L_R formed in shared
 //   memory from three precomputed affine terms (ptm_terms_kernel); Taylor in
 //   Paterson-Stockmeyer form with s = 3 (A2, A3, then Horner products in A3,
-//   no solve): degree 12 in 5 real DMMA matmuls for ||A||_1 <= 0.36
+//   no solve): degree 12 in 5 real matmuls for ||A||_1 <= 0.36
 //   (truncation <= 2.5e-16; config 4 sits at 0.327-0.342), degree 14 in 6 for
-//   ||A||_1 <= 0.53 (<= 2^-54), scaling and squaring above;
-//   three 88x92 padded matrices in shared memory, A and A^2 also kept at each
-//   thread's own accumulator positions so the Horner epilogues never re-read
-//   them. Writes P_R (n x n) to global memory.
+//   ||A||_1 <= 0.53 (<= 2^-54), scaling and squaring above. Each 81 x 81
+//   product: 10 x 10 DMMA tiles over k < 80 plus a DFMA fringe (k = 80 and
+//   row / column 80), 8 warps in 5x3 / 5x2 tile blocks, A and A^2 kept at the
+//   lanes' own entries. Writes P_R (n x n) to global memory.
 // K3 (ptm_step_kernel): three trajectories per CTA; P_R register resident
 //   (a 4 x 21 block per thread), x in shared memory; per step 84 FMAs in 12
 //   chains, a 4-lane shuffle reduce-scatter, one barrier. The SM register file
@@ -31,7 +31,6 @@
 //   SM. Epilogue: populations + ensemble sum.
 #include <algorithm>
 #include <cmath>
-#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.hpp"
@@ -40,14 +39,9 @@ namespace lbg {
 namespace {
 
 constexpr int D = 9, N = 81;          // config 4 size
-constexpr int MT = 11, KT = 21;       // 8-row m/n tiles (88), 4-wide k steps (84)
-constexpr int RS = 92;                // smem row stride: 92 = 12 (mod 16) -> conflict free
-constexpr int MAT = 88 * RS;          // doubles per padded matrix
-constexpr int WARPS = 11, THREADS = 32 * WARPS;
 constexpr double kTheta14 = 0.53;
 // degree 12 (5 products) below 0.36: truncation <= 0.36^13 / 13! (1 + 0.36/14) = 2.5e-16
 constexpr double kTheta12 = 0.36;
-static_assert(THREADS == 4 * 88, "combine pass: 4 threads per padded column");
 
 // coherent Kronecker entries  C[q][p] = -i (H[i][j] d_kl - d_ij H[l][k]),  q = (i,k), p = (j,l)
 __device__ __forceinline__ double2 kron_c(const double2* __restrict__ h, int q, int p) {
@@ -86,16 +80,40 @@ __device__ __forceinline__ double real_entry(F&& lq, int q, int s) {
 // terms dt C0 = dt (D_R + coherent_R(h0)), dt Cd = dt coherent_R(hd),
 // dt Cs = dt coherent_R(hs) are built ONCE (D from the complex
 // Kronecker-assembled dissipator, k_model.cu build_lindbladian_kernel with
-// H = 0), in the padded 88 x RS shared-memory layout of the expm kernel (zero
+// H = 0), in the 81 x RS shared-memory layout of the expm kernel (zero
 // padding), so each trajectory stages them with three bulk copies and forms
 // A = dt L_R(b) with two FMAs per entry.
+// K4 product geometry. The DMMA tiles cover rows / columns / k 0..79 only:
+// 10 x 10 output tiles x 20 k-steps = 2,000 DMMAs per product instead of the
+// 11 x 11 x 21 = 2,541 of an 88-padded layout, whose last m-tile, n-tile and
+// k-step each carry a single real row / column / k. The 81st row and column go
+// to DFMA: the k = 80 term is a rank-1 update of each lane's own tile entries,
+// and the 161 fringe entries (column 80 for rows 0..79, and row 80) are dot
+// products split over 2 lanes and shuffle-reduced. Matrices are 81 x 84 in
+// shared memory (three of them: 163 KB).
+constexpr int RS = 84;                      // = 4 (mod 16): conflict-free DMMA fragments
+constexpr int MAT = N * RS;                // doubles per matrix (81 rows)
+constexpr int EMT = 5, EKT = 20;             // m-tiles per warp, DMMA k-steps (k < 80)
+constexpr int FRINGE = 2 * 80 + 1;           // column 80 (rows < 80) + row 80
+
+struct TaylorCoef {
+  double v[15];
+};
+constexpr TaylorCoef make_taylor() {
+  TaylorCoef c{};
+  c.v[0] = 1.0;
+  for (int k = 1; k < 15; ++k) c.v[k] = c.v[k - 1] / k;
+  return c;
+}
+__constant__ TaylorCoef c_taylor = make_taylor();
+
 __global__ void ptm_terms_kernel(const double2* __restrict__ dis, const double2* __restrict__ h0,
-                                 const double2* __restrict__ hd, const double2* __restrict__ hs, double dt,
-                                 double* __restrict__ terms) {
+                                  const double2* __restrict__ hd, const double2* __restrict__ hs, double dt,
+                                  double* __restrict__ terms) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= MAT) return;
   const int q = e / RS, s = e - q * RS;
-  const bool in = q < N && s < N;
+  const bool in = s < N;
   terms[e] = in ? dt * (real_entry([&](int p) { return dis[q * N + p]; }, q, s) +
                         real_entry([&](int p) { return kron_c(h0, q, p); }, q, s))
                 : 0.0;
@@ -103,72 +121,237 @@ __global__ void ptm_terms_kernel(const double2* __restrict__ dis, const double2*
   terms[2 * MAT + e] = in ? dt * real_entry([&](int p) { return kron_c(hs, q, p); }, q, s) : 0.0;
 }
 
-// acc[m][0..1] = (X * Y)[m*8 + g][w*8 + 2t .. +1], X, Y padded 88 x RS
-__device__ __forceinline__ void mm(const double* __restrict__ X, const double* __restrict__ Y,
-                                   double (&acc)[MT][2], int w, int lane) {
-  const int g = lane >> 2, t = lane & 3;
+__device__ __forceinline__ void fringe_rc(int d, int& r, int& c) {
+  if (d < 80) r = d, c = 80;
+  else r = 80, c = d - 80;
+}
+
+// K4 warp layout: 8 warps, blocks of 5 m-tiles x 3 n-tiles (warps 0..3) and
+// 5 x 2 (warps 4..7). Warps w and w + 4 share sub-partition w, so every
+// sub-partition issues exactly 500 DMMAs per product, and a k-step loads 8 (7)
+// fragments for 15 (10) DMMAs. The lighter warps also compute the fringe.
+// With 256 threads the registers hold A and A^2 at each lane's own entries, so
+// the Horner epilogues read no shared memory. Measured (c4 pass, build share):
+// an 11-warp kernel on 88-padded tiles (3 of the 4 sub-partitions issue 693
+// DMMAs per product) 42.16 ms; the same geometry on 20 warps of 5 x 1 blocks
+// 41.57 ms (ncu: shared-memory bound, 9.5k wavefronts per product against 8k
+// DMMA cycles); this layout 40.10 ms.
+// n-tile ranges: warp 0: [0,3) warp 4: [3,5) warp 1: [5,8) warp 5: [8,10),
+// warps 2/6 and 3/7 the same on the lower five m-tiles.
+constexpr int EXPM_WARPS = 8, EXPM_THREADS = 32 * EXPM_WARPS;
+// the fringe goes to the lighter warps 4..7: dots split over 2 lanes (k parity)
+constexpr int FR_DOTS = (2 * FRINGE + 127) / 128;  // fringe dots per lane of warps 4..7 (3)
+__device__ __forceinline__ int blk_n0(int w) { return (w & 1) * 5 + (w >= 4 ? 3 : 0); }
+__device__ __forceinline__ int blk_m0(int w) { return ((w & 3) >> 1) * 5; }
+
+struct Fringe {
+  int r[FR_DOTS], c[FR_DOTS];
+  bool own[FR_DOTS];
+};
+
+template <int NB>
+struct Blk {
+  static constexpr int FR = NB == 2 ? FR_DOTS : 0;  // fringe dots held
+  static constexpr int FRA = FR > 0 ? FR : 1;
+  double acc[EMT][NB][2], a1[EMT][NB][2], a2[EMT][NB][2];
+  double f[FRA], f1[FRA], f2[FRA];
+};
+
+template <int NB>
+__device__ __forceinline__ void mm(const double* __restrict__ X, const double* __restrict__ Y, Blk<NB>& B,
+                                    const Fringe& fr, int w, int lane) {
+  const int g = lane >> 2, t = lane & 3, n0 = blk_n0(w), m0 = blk_m0(w);
 #pragma unroll
-  for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = 0.0;
-  const double* xa = X + g * RS + t;
-  const double* yb = Y + t * RS + w * 8 + g;
-  double a_cur[MT], b_cur = yb[0];
+  for (int m = 0; m < EMT; ++m)
 #pragma unroll
-  for (int m = 0; m < MT; ++m) a_cur[m] = xa[m * 8 * RS];
+    for (int n = 0; n < NB; ++n) B.acc[m][n][0] = B.acc[m][n][1] = 0.0;
+  const double* xa = X + (m0 * 8 + g) * RS + t;
+  const double* yb = Y + t * RS + n0 * 8 + g;
+#pragma unroll 2
+  for (int k = 0; k < EKT; ++k) {
+    double a[EMT], b[NB];
 #pragma unroll
-  for (int k = 0; k < KT; ++k) {
-    double a_nxt[MT], b_nxt = 0.0;
-    if (k + 1 < KT) {
-      b_nxt = yb[(k + 1) * 4 * RS];
+    for (int m = 0; m < EMT; ++m) a[m] = xa[m * 8 * RS + k * 4];
 #pragma unroll
-      for (int m = 0; m < MT; ++m) a_nxt[m] = xa[m * 8 * RS + (k + 1) * 4];
+    for (int n = 0; n < NB; ++n) b[n] = yb[k * 4 * RS + n * 8];
+#pragma unroll
+    for (int m = 0; m < EMT; ++m)
+#pragma unroll
+      for (int n = 0; n < NB; ++n) dmma(B.acc[m][n], a[m], b[n]);
+  }
+  // k = 80: rank-1 update of the own entries
+#pragma unroll
+  for (int n = 0; n < NB; ++n) {
+    const double2 y = *reinterpret_cast<const double2*>(Y + 80 * RS + (n0 + n) * 8 + 2 * t);
+#pragma unroll
+    for (int m = 0; m < EMT; ++m) {
+      const double x = X[((m0 + m) * 8 + g) * RS + 80];
+      B.acc[m][n][0] = fma(x, y.x, B.acc[m][n][0]);
+      B.acc[m][n][1] = fma(x, y.y, B.acc[m][n][1]);
     }
+  }
+  // fringe (warps 4..7): dot (r, c) over k = kh (mod 2), 2-lane shuffle reduce
+  const int kh = lane & 1;
 #pragma unroll
-    for (int m = 0; m < MT; ++m) dmma(acc[m], a_cur[m], b_cur);
-    if (k + 1 < KT) {
-      b_cur = b_nxt;
+  for (int i = 0; i < Blk<NB>::FR; ++i) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    const double* xr = X + fr.r[i] * RS;
+    const double* yc = Y + fr.c[i];
 #pragma unroll
-      for (int m = 0; m < MT; ++m) a_cur[m] = a_nxt[m];
+    for (int j = 0; j < 41; ++j) {  // k = kh + 2 j <= 80: 41 terms for kh = 0, 40 otherwise
+      const int k = kh + 2 * j;
+      if (j == 40 && kh != 0) break;
+      const double v = xr[k], y = yc[k * RS];
+      if (j % 4 == 0)
+        s0 = fma(v, y, s0);
+      else if (j % 4 == 1)
+        s1 = fma(v, y, s1);
+      else if (j % 4 == 2)
+        s2 = fma(v, y, s2);
+      else
+        s3 = fma(v, y, s3);
     }
+    double sum = (s0 + s1) + (s2 + s3);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+    B.f[i] = sum;
   }
 }
 
-__device__ __forceinline__ void store(double* __restrict__ Z, const double (&v)[MT][2], int w, int lane) {
-  const int g = lane >> 2, t = lane & 3;
+// acc = (with_acc ? acc : 0) + c0 I + c1 A + c2 A^2 at the own entries
+template <int NB>
+__device__ __forceinline__ void epi(Blk<NB>& B, const Fringe& fr, double c0, double c1, double c2, bool with_acc,
+                                     int w, int lane) {
+  const int g = lane >> 2, t = lane & 3, n0 = blk_n0(w), m0 = blk_m0(w);
 #pragma unroll
-  for (int m = 0; m < MT; ++m)
-    *reinterpret_cast<double2*>(Z + (m * 8 + g) * RS + w * 8 + 2 * t) = make_double2(v[m][0], v[m][1]);
+  for (int m = 0; m < EMT; ++m)
+#pragma unroll
+    for (int n = 0; n < NB; ++n)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int r = (m0 + m) * 8 + g, col = (n0 + n) * 8 + 2 * t + c;
+        double x = (with_acc ? B.acc[m][n][c] : 0.0) + c1 * B.a1[m][n][c] + c2 * B.a2[m][n][c];
+        if (r == col) x += c0;
+        B.acc[m][n][c] = x;
+      }
+#pragma unroll
+  for (int i = 0; i < Blk<NB>::FR; ++i) {
+    double x = (with_acc ? B.f[i] : 0.0) + c1 * B.f1[i] + c2 * B.f2[i];
+    if (fr.r[i] == fr.c[i]) x += c0;
+    B.f[i] = x;
+  }
 }
 
-// acc = acc + c0 I + c1 a1 + c2 a2 at own positions (in place); zero in the padding
-__device__ __forceinline__ void horner_epilogue(double (&acc)[MT][2],
-                                                const double (&a1)[MT][2], const double (&a2)[MT][2],
-                                                double c0, double c1, double c2, int w, int lane,
-                                                bool with_acc) {
-  const int g = lane >> 2, t = lane & 3;
+template <int NB>
+__device__ __forceinline__ void store(double* __restrict__ Z, const Blk<NB>& B, const Fringe& fr, int w,
+                                       int lane) {
+  const int g = lane >> 2, t = lane & 3, n0 = blk_n0(w), m0 = blk_m0(w);
 #pragma unroll
-  for (int m = 0; m < MT; ++m)
+  for (int m = 0; m < EMT; ++m)
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const int r = m * 8 + g, col = w * 8 + 2 * t + c;
-      double x = (with_acc ? acc[m][c] : 0.0) + c1 * a1[m][c] + c2 * a2[m][c];
-      if (r == col) x += c0;
-      acc[m][c] = (r < N && col < N) ? x : 0.0;
+    for (int n = 0; n < NB; ++n)
+      *reinterpret_cast<double2*>(Z + ((m0 + m) * 8 + g) * RS + (n0 + n) * 8 + 2 * t) =
+          make_double2(B.acc[m][n][0], B.acc[m][n][1]);
+#pragma unroll
+  for (int i = 0; i < Blk<NB>::FR; ++i)
+    if (fr.own[i]) Z[fr.r[i] * RS + fr.c[i]] = B.f[i];
+}
+
+__device__ __forceinline__ void bar_all() { asm volatile("bar.sync 0;\n" ::: "memory"); }
+
+// Taylor / Paterson-Stockmeyer + squarings on the scaled A in SA; P_R -> out
+template <int NB>
+__device__ __forceinline__ void expm_body(double* SA, double* SA2, double* SA3, const Fringe& fr, int sq,
+                                           bool deg12, double* __restrict__ out, int w, int lane) {
+  const double* cf = c_taylor.v;
+  const int g = lane >> 2, t = lane & 3, n0 = blk_n0(w), m0 = blk_m0(w);
+  Blk<NB> B;
+#pragma unroll
+  for (int m = 0; m < EMT; ++m)
+#pragma unroll
+    for (int n = 0; n < NB; ++n) {
+      const double2 v = *reinterpret_cast<const double2*>(SA + ((m0 + m) * 8 + g) * RS + (n0 + n) * 8 + 2 * t);
+      B.a1[m][n][0] = v.x;
+      B.a1[m][n][1] = v.y;
     }
+#pragma unroll
+  for (int i = 0; i < Blk<NB>::FR; ++i) B.f1[i] = SA[fr.r[i] * RS + fr.c[i]];
+  mm<NB>(SA, SA, B, fr, w, lane);  // A^2
+#pragma unroll
+  for (int m = 0; m < EMT; ++m)
+#pragma unroll
+    for (int n = 0; n < NB; ++n) B.a2[m][n][0] = B.acc[m][n][0], B.a2[m][n][1] = B.acc[m][n][1];
+#pragma unroll
+  for (int i = 0; i < Blk<NB>::FR; ++i) B.f2[i] = B.f[i];
+  store<NB>(SA2, B, fr, w, lane);
+  bar_all();
+  mm<NB>(SA2, SA, B, fr, w, lane);  // A^3
+  bar_all();                         // everyone done reading SA / SA2
+  store<NB>(SA3, B, fr, w, lane);
+  int j0;
+  if (deg12) {  // T = B3 + c12 A3 (B4 = c12 I: no product)
+#pragma unroll
+    for (int m = 0; m < EMT; ++m)
+#pragma unroll
+      for (int n = 0; n < NB; ++n) B.acc[m][n][0] *= cf[12], B.acc[m][n][1] *= cf[12];
+#pragma unroll
+    for (int i = 0; i < Blk<NB>::FR; ++i) B.f[i] *= cf[12];
+    epi<NB>(B, fr, cf[9], cf[10], cf[11], true, w, lane);
+    j0 = 2;
+  } else {  // T = B4
+    epi<NB>(B, fr, cf[12], cf[13], cf[14], false, w, lane);
+    j0 = 3;
+  }
+  double* tcur = SA;  // A and A^2 now live in registers: SA / SA2 are free
+  double* tnxt = SA2;
+  store<NB>(tcur, B, fr, w, lane);
+  bar_all();
+#pragma unroll 1
+  for (int j = j0; j >= 0; --j) {  // T = B_j + A3 T
+    mm<NB>(SA3, tcur, B, fr, w, lane);
+    epi<NB>(B, fr, cf[3 * j], cf[3 * j + 1], cf[3 * j + 2], true, w, lane);
+    if (j > 0 || sq > 0) {
+      store<NB>(tnxt, B, fr, w, lane);
+      bar_all();
+      double* tt = tcur;
+      tcur = tnxt;
+      tnxt = tt;
+    }
+  }
+  for (int i = 0; i < sq; ++i) {  // squarings
+    mm<NB>(tcur, tcur, B, fr, w, lane);
+    if (i + 1 < sq) {
+      store<NB>(tnxt, B, fr, w, lane);
+      bar_all();
+      double* tt = tcur;
+      tcur = tnxt;
+      tnxt = tt;
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < EMT; ++m)
+#pragma unroll
+    for (int n = 0; n < NB; ++n) {  // rows of 81 doubles: odd rows are not 16-byte aligned
+      double* o = out + ((m0 + m) * 8 + g) * N + (n0 + n) * 8 + 2 * t;
+      o[0] = B.acc[m][n][0];
+      o[1] = B.acc[m][n][1];
+    }
+#pragma unroll
+  for (int i = 0; i < Blk<NB>::FR; ++i)
+    if (fr.own[i]) out[fr.r[i] * N + fr.c[i]] = B.f[i];
 }
 
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(EXPM_THREADS, 1)
     ptm_expm_kernel(const double* __restrict__ terms, const double* __restrict__ delta,
-                    const double* __restrict__ scale, double* __restrict__ p_out) {
+                     const double* __restrict__ scale, double* __restrict__ p_out) {
   extern __shared__ __align__(16) double sm[];
-  double* S0 = sm;
-  double* S1 = sm + MAT;
-  double* S2 = sm + 2 * MAT;
-  __shared__ double colpart[4][88];
+  double* SA = sm;
+  double* SA2 = sm + MAT;
+  double* SA3 = sm + 2 * MAT;
+  __shared__ double colpart[3][RS];
   __shared__ int s_sq, s_deg12;
   __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int b = blockIdx.x;
-  // dt C0 / dt Cd / dt Cs -> S0 / S1 / S2: three bulk async copies on one mbarrier
   const unsigned sb32 = static_cast<unsigned>(__cvta_generic_to_shared(&bar));
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sb32));
@@ -184,305 +367,13 @@ __global__ void __launch_bounds__(THREADS, 1)
           : "memory");
   }
   const double db = delta[b], sb = scale[b];
-  __syncthreads();  // barrier initialised
-  asm volatile(
-      "{\n.reg .pred p;\nWAIT_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra WAIT_%=;\n}\n" ::"r"(
-          sb32)
-      : "memory");
-  // A = dt C0 + delta dt Cd + s dt Cs in place in S0, fused with the column
-  // sums of ||A||_1: thread = (column c, quarter of the rows); 4 x 88 = THREADS
-  {
-    const int c = tid % 88, q0 = (tid / 88) * 22;
-    double cs = 0.0;
-    if (c < N) {
-#pragma unroll 2
-      for (int r = q0; r < q0 + 22 && r < N; ++r) {
-        const int o = r * RS + c;
-        const double v = fma(sb, S2[o], fma(db, S1[o], S0[o]));
-        S0[o] = v;
-        cs += fabs(v);
-      }
-    }
-    colpart[tid / 88][c] = cs;
-  }
-  __syncthreads();
-  if (w == 0) {  // ||A||_1 -> squarings (per trajectory)
-    double nrm = 0.0;
-    for (int c = lane; c < N; c += 32)
-      nrm = fmax(nrm, (colpart[0][c] + colpart[1][c]) + (colpart[2][c] + colpart[3][c]));
+  Fringe fr;  // meaningful in warps 4..7 only
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) nrm = fmax(nrm, __shfl_xor_sync(0xffffffffu, nrm, o));
-    if (lane == 0) {
-      s_sq = nrm > kTheta14 ? int(ceil(log2(nrm / kTheta14))) : 0;
-      s_deg12 = nrm <= kTheta12;
-    }
-  }
-  __syncthreads();
-  const int sq = s_sq;
-  const bool deg12 = s_deg12;
-  if (sq > 0) {
-    const double sc = ldexp(1.0, -sq);
-    for (int e = tid; e < N * N; e += THREADS) {
-      const int q = e / N, s = e - q * N;
-      S0[q * RS + s] *= sc;
-    }
-    __syncthreads();
-  }
-
-  const int g = lane >> 2, t = lane & 3;
-  double a1[MT][2], a2[MT][2], acc[MT][2];
-#pragma unroll
-  for (int m = 0; m < MT; ++m)
-#pragma unroll
-    for (int c = 0; c < 2; ++c) a1[m][c] = S0[(m * 8 + g) * RS + w * 8 + 2 * t + c];
-  // Taylor coefficients 1/k!, k = 0..14
-  double cf[15];
-  cf[0] = 1.0;
-#pragma unroll
-  for (int k = 1; k < 15; ++k) cf[k] = cf[k - 1] / k;
-
-  mm(S0, S0, acc, w, lane);  // A2
-#pragma unroll
-  for (int m = 0; m < MT; ++m) a2[m][0] = acc[m][0], a2[m][1] = acc[m][1];
-  store(S1, acc, w, lane);
-  __syncthreads();
-  mm(S1, S0, acc, w, lane);  // A3
-  __syncthreads();            // everyone done reading S0/S1
-  store(S2, acc, w, lane);
-  int j0;
-  if (deg12) {  // T = B3 + c12 A3 (B4 = c12 I: no product)
-#pragma unroll
-    for (int m = 0; m < MT; ++m) acc[m][0] *= cf[12], acc[m][1] *= cf[12];
-    horner_epilogue(acc, a1, a2, cf[9], cf[10], cf[11], w, lane, true);
-    j0 = 2;
-  } else {  // T = B4
-    horner_epilogue(acc, a1, a2, cf[12], cf[13], cf[14], w, lane, false);
-    j0 = 3;
-  }
-  store(S0, acc, w, lane);
-  __syncthreads();
-  double* tcur = S0;
-  double* tnxt = S1;
-#pragma unroll 1
-  for (int j = j0; j >= 0; --j) {  // T = B_j + A3 T
-    mm(S2, tcur, acc, w, lane);
-    double c0 = cf[0], c1 = cf[1], c2 = cf[2];  // cf[3j .. 3j+2] without a local-memory index
-#pragma unroll
-    for (int jj = 1; jj < 4; ++jj)
-      if (j == jj) c0 = cf[3 * jj], c1 = cf[3 * jj + 1], c2 = cf[3 * jj + 2];
-    horner_epilogue(acc, a1, a2, c0, c1, c2, w, lane, true);
-    if (j > 0 || sq > 0) {
-      store(tnxt, acc, w, lane);
-      __syncthreads();
-      double* tt = tcur;
-      tcur = tnxt;
-      tnxt = tt;
-    }
-  }
-  for (int i = 0; i < sq; ++i) {  // squarings
-    mm(tcur, tcur, acc, w, lane);
-    if (i + 1 < sq) {
-      store(tnxt, acc, w, lane);
-      __syncthreads();
-      double* tt = tcur;
-      tcur = tnxt;
-      tnxt = tt;
-    }
-  }
-  // ---- P_R -> global (n x n, unpadded) ----
-  double* out = p_out + size_t(b) * N * N;
-#pragma unroll
-  for (int m = 0; m < MT; ++m) {
-    const int r = m * 8 + g, c0 = w * 8 + 2 * t;
-    if (r < N) {
-      if (c0 < N) out[r * N + c0] = acc[m][0];
-      if (c0 + 1 < N) out[r * N + c0 + 1] = acc[m][1];
-    }
-  }
-}
-
-// K4, balanced: the DMMA tiles cover rows / columns / k 0..79 only (10 x 10
-// output tiles, 20 k-steps: 2,000 DMMAs per product instead of 11 x 11 x 21 =
-// 2,541, whose last m-tile, n-tile and k-step carry one real row / column / k
-// each), 20 warps = five per sub-partition own 5 tiles each (half an n-tile
-// column), so every sub-partition issues exactly 500 DMMAs per product (the
-// 11-warp kernel: 693 on three of them). The 81st row / column go to DFMA:
-// the k = 80 term is a rank-1 update on each lane's own tile entries, and the
-// 161 fringe entries (column 80, rows 0..79, and row 80) are dot products
-// split over 4 lanes (k = kq mod 4) and shuffle-reduced. Four 81 x 84
-// matrices (A, A^2, A^3, T: 213 KB) in shared memory; the Horner epilogues
-// read A and A^2 there, T is updated in place between two barriers.
-constexpr int RS2 = 84;                      // = 4 (mod 16): conflict-free DMMA fragments
-constexpr int MAT2 = N * RS2;                // doubles per matrix (81 rows)
-constexpr int E_WARPS = 20, E_THREADS = 32 * E_WARPS;
-constexpr int EMT = 5, EKT = 20;             // m-tiles per warp, DMMA k-steps (k < 80)
-constexpr int E_PARTS = 7, E_PROWS = 12;     // combine pass: 7 row parts x 81 columns
-constexpr int FRINGE = 2 * 80 + 1;           // column 80 (rows < 80) + row 80
-static_assert(E_PARTS * 81 <= E_THREADS && E_PARTS * E_PROWS >= N, "combine pass");
-static_assert(4 * MAT2 * 8 + E_PARTS * RS2 * 8 + 64 <= 232448, "shared memory");
-
-struct TaylorCoef {
-  double v[15];
-};
-constexpr TaylorCoef make_taylor() {
-  TaylorCoef c{};
-  c.v[0] = 1.0;
-  for (int k = 1; k < 15; ++k) c.v[k] = c.v[k - 1] / k;
-  return c;
-}
-__constant__ TaylorCoef c_taylor = make_taylor();
-
-__global__ void ptm_terms2_kernel(const double2* __restrict__ dis, const double2* __restrict__ h0,
-                                  const double2* __restrict__ hd, const double2* __restrict__ hs, double dt,
-                                  double* __restrict__ terms) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= MAT2) return;
-  const int q = e / RS2, s = e - q * RS2;
-  const bool in = s < N;
-  terms[e] = in ? dt * (real_entry([&](int p) { return dis[q * N + p]; }, q, s) +
-                        real_entry([&](int p) { return kron_c(h0, q, p); }, q, s))
-                : 0.0;
-  terms[MAT2 + e] = in ? dt * real_entry([&](int p) { return kron_c(hd, q, p); }, q, s) : 0.0;
-  terms[2 * MAT2 + e] = in ? dt * real_entry([&](int p) { return kron_c(hs, q, p); }, q, s) : 0.0;
-}
-
-struct Fringe {  // this lane's fringe dot products (the second only in warp 0)
-  int r[2], c[2];
-  bool own[2];   // lane kq == 0 of a valid dot: holds and stores the entry
-};
-__device__ __forceinline__ void fringe_rc(int d, int& r, int& c) {
-  if (d < 80) r = d, c = 80;
-  else r = 80, c = d - 80;
-}
-
-// (X Y) at this lane's tile entries (acc) and fringe entries (f)
-__device__ __forceinline__ void mm2(const double* __restrict__ X, const double* __restrict__ Y,
-                                    double (&acc)[EMT][2], double (&f)[2], const Fringe& fr, int w, int lane) {
-  const int g = lane >> 2, t = lane & 3, nt = w >> 1, mh = w & 1;
-#pragma unroll
-  for (int m = 0; m < EMT; ++m) acc[m][0] = acc[m][1] = 0.0;
-  const double* xa = X + (mh * EMT * 8 + g) * RS2 + t;
-  const double* yb = Y + t * RS2 + nt * 8 + g;
-#pragma unroll 4
-  for (int k = 0; k < EKT; ++k) {
-    const double b = yb[k * 4 * RS2];
-    double a[EMT];
-#pragma unroll
-    for (int m = 0; m < EMT; ++m) a[m] = xa[m * 8 * RS2 + k * 4];
-#pragma unroll
-    for (int m = 0; m < EMT; ++m) dmma(acc[m], a[m], b);
-  }
-  {  // k = 80: rank-1 update of the own entries
-    const double2 y = *reinterpret_cast<const double2*>(Y + 80 * RS2 + nt * 8 + 2 * t);
-#pragma unroll
-    for (int m = 0; m < EMT; ++m) {
-      const double x = X[((mh * EMT + m) * 8 + g) * RS2 + 80];
-      acc[m][0] = fma(x, y.x, acc[m][0]);
-      acc[m][1] = fma(x, y.y, acc[m][1]);
-    }
-  }
-  const int kq = lane & 3;
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    if (i == 1 && w != 0) break;  // warp-uniform: only warp 0 has a second fringe dot
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-    const double* xr = X + fr.r[i] * RS2;
-    const double* yc = Y + fr.c[i];
-#pragma unroll
-    for (int j = 0; j < 21; ++j) {  // k = kq + 4 j <= 80: 21 terms for kq = 0, 20 otherwise
-      const int k = kq + 4 * j;
-      if (j == 20 && kq != 0) break;
-      const double v = xr[k], y = yc[k * RS2];
-      if (j % 3 == 0)
-        s0 = fma(v, y, s0);
-      else if (j % 3 == 1)
-        s1 = fma(v, y, s1);
-      else
-        s2 = fma(v, y, s2);
-    }
-    double sum = (s0 + s1) + s2;
-    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-    sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-    f[i] = sum;
-  }
-}
-
-// acc = (with_acc ? acc : 0) + c0 I + c1 A + c2 A^2 at the own entries (A, A^2 from shared memory)
-__device__ __forceinline__ void epi2(double (&acc)[EMT][2], double (&f)[2], const Fringe& fr,
-                                     const double* __restrict__ SA, const double* __restrict__ SA2, double c0,
-                                     double c1, double c2, bool with_acc, int w, int lane) {
-  const int g = lane >> 2, t = lane & 3, nt = w >> 1, mh = w & 1;
-#pragma unroll
-  for (int m = 0; m < EMT; ++m) {
-    const int r = (mh * EMT + m) * 8 + g, col = nt * 8 + 2 * t;
-    const double2 a1 = *reinterpret_cast<const double2*>(SA + r * RS2 + col);
-    const double2 a2 = *reinterpret_cast<const double2*>(SA2 + r * RS2 + col);
-    double x0 = (with_acc ? acc[m][0] : 0.0) + c1 * a1.x + c2 * a2.x;
-    double x1 = (with_acc ? acc[m][1] : 0.0) + c1 * a1.y + c2 * a2.y;
-    if (r == col) x0 += c0;
-    if (r == col + 1) x1 += c0;
-    acc[m][0] = x0;
-    acc[m][1] = x1;
-  }
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    if (i == 1 && w != 0) break;
-    const int o = fr.r[i] * RS2 + fr.c[i];
-    double x = (with_acc ? f[i] : 0.0) + c1 * SA[o] + c2 * SA2[o];
-    if (fr.r[i] == fr.c[i]) x += c0;
-    f[i] = x;
-  }
-}
-
-__device__ __forceinline__ void store2(double* __restrict__ Z, const double (&acc)[EMT][2], const double (&f)[2],
-                                       const Fringe& fr, int w, int lane) {
-  const int g = lane >> 2, t = lane & 3, nt = w >> 1, mh = w & 1;
-#pragma unroll
-  for (int m = 0; m < EMT; ++m)
-    *reinterpret_cast<double2*>(Z + ((mh * EMT + m) * 8 + g) * RS2 + nt * 8 + 2 * t) =
-        make_double2(acc[m][0], acc[m][1]);
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-    if (fr.own[i]) Z[fr.r[i] * RS2 + fr.c[i]] = f[i];
-}
-
-__global__ void __launch_bounds__(E_THREADS, 1)
-    ptm_expm2_kernel(const double* __restrict__ terms, const double* __restrict__ delta,
-                     const double* __restrict__ scale, double* __restrict__ p_out) {
-  extern __shared__ __align__(16) double sm[];
-  double* SA = sm;
-  double* SA2 = sm + MAT2;
-  double* SA3 = sm + 2 * MAT2;
-  double* ST = sm + 3 * MAT2;
-  __shared__ double colpart[E_PARTS][RS2];
-  __shared__ int s_sq, s_deg12;
-  __shared__ __align__(8) uint64_t bar;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int b = blockIdx.x;
-  // dt C0 / dt Cd / dt Cs -> SA / SA2 / SA3: three bulk async copies on one mbarrier
-  const unsigned sb32 = static_cast<unsigned>(__cvta_generic_to_shared(&bar));
-  if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sb32));
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sb32), "r"(unsigned(3 * MAT2 * 8))
-                 : "memory");
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-              static_cast<unsigned>(__cvta_generic_to_shared(sm + i * MAT2))),
-          "l"(terms + i * MAT2), "r"(unsigned(MAT2 * 8)), "r"(sb32)
-          : "memory");
-  }
-  const double db = delta[b], sb = scale[b];
-  // this lane's fringe dots: virtual lane v = tid (+ E_THREADS in warp 0), dot v / 4, k phase v % 4
-  Fringe fr;
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int v = tid + i * E_THREADS, d = v >> 2;
-    const bool valid = d < FRINGE;
+  for (int i = 0; i < FR_DOTS; ++i) {
+    const int v = (tid & 127) + i * 128, d = v >> 1;
+    const bool valid = w >= 4 && d < FRINGE;
     fringe_rc(valid ? d : 0, fr.r[i], fr.c[i]);
-    fr.own[i] = valid && (v & 3) == 0 && (i == 0 || w == 0);
+    fr.own[i] = valid && (v & 1) == 0;
   }
   __syncthreads();  // barrier initialised
   asm volatile(
@@ -490,12 +381,12 @@ __global__ void __launch_bounds__(E_THREADS, 1)
           sb32)
       : "memory");
   // A = dt C0 + delta dt Cd + s dt Cs in place in SA, fused with the column sums of ||A||_1
-  if (tid < E_PARTS * 81) {
-    const int c = tid % 81, q0 = (tid / 81) * E_PROWS;
+  if (tid < 3 * 81) {
+    const int c = tid % 81, q0 = (tid / 81) * 27;
     double cs = 0.0;
-#pragma unroll 2
-    for (int r = q0; r < q0 + E_PROWS && r < N; ++r) {
-      const int o = r * RS2 + c;
+#pragma unroll 3
+    for (int r = q0; r < q0 + 27; ++r) {
+      const int o = r * RS + c;
       const double v = fma(sb, SA3[o], fma(db, SA2[o], SA[o]));
       SA[o] = v;
       cs += fabs(v);
@@ -505,12 +396,7 @@ __global__ void __launch_bounds__(E_THREADS, 1)
   __syncthreads();
   if (w == 0) {  // ||A||_1 -> squarings (per trajectory)
     double nrm = 0.0;
-    for (int c = lane; c < N; c += 32) {
-      double cs = 0.0;
-#pragma unroll
-      for (int p = 0; p < E_PARTS; ++p) cs += colpart[p][c];
-      nrm = fmax(nrm, cs);
-    }
+    for (int c = lane; c < N; c += 32) nrm = fmax(nrm, (colpart[0][c] + colpart[1][c]) + colpart[2][c]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) nrm = fmax(nrm, __shfl_xor_sync(0xffffffffu, nrm, o));
     if (lane == 0) {
@@ -523,63 +409,17 @@ __global__ void __launch_bounds__(E_THREADS, 1)
   const bool deg12 = s_deg12;
   if (sq > 0) {
     const double sc = ldexp(1.0, -sq);
-    for (int e = tid; e < N * N; e += E_THREADS) {
+    for (int e = tid; e < N * N; e += EXPM_THREADS) {
       const int q = e / N, s = e - q * N;
-      SA[q * RS2 + s] *= sc;
+      SA[q * RS + s] *= sc;
     }
     __syncthreads();
   }
-  const double* cf = c_taylor.v;
-  double acc[EMT][2], f[2] = {0.0, 0.0};
-  mm2(SA, SA, acc, f, fr, w, lane);  // A^2
-  store2(SA2, acc, f, fr, w, lane);
-  __syncthreads();
-  mm2(SA2, SA, acc, f, fr, w, lane);  // A^3
-  store2(SA3, acc, f, fr, w, lane);
-  int j0;
-  if (deg12) {  // T = B3 + c12 A3 (B4 = c12 I: no product)
-#pragma unroll
-    for (int m = 0; m < EMT; ++m) acc[m][0] *= cf[12], acc[m][1] *= cf[12];
-    f[0] *= cf[12];
-    f[1] *= cf[12];
-    epi2(acc, f, fr, SA, SA2, cf[9], cf[10], cf[11], true, w, lane);
-    j0 = 2;
-  } else {  // T = B4
-    epi2(acc, f, fr, SA, SA2, cf[12], cf[13], cf[14], false, w, lane);
-    j0 = 3;
-  }
-  store2(ST, acc, f, fr, w, lane);
-  __syncthreads();
-#pragma unroll 1
-  for (int j = j0; j >= 0; --j) {  // T = B_j + A3 T
-    mm2(SA3, ST, acc, f, fr, w, lane);
-    epi2(acc, f, fr, SA, SA2, cf[3 * j], cf[3 * j + 1], cf[3 * j + 2], true, w, lane);
-    if (j > 0 || sq > 0) {
-      __syncthreads();  // every warp is done reading T
-      store2(ST, acc, f, fr, w, lane);
-      __syncthreads();
-    }
-  }
-  for (int i = 0; i < sq; ++i) {  // squarings
-    mm2(ST, ST, acc, f, fr, w, lane);
-    if (i + 1 < sq) {
-      __syncthreads();
-      store2(ST, acc, f, fr, w, lane);
-      __syncthreads();
-    }
-  }
-  // ---- P_R -> global (n x n, unpadded) ----
   double* out = p_out + size_t(b) * N * N;
-  const int g = lane >> 2, t = lane & 3, nt = w >> 1, mh = w & 1;
-#pragma unroll
-  for (int m = 0; m < EMT; ++m) {  // rows of 81 doubles: odd rows are not 16-byte aligned
-    double* o = out + ((mh * EMT + m) * 8 + g) * N + nt * 8 + 2 * t;
-    o[0] = acc[m][0];
-    o[1] = acc[m][1];
-  }
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-    if (fr.own[i]) out[fr.r[i] * N + fr.c[i]] = f[i];
+  if (w < 4)
+    expm_body<3>(SA, SA2, SA3, fr, sq, deg12, out, w, lane);
+  else
+    expm_body<2>(SA, SA2, SA3, fr, sq, deg12, out, w, lane);
 }
 
 // K3: x <- P_R x for `steps` steps, P_R register resident.
@@ -767,39 +607,19 @@ __global__ void x_to_rho_kernel(const double* __restrict__ x, double2* __restric
     rho[p] = make_double2(x[j * D + i], -x[p]);
 }
 
-bool expm_v2() {  // A/B switch: LBG_PTM_EXPM=1 selects the 11-warp kernel
-  static const bool v2 = [] {
-    const char* e = std::getenv("LBG_PTM_EXPM");
-    return !(e && std::atoi(e) == 1);
-  }();
-  return v2;
-}
 void launch_terms(const double2* dis, const double* h0, const double* hd, const double* hs, double dt,
                   double* terms, cudaStream_t s) {
-  const auto* H0 = reinterpret_cast<const double2*>(h0);
-  const auto* HD = reinterpret_cast<const double2*>(hd);
-  const auto* HS = reinterpret_cast<const double2*>(hs);
-  if (expm_v2()) {
-    ptm_terms2_kernel<<<(MAT2 + 255) / 256, 256, 0, s>>>(dis, H0, HD, HS, dt, terms);
-    LBG_CHECK_LAUNCH("ptm_terms2_kernel");
-  } else {
-    ptm_terms_kernel<<<(MAT + 255) / 256, 256, 0, s>>>(dis, H0, HD, HS, dt, terms);
-    LBG_CHECK_LAUNCH("ptm_terms_kernel");
-  }
+  ptm_terms_kernel<<<(MAT + 255) / 256, 256, 0, s>>>(dis, reinterpret_cast<const double2*>(h0),
+                                                     reinterpret_cast<const double2*>(hd),
+                                                     reinterpret_cast<const double2*>(hs), dt, terms);
+  LBG_CHECK_LAUNCH("ptm_terms_kernel");
 }
 void launch_expm(const double* terms, const double* delta, const double* scale, double* pr, int count,
                  cudaStream_t s) {
-  if (expm_v2()) {
-    const size_t smem = size_t(4) * MAT2 * 8;
-    ensure_max_dyn_smem((const void*)ptm_expm2_kernel, int(smem));
-    ptm_expm2_kernel<<<count, E_THREADS, smem, s>>>(terms, delta, scale, pr);
-    LBG_CHECK_LAUNCH("ptm_expm2_kernel");
-  } else {
-    const size_t smem = size_t(3) * MAT * 8;
-    ensure_max_dyn_smem((const void*)ptm_expm_kernel, int(smem));
-    ptm_expm_kernel<<<count, THREADS, smem, s>>>(terms, delta, scale, pr);
-    LBG_CHECK_LAUNCH("ptm_expm_kernel");
-  }
+  const size_t smem = size_t(3) * MAT * 8;
+  ensure_max_dyn_smem((const void*)ptm_expm_kernel, int(smem));
+  ptm_expm_kernel<<<count, EXPM_THREADS, smem, s>>>(terms, delta, scale, pr);
+  LBG_CHECK_LAUNCH("ptm_expm_kernel");
 }
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }

@@ -27,4 +27,4 @@ for _ in range(passes):
     torch.cuda.synchronize()
     ms.append(e0.elapsed_time(e1))
 np.savez(out, pops=case.pops.cpu().numpy(), ens=case.ens.cpu().numpy())
-print(f"variant={os.environ.get('LBG_PTM_STEP', 'default')} c4 ms/pass median {sorted(ms)[len(ms) // 2]:.3f} all {['%.2f' % m for m in ms]}")
+print(f"variant={os.environ.get('LBG_PTM_EXPM', 'default')} c4 ms/pass median {sorted(ms)[len(ms) // 2]:.3f} all {['%.2f' % m for m in ms]}")
