@@ -135,7 +135,8 @@ __device__ __forceinline__ void fringe_rc(int d, int& r, int& c) {
 // an 11-warp kernel on 88-padded tiles (3 of the 4 sub-partitions issue 693
 // DMMAs per product) 42.16 ms; the same geometry on 20 warps of 5 x 1 blocks
 // 41.57 ms (ncu: shared-memory bound, 9.5k wavefronts per product against 8k
-// DMMA cycles); this layout 40.10 ms.
+// DMMA cycles); this layout 40.10 ms; 12 warps in 5x2 / 5x2 / 5x1 blocks (three
+// per sub-partition, 168 registers) 40.45 ms.
 // n-tile ranges: warp 0: [0,3) warp 4: [3,5) warp 1: [5,8) warp 5: [8,10),
 // warps 2/6 and 3/7 the same on the lower five m-tiles.
 constexpr int EXPM_WARPS = 8, EXPM_THREADS = 32 * EXPM_WARPS;
