@@ -81,7 +81,8 @@ __device__ __forceinline__ double real_entry(F&& lq, int q, int s) {
 // dt Cs = dt coherent_R(hs) are built ONCE (D from the complex
 // Kronecker-assembled dissipator, k_model.cu build_lindbladian_kernel with
 // H = 0), in the 81 x RS shared-memory layout of the expm kernel (zero
-// padding), so each trajectory stages them with three bulk copies and forms
+// padding); dt Cd and dt Cs are then compacted to their non-zero entries
+// (ptm_sparse_kernel), so each trajectory stages dt C0 with one bulk copy and forms
 // A = dt L_R(b) with two FMAs per entry.
 // K4 product geometry. The DMMA tiles cover rows / columns / k 0..79 only:
 // 10 x 10 output tiles x 20 k-steps = 2,000 DMMAs per product instead of the
@@ -119,6 +120,35 @@ __global__ void ptm_terms_kernel(const double2* __restrict__ dis, const double2*
                 : 0.0;
   terms[MAT + e] = in ? dt * real_entry([&](int p) { return kron_c(hd, q, p); }, q, s) : 0.0;
   terms[2 * MAT + e] = in ? dt * real_entry([&](int p) { return kron_c(hs, q, p); }, q, s) : 0.0;
+}
+
+// dt Cd and dt Cs are sparse (config 4: ~130 and ~430 of the 6,561 entries):
+// compact the entries where either is non-zero into (offset, (cd, cs)) so the
+// expm kernel stages only dt C0 by bulk copy and applies the rest from L2.
+// Slot order is the atomics' (arbitrary); each entry's update is independent,
+// so the result does not depend on it.
+struct SparseTerms {
+  double2* val;
+  int* idx;
+  int* count;
+};
+__host__ __device__ inline SparseTerms sparse_terms(double* terms) {
+  char* base = reinterpret_cast<char*>(terms + 3 * MAT);
+  return {reinterpret_cast<double2*>(base), reinterpret_cast<int*>(base + size_t(MAT) * 16),
+          reinterpret_cast<int*>(base + size_t(MAT) * 20)};
+}
+constexpr size_t kTermsBytes = size_t(3) * MAT * 8 + size_t(MAT) * 20 + 16;
+
+__global__ void ptm_sparse_kernel(double* __restrict__ terms) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= MAT) return;
+  const double cd = terms[MAT + e], cs = terms[2 * MAT + e];
+  if (cd != 0.0 || cs != 0.0) {
+    const SparseTerms sp = sparse_terms(terms);
+    const int slot = atomicAdd(sp.count, 1);
+    sp.idx[slot] = e;
+    sp.val[slot] = make_double2(cd, cs);
+  }
 }
 
 __device__ __forceinline__ void fringe_rc(int d, int& r, int& c) {
@@ -342,8 +372,10 @@ __device__ __forceinline__ void expm_body(double* SA, double* SA2, double* SA3, 
 }
 
 __global__ void __launch_bounds__(EXPM_THREADS, 1)
-    ptm_expm_kernel(const double* __restrict__ terms, const double* __restrict__ delta,
-                     const double* __restrict__ scale, double* __restrict__ p_out) {
+    ptm_expm_kernel(const double* __restrict__ terms, const double2* __restrict__ sp_val,
+                    const int* __restrict__ sp_idx, const int* __restrict__ sp_count,
+                    const double* __restrict__ delta, const double* __restrict__ scale,
+                    double* __restrict__ p_out) {
   extern __shared__ __align__(16) double sm[];
   double* SA = sm;
   double* SA2 = sm + MAT;
@@ -357,16 +389,15 @@ __global__ void __launch_bounds__(EXPM_THREADS, 1)
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sb32));
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sb32), "r"(unsigned(3 * MAT * 8))
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sb32), "r"(unsigned(MAT * 8))
                  : "memory");
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-              static_cast<unsigned>(__cvta_generic_to_shared(sm + i * MAT))),
-          "l"(terms + i * MAT), "r"(unsigned(MAT * 8)), "r"(sb32)
-          : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            static_cast<unsigned>(__cvta_generic_to_shared(sm))),
+        "l"(terms), "r"(unsigned(MAT * 8)), "r"(sb32)
+        : "memory");
   }
+  const int nsp = *sp_count;
   const double db = delta[b], sb = scale[b];
   Fringe fr;  // meaningful in warps 4..7 only
 #pragma unroll
@@ -381,17 +412,18 @@ __global__ void __launch_bounds__(EXPM_THREADS, 1)
       "{\n.reg .pred p;\nWAIT_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra WAIT_%=;\n}\n" ::"r"(
           sb32)
       : "memory");
-  // A = dt C0 + delta dt Cd + s dt Cs in place in SA, fused with the column sums of ||A||_1
+  // A = dt C0 + delta dt Cd + s dt Cs in place in SA (sparse terms), then the column sums of ||A||_1
+  for (int i = tid; i < nsp; i += EXPM_THREADS) {
+    const int o = sp_idx[i];
+    const double2 v = sp_val[i];
+    SA[o] = fma(sb, v.y, fma(db, v.x, SA[o]));
+  }
+  __syncthreads();
   if (tid < 3 * 81) {
     const int c = tid % 81, q0 = (tid / 81) * 27;
     double cs = 0.0;
 #pragma unroll 3
-    for (int r = q0; r < q0 + 27; ++r) {
-      const int o = r * RS + c;
-      const double v = fma(sb, SA3[o], fma(db, SA2[o], SA[o]));
-      SA[o] = v;
-      cs += fabs(v);
-    }
+    for (int r = q0; r < q0 + 27; ++r) cs += fabs(SA[r * RS + c]);
     colpart[tid / 81][c] = cs;
   }
   __syncthreads();
@@ -614,12 +646,16 @@ void launch_terms(const double2* dis, const double* h0, const double* hd, const 
                                                      reinterpret_cast<const double2*>(hd),
                                                      reinterpret_cast<const double2*>(hs), dt, terms);
   LBG_CHECK_LAUNCH("ptm_terms_kernel");
+  check_cuda(cudaMemsetAsync(sparse_terms(terms).count, 0, sizeof(int), s), "memset");
+  ptm_sparse_kernel<<<(MAT + 255) / 256, 256, 0, s>>>(terms);
+  LBG_CHECK_LAUNCH("ptm_sparse_kernel");
 }
 void launch_expm(const double* terms, const double* delta, const double* scale, double* pr, int count,
                  cudaStream_t s) {
   const size_t smem = size_t(3) * MAT * 8;
   ensure_max_dyn_smem((const void*)ptm_expm_kernel, int(smem));
-  ptm_expm_kernel<<<count, EXPM_THREADS, smem, s>>>(terms, delta, scale, pr);
+  const SparseTerms sp = sparse_terms(const_cast<double*>(terms));
+  ptm_expm_kernel<<<count, EXPM_THREADS, smem, s>>>(terms, sp.val, sp.idx, sp.count, delta, scale, pr);
   LBG_CHECK_LAUNCH("ptm_expm_kernel");
 }
 
@@ -631,7 +667,7 @@ constexpr int64_t kChunk = 16384;
 size_t ptm_sweep_workspace(int64_t batch) {
   const size_t chunk = size_t(std::min<int64_t>(std::max<int64_t>(batch, 1), kChunk));
   return align_up(chunk * N * N * 8) + align_up(size_t(N) * N * 16) + align_up(2 * N * 8) +
-         align_up(size_t(3) * MAT * 8) + 256;
+         align_up(kTermsBytes) + 256;
 }
 
 bool ptm_sweep_supported(size_t d) { return d == size_t(D); }
@@ -671,7 +707,7 @@ void launch_ptm_sweep(size_t d, const double* h0, const double* hd, const double
 bool ptm_grape_supported(size_t d) { return d == size_t(D); }
 
 size_t ptm_grape_workspace(int64_t segments) {
-  return align_up(size_t(segments) * N * N * 8) + align_up(size_t(N) * N * 16) + align_up(size_t(3) * MAT * 8) +
+  return align_up(size_t(segments) * N * N * 8) + align_up(size_t(N) * N * 16) + align_up(kTermsBytes) +
          align_up(size_t(segments) * 8) + 256;
 }
 
@@ -687,7 +723,7 @@ void launch_ptm_grape(const double* h0, const double* hc, const double* zero_h, 
   double* pr = reinterpret_cast<double*>(w);
   double2* dis = reinterpret_cast<double2*>(w + align_up(size_t(segments) * N * N * 8));
   double* terms = reinterpret_cast<double*>(reinterpret_cast<char*>(dis) + align_up(size_t(N) * N * 16));
-  double* zeros = reinterpret_cast<double*>(reinterpret_cast<char*>(terms) + align_up(size_t(3) * MAT * 8));
+  double* zeros = reinterpret_cast<double*>(reinterpret_cast<char*>(terms) + align_up(kTermsBytes));
   check_cuda(cudaMemsetAsync(zeros, 0, size_t(segments) * 8, s), "memset");
   launch_build_lindbladian(size_t(D), zero_h, n_ops, ops, reinterpret_cast<double*>(dis), s);
   launch_terms(dis, h0, hc, zero_h, dt, terms, s);
