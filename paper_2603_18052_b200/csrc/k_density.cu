@@ -201,7 +201,12 @@ struct RGeom {  // P_R: mt*8 rows x sp cols; V: kVec x sv
 
 // N > 0: n known at compile time (n = 81 for config 2: no predicates, k loop
 // fully unrolled); N == 0: runtime n. MG = m-tiles of the larger half.
-template <int N, int MG>
+// FRINGE (n = 81 only): the DMMA tiles cover rows and k 0..79 (10 m-tiles x 20
+// k-steps, 5 + 5 per row half, instead of 11 x 21 over the 88 x 84 padding);
+// the k = 80 term is a rank-1 DFMA update of each lane's own entries, and row 80
+// is 32 dot products (8 lanes each, k = kq mod 8) split between the two warps
+// of an n-tile -- the scheme of the c4 expm kernel (k_ptm.cu).
+template <int N, int MG, bool FRINGE = false>
 __global__ void __launch_bounds__(32 * kWarpsR, 1) smem_real_kernel(const double* __restrict__ pr, int n_rt,
                                                                     double* __restrict__ x, int64_t count,
                                                                     int64_t half, const int* __restrict__ flag,
@@ -227,10 +232,12 @@ __global__ void __launch_bounds__(32 * kWarpsR, 1) smem_real_kernel(const double
     vb[e] = 0.0;
   }
   __syncthreads();
+  static_assert(!FRINGE || (N == 81 && MG == 5), "fringe layout: n = 81, 5 + 5 m-tiles");
   const int nt = warp & 3, rhalf = warp >> 2;
-  const int m_split = (g.mt + 1) / 2;
+  const int mt_d = FRINGE ? 10 : g.mt, kt_d = FRINGE ? 20 : g.kt;
+  const int m_split = (mt_d + 1) / 2;
   const int m_begin = rhalf ? m_split : 0;
-  const int mcount = rhalf ? g.mt - m_split : m_split;
+  const int mcount = rhalf ? mt_d - m_split : m_split;
   const int gq = lane >> 2, tq = lane & 3;
   const double* pa = ps + size_t(m_begin * 8 + gq) * g.sp + tq;  // A frag: P_R[m*8+g][k*4+t]
   const int mstride = 8 * g.sp;
@@ -245,9 +252,9 @@ __global__ void __launch_bounds__(32 * kWarpsR, 1) smem_real_kernel(const double
 #pragma unroll
     for (int mi = 0; mi < MG; ++mi) a_cur[mi] = mi < mcount ? pa[mi * mstride] : 0.0;
 #pragma unroll(N > 0 ? 21 : 1)
-    for (int ks = 0; ks < g.kt; ++ks) {
+    for (int ks = 0; ks < kt_d; ++ks) {
       double a_nxt[MG], b_nxt = 0.0;
-      const bool more = ks + 1 < g.kt;
+      const bool more = ks + 1 < kt_d;
       if (more) {
         b_nxt = vrow[(ks + 1) * 4];
 #pragma unroll
@@ -261,6 +268,36 @@ __global__ void __launch_bounds__(32 * kWarpsR, 1) smem_real_kernel(const double
 #pragma unroll
         for (int mi = 0; mi < MG; ++mi) a_cur[mi] = a_nxt[mi];
       }
+    }
+    if (FRINGE) {
+      // k = 80: rank-1 update of the own entries
+      const int t0 = nt * 8 + 2 * tq;
+      const double v0 = va[t0 * g.sv + 80], v1 = va[(t0 + 1) * g.sv + 80];
+#pragma unroll
+      for (int mi = 0; mi < MG; ++mi) {
+        const double pk = ps[size_t((m_begin + mi) * 8 + gq) * g.sp + 80];
+        acc[mi][0] = fma(pk, v0, acc[mi][0]);
+        acc[mi][1] = fma(pk, v1, acc[mi][1]);
+      }
+      // row 80 for vectors nt*8 + 4*rhalf + (lane >> 3): k = kq (mod 8)
+      const int vec = nt * 8 + 4 * rhalf + (lane >> 3), kq = lane & 7;
+      const double* p80 = ps + size_t(80) * g.sp;
+      const double* vv = va + vec * g.sv;
+      double f0 = 0.0, f1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < 11; ++j) {
+        const int k = kq + 8 * j;
+        if (j == 10 && kq != 0) break;
+        if (j & 1)
+          f1 = fma(p80[k], vv[k], f1);
+        else
+          f0 = fma(p80[k], vv[k], f0);
+      }
+      double f = f0 + f1;
+      f += __shfl_xor_sync(0xffffffffu, f, 1);
+      f += __shfl_xor_sync(0xffffffffu, f, 2);
+      f += __shfl_xor_sync(0xffffffffu, f, 4);
+      if (kq == 0) vb[vec * g.sv + 80] = f;
     }
 #pragma unroll
     for (int mi = 0; mi < MG; ++mi) {
@@ -285,7 +322,7 @@ __global__ void __launch_bounds__(32 * kWarpsR, 1) smem_real_kernel(const double
   }
 }
 
-template <int N, int MG>
+template <int N, int MG, bool FRINGE = false>
 void launch_smem_real(const double* pr, int n, double* x, int64_t count, int64_t half, const int* flag,
                       int64_t steps, cudaStream_t s) {
   const RGeom g(n);
@@ -299,9 +336,9 @@ void launch_smem_real(const double* pr, int n, double* x, int64_t count, int64_t
   int smem_sm = 0;
   check_cuda(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev), "attr");
   const size_t bytes = std::max(g.total, size_t(smem_sm / 2 + 1024));
-  ensure_max_dyn_smem((const void*)smem_real_kernel<N, MG>, int(bytes));
-  smem_real_kernel<N, MG><<<unsigned((count + kVec - 1) / kVec), 32 * kWarpsR, bytes, s>>>(pr, n, x, count, half,
-                                                                                          flag, steps);
+  ensure_max_dyn_smem((const void*)smem_real_kernel<N, MG, FRINGE>, int(bytes));
+  smem_real_kernel<N, MG, FRINGE><<<unsigned((count + kVec - 1) / kVec), 32 * kWarpsR, bytes, s>>>(
+      pr, n, x, count, half, flag, steps);
   LBG_CHECK_LAUNCH("smem_real_kernel");
 }
 
@@ -349,7 +386,8 @@ static void step_real(const double* pr, size_t n, double* x, int64_t count, int6
     return;
   }
   const int ni = int(n);
-  if (ni == 81) return launch_smem_real<81, 6>(pr, ni, x, count, half, flag, steps, s);
+  // n = 81 (config 2): the fringe layout, 2.10 vs 2.24 ms per c2 pass over the 88 x 84 padded tiles
+  if (ni == 81) return launch_smem_real<81, 5, true>(pr, ni, x, count, half, flag, steps, s);
   switch (((ni + 7) / 8 + 1) / 2) {
 #define LBG_MG(M) \
   case M: return launch_smem_real<0, M>(pr, ni, x, count, half, flag, steps, s);
