@@ -68,4 +68,25 @@ __device__ __forceinline__ double2 pair_complex(const double (&c)[2], int lane, 
   return a ? make_double2(recv, c[1]) : make_double2(c[0], recv);
 }
 
+
+// Software grid barrier for cooperative (all-resident) launches: the arrival
+// counter only grows (gridDim.x per barrier), so the target is compared
+// wrap-safely — (int)(v - target) >= 0 stays correct after the 32-bit counter
+// wraps (steps * grid >= 2^32), as long as fewer than 2^31 arrivals separate
+// the fastest CTA from the target (one barrier's worth here).
+__device__ __forceinline__ void grid_barrier_sync(unsigned int* bar, unsigned int target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // release-add after the CTA barrier (cumulativity carries the other warps'
+    // stores; no full membar), acquire poll (no trailing fence needed)
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(bar) : "memory");
+    while (true) {
+      unsigned int v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(bar) : "memory");
+      if (int(v - target) >= 0) break;
+    }
+  }
+  __syncthreads();
+}
+
 }  // namespace lbg

@@ -155,20 +155,6 @@ __global__ void x_to_rho_real_kernel(const double* __restrict__ x, int d, double
 
 // ---- the chain: real rows of P_R,j spread over every SM, one grid barrier per step
 constexpr int RT = 256;
-__device__ __forceinline__ void grid_sync_r(unsigned int* bar, unsigned int target) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    // release-add (no separate membar) after the CTA barrier: cumulativity carries the
-    // other warps' stores; the acquire poll orders the reloads after it
-    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(bar) : "memory");
-    while (true) {
-      unsigned int v;
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(bar) : "memory");
-      if (v >= target) break;
-    }
-  }
-  __syncthreads();
-}
 
 __global__ void __launch_bounds__(RT) rowsplit_real_kernel(const double* __restrict__ props, int n, int ld,
                                                            double* x0, double* x1, int64_t segments, int64_t sps,
@@ -208,7 +194,7 @@ __global__ void __launch_bounds__(RT) rowsplit_real_kernel(const double* __restr
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if (lane == 0) nxt[r0 + r] = v;
       }
-      grid_sync_r(bar, ++epoch * gridDim.x);
+      grid_barrier_sync(bar, ++epoch * gridDim.x);
       double* t = cur;
       cur = nxt;
       nxt = t;

@@ -112,20 +112,6 @@ __global__ void __launch_bounds__(4 * kMaxCtaN) cta_chain_kernel(const double2* 
 // ---------------------------------------------------------------- K2c ------
 constexpr int RS_THREADS = 256;
 
-__device__ __forceinline__ void grid_sync(unsigned int* bar, unsigned int target) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    // release-add after the CTA barrier (cumulativity carries the other warps'
-    // stores; no full membar), acquire poll (no trailing fence needed)
-    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(bar) : "memory");
-    while (true) {
-      unsigned int v;
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(bar) : "memory");
-      if (v >= target) break;
-    }
-  }
-  __syncthreads();
-}
 
 // x0/x1: batch x n complex ping-pong state in global memory (L2 resident)
 __global__ void __launch_bounds__(RS_THREADS) rowsplit_kernel(const double2* __restrict__ p, int n,
@@ -177,7 +163,7 @@ __global__ void __launch_bounds__(RS_THREADS) rowsplit_kernel(const double2* __r
       }
       if (lane == 0) nxt[size_t(b) * n + r0 + r] = make_double2(re, im);
     }
-    grid_sync(bar, unsigned(s + 1) * gridDim.x);
+    grid_barrier_sync(bar, unsigned(s + 1) * gridDim.x);
     double2* t = cur;
     cur = nxt;
     nxt = t;

@@ -29,6 +29,9 @@
 #include <cuda.h>  // CUtensorMap (driver types only; the encoder comes via cudaGetDriverEntryPoint)
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 #include <map>
 #include <mutex>
 
@@ -39,8 +42,8 @@ namespace lbg {
 
 namespace {
 
-constexpr int BM = 32, BK = 32, STAGES = 2;
-constexpr int CWARPS = 8, THREADS = 32 * (CWARPS + 1);
+constexpr int BM = 32, BK = 32, STAGES = 2;  // default ring depth
+constexpr int CWARPS = 8, THREADS = 32 * (CWARPS + 1);  // defaults (Geo<..., CW_>)
 constexpr int SA = BK + 2;  // complex stride of A rows: 2 (mod 8), see header
 constexpr int A_ELEMS = BM * SA;
 
@@ -52,20 +55,22 @@ constexpr int A_ELEMS = BM * SA;
 // x BN tiles, K chunk 32, A stride 36 = 4 (mod 16) and B stride BN + 8 =
 // 8 (mod 16) doubles (conflict-free m8n8k4 fragments), the same byte size per
 // stage as the complex geometry.
-template <int BN_, bool REAL_ = false, int BK_ = BK>
+template <int BN_, bool REAL_ = false, int BK_ = BK, int ST_ = STAGES, int CW_ = CWARPS>
 struct Geo {
+  static constexpr int ST = ST_;  // ring stages
+  static constexpr int CW = CW_, NT = 32 * (CW_ + 1);  // consumer warps, threads (+ producer warp)
   static constexpr bool REAL = REAL_;
   static constexpr int CPX = REAL ? 1 : 2;         // doubles per element
   static constexpr int BMg = REAL ? 64 : BM;       // rows per tile
   static constexpr int BKg = BK_;                  // K chunk (elements)
   static constexpr int SAg = REAL ? BKg + 4 : SA;  // A row stride (elements)
-  static constexpr int BN = BN_, NI = 2, WN = BN_ / (8 * NI), WM = CWARPS / WN;
+  static constexpr int BN = BN_, NI = 2, WN = BN_ / (8 * NI), WM = CW / WN;
   static constexpr int MI = (REAL ? BMg / 8 : BMg / 4) / WM;
   static constexpr int SB = REAL ? BN_ + 8 : BN_ + 4;  // B row stride (elements)
   static constexpr int A_ELEMS = BMg * SAg * CPX / 2, B_ELEMS = BKg * SB * CPX / 2;  // double2 units
   static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
-  static constexpr size_t kSmemBytes = size_t(STAGES) * STAGE_ELEMS * sizeof(double2) + 256;
-  static_assert(WN * WM == CWARPS && MI * WM * (REAL ? 8 : 4) == BMg, "tile geometry");
+  static constexpr size_t kSmemBytes = size_t(ST) * STAGE_ELEMS * sizeof(double2) + 256;
+  static_assert(WN * WM == CW && MI * WM * (REAL ? 8 : 4) == BMg, "tile geometry");
   static_assert(REAL || BK_ == BK, "complex tiles use the global K chunk (SA and the B box follow BK)");
 };
 
@@ -133,10 +138,10 @@ template <class G>
 __device__ __forceinline__ Ring carve(unsigned char* smem) {
   Ring r;
   r.data = reinterpret_cast<double2*>(smem);
-  unsigned char* tail = smem + size_t(STAGES) * G::STAGE_ELEMS * sizeof(double2);
+  unsigned char* tail = smem + size_t(G::ST) * G::STAGE_ELEMS * sizeof(double2);
   r.full = reinterpret_cast<uint64_t*>(tail);
-  r.empty = r.full + STAGES;
-  r.hdr = reinterpret_cast<int*>(r.empty + STAGES);
+  r.empty = r.full + G::ST;
+  r.hdr = reinterpret_cast<int*>(r.empty + G::ST);
   return r;
 }
 
@@ -150,8 +155,9 @@ struct Problem {  // C (M x N) = A (M x K) * B (K x N), complex row-major
   int M, N, K;
 };
 
+template <int NST>
 __device__ __forceinline__ void advance(int& stage, unsigned& phase) {
-  if (++stage == STAGES) {
+  if (++stage == NST) {
     stage = 0;
     phase ^= 1u;
   }
@@ -189,31 +195,40 @@ __device__ __forceinline__ void produce_range_tma(const Ring& r, const Problem& 
       tma_g2s_2d(as + G::A_ELEMS, map_b, G::CPX * n0, b_row0 + kc * BK, &r.full[stage]);
     }
     __syncwarp();
-    advance(stage, phase);
+    advance<G::ST>(stage, phase);
   }
 }
 
+template <class G>
 __device__ __forceinline__ void produce_end(const Ring& r, int& stage, unsigned& phase, int lane) {
   mbar_wait(&r.empty[stage], phase ^ 1u);
   if (lane == 0) {
     r.hdr[4 * stage] = -1;
     mbar_arrive(&r.full[stage]);
   }
-  advance(stage, phase);
+  advance<G::ST>(stage, phase);
 }
 
 // Consumer warps: run tiles until the end-of-step sentinel.
-// Split tiles (stream-K): a tile cut between two CTAs' ranges has a HEAD part
-// (chunks from 0) and a TAIL part (chunks up to nk-1). The TAIL CTA computes its
-// part at the START of its range and publishes it (partial buffer + epoch
-// flag); the HEAD CTA reaches its part at the END of its range, adds the
-// published partial (fixed order: deterministic) and stores the tile.
+// Split tiles (stream-K): a tile cut between CTAs' ranges has a HEAD part
+// (chunks from 0), possibly MIDDLE parts (a CTA whose whole range lies inside
+// the tile) and a TAIL part (chunks up to nk-1). A TAIL or MIDDLE CTA reaches
+// its part at the START of its range and publishes it (its own partial slot +
+// epoch flag: a CTA publishes at most once per step); the HEAD CTA reaches its
+// part at the END of its range, adds the published partials of the CTAs after
+// it in CTA order (fixed order: deterministic) and stores the tile.
 struct SplitK {
-  double2* part;          // ntiles x (CWARPS x 32 lanes x MI x NI) accumulator slots
-  unsigned int* flags;    // ntiles, = epoch when the TAIL partial is published
+  double2* part;          // gridDim.x x (CW x 32 lanes x MI x NI) accumulator slots
+  unsigned int* flags;    // gridDim.x, = epoch when that CTA's partial is published
   unsigned int epoch;
+  long long work;         // (tile, K chunk) iterations per step
 };
-__device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, 256;\n" ::: "memory"); }
+// the CTA whose stream-K range [work c / G, work (c+1) / G) holds iteration x
+__device__ __forceinline__ unsigned cta_of_iter(long long x, long long work) {
+  return unsigned(((x + 1) * (long long)gridDim.x - 1) / work);
+}
+template <int NTHREADS>
+__device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(NTHREADS) : "memory"); }
 
 template <class G>
 __device__ __forceinline__ void consume(const Ring& r, const Problem& p, int tiles_m, int& stage,
@@ -230,9 +245,6 @@ __device__ __forceinline__ void consume(const Ring& r, const Problem& p, int til
   const int b_off = G::REAL ? tq * SB + wn * NI * 8 + gq
                             : 2 * (((lane & 3) >> 1) * SB + wn * NI * 8 + (lane >> 2)) + (lane & 1);
   double acc[MI][NI][2] = {};
-  bool row_ok[MI];
-#pragma unroll
-  for (int mi = 0; mi < MI; ++mi) row_ok[mi] = true;
   int m0 = 0, n0 = 0;
   while (true) {
     mbar_wait(&r.full[stage], phase);
@@ -241,31 +253,22 @@ __device__ __forceinline__ void consume(const Ring& r, const Problem& p, int til
     if (tile < 0) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&r.empty[stage]);
-      advance(stage, phase);
+      advance<G::ST>(stage, phase);
       return;
     }
     if (kc == lo) {
       m0 = (tile % tiles_m) * G::BMg;
       n0 = (tile / tiles_m) * BN;
 #pragma unroll
-      for (int mi = 0; mi < MI; ++mi) {
-        row_ok[mi] = G::REAL ? m0 + (wm * MI + mi) * 8 + gq < p.M : m0 + (wm * MI + mi) * 4 + af.di < p.M;
+      for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
         for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-      }
     }
     const double* ad = reinterpret_cast<const double*>(r.data + stage * STAGE_ELEMS) + a_off;
     const double* bd = reinterpret_cast<const double*>(r.data + stage * STAGE_ELEMS + G::A_ELEMS) + b_off;
-    const int k0 = kc * BK;
-    bool all_rows = true;
-#pragma unroll
-    for (int mi = 0; mi < MI; ++mi) all_rows = all_rows && row_ok[mi];
-    // row_ok depends on the lane's fragment row: the path choice must be
-    // warp-uniform, mma.sync needs all 32 lanes converged
-    all_rows = __all_sync(0xffffffffu, all_rows);
+    // rows >= M and k >= K arrive zero-filled by the TMA (the tensor maps end at
+    // M rows / K columns of A and K rows of B): no masking in the inner loop
     if constexpr (G::REAL) {
-      // rows >= M and k >= K arrive zero-filled by the TMA: no masking needed
-      (void)all_rows;
 #pragma unroll
       for (int ks = 0; ks < BK / 4; ++ks) {
         double a[MI], b[NI];
@@ -278,7 +281,7 @@ __device__ __forceinline__ void consume(const Ring& r, const Problem& p, int til
 #pragma unroll
           for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
       }
-    } else if (k0 + BK <= p.K && all_rows) {
+    } else {
 #pragma unroll
       for (int ks = 0; ks < BK / 2; ++ks) {
         double a[MI], b[NI];
@@ -291,57 +294,63 @@ __device__ __forceinline__ void consume(const Ring& r, const Problem& p, int til
 #pragma unroll
           for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
       }
-    } else {  // ragged edge: rows >= M and k >= K masked in registers
-#pragma unroll
-      for (int ks = 0; ks < BK / 2; ++ks) {
-        const bool kok = k0 + ks * 2 + af.dj < p.K;
-        double a[MI], b[NI];
-#pragma unroll
-        for (int mi = 0; mi < MI; ++mi)
-          a[mi] = (kok && row_ok[mi]) ? af.sign(ad[2 * (mi * 4 * SA) + 4 * ks]) : 0.0;
-#pragma unroll
-        for (int ni = 0; ni < NI; ++ni) b[ni] = kok ? bd[2 * (2 * ks * SB + ni * 8)] : 0.0;
-#pragma unroll
-        for (int mi = 0; mi < MI; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
-      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&r.empty[stage]);
-    advance(stage, phase);
+    advance<G::ST>(stage, phase);
     if (kc != hi) continue;
-    constexpr int SLOT = CWARPS * 32 * MI * NI;
-    if (sk && lo > 0) {  // TAIL part: publish the partial accumulators
-      double2* dst = sk->part + (long long)tile * SLOT;
+    constexpr int SLOT = G::CW * 32 * MI * NI;
+    if (sk && lo > 0) {  // TAIL / MIDDLE part: publish the partial accumulators
+      double2* dst = sk->part + (long long)blockIdx.x * SLOT;
 #pragma unroll
       for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
         for (int ni = 0; ni < NI; ++ni)
           __stcg(dst + ((warp * MI + mi) * NI + ni) * 32 + lane, make_double2(acc[mi][ni][0], acc[mi][ni][1]));
-      consumer_bar();
+      consumer_bar<32 * G::CW>();
       if (warp == 0 && lane == 0)  // release store: cumulative over the warps' partials (consumer barrier)
-        asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(sk->flags + tile), "r"(sk->epoch) : "memory");
+        asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(sk->flags + blockIdx.x), "r"(sk->epoch)
+                     : "memory");
       continue;
     }
-    if (sk && hi < nk - 1) {  // HEAD part: add the TAIL partial, then store
+    if (sk && hi < nk - 1) {  // HEAD part: add the later parts' partials in CTA order, then store
+      const unsigned c_last = cta_of_iter((long long)(tile + 1) * nk - 1, sk->work);
       if (warp == 0 && lane == 0) {
-        while (true) {
-          unsigned v;
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(sk->flags + tile) : "memory");
-          if (v == sk->epoch) break;
-        }
+        for (unsigned c = blockIdx.x + 1; c <= c_last; ++c)
+          while (true) {
+            unsigned v;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(sk->flags + c) : "memory");
+            if (v == sk->epoch) break;
+          }
       }
-      consumer_bar();
-      const double2* src = sk->part + (long long)tile * SLOT;
+      consumer_bar<32 * G::CW>();
+      // partials of up to kBatch contributors are loaded together (one L2
+      // round trip per batch), then added in CTA order
+      constexpr int kBatch = 4;
+      for (unsigned c0 = blockIdx.x + 1; c0 <= c_last; c0 += kBatch) {
+        double2 q[kBatch][MI][NI];
 #pragma unroll
-      for (int mi = 0; mi < MI; ++mi)
+        for (int j = 0; j < kBatch; ++j) {
+          const double2* src = sk->part + (long long)(c0 + j) * SLOT;
 #pragma unroll
-        for (int ni = 0; ni < NI; ++ni) {
-          const double2 q = __ldcg(src + ((warp * MI + mi) * NI + ni) * 32 + lane);
-          acc[mi][ni][0] += q.x;
-          acc[mi][ni][1] += q.y;
+          for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni)
+              q[j][mi][ni] = c0 + j <= c_last ? __ldcg(src + ((warp * MI + mi) * NI + ni) * 32 + lane)
+                                              : make_double2(0.0, 0.0);
         }
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j)
+          if (c0 + j <= c_last) {
+#pragma unroll
+            for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+              for (int ni = 0; ni < NI; ++ni) {
+                acc[mi][ni][0] += q[j][mi][ni].x;
+                acc[mi][ni][1] += q[j][mi][ni].y;
+              }
+          }
+      }
     }
     if constexpr (G::REAL) {  // tile done: registers -> global (row g, columns 2t, 2t+1)
       double* C = reinterpret_cast<double*>(p.C);
@@ -371,11 +380,12 @@ __device__ __forceinline__ void consume(const Ring& r, const Problem& p, int til
   }
 }
 
+template <class G>
 __device__ __forceinline__ void init_ring(const Ring& r) {
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < G::ST; ++s) {
       mbar_init(&r.full[s], 1);
-      mbar_init(&r.empty[s], CWARPS);
+      mbar_init(&r.empty[s], G::CW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -390,7 +400,7 @@ __device__ __forceinline__ void init_ring(const Ring& r) {
 // G complex (zgemm) or REAL (dgemm on matrices with leading dimension ld; the
 // batch strides sa / sb / sc are in elements)
 template <class G>
-__global__ void __launch_bounds__(THREADS) gemm_kernel(const double2* __restrict__ A,
+__global__ void __launch_bounds__(G::NT) gemm_kernel(const double2* __restrict__ A,
                                                        const double2* __restrict__ B,
                                                        double2* __restrict__ C, int n, int ld,
                                                        long long sa, long long sb, long long sc,
@@ -414,17 +424,17 @@ __global__ void __launch_bounds__(THREADS) gemm_kernel(const double2* __restrict
   }
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const Ring r = carve<G>(smem_raw);
-  init_ring(r);
+  init_ring<G>(r);
   const Problem p{A + off(b * sa), ld, B + off(b * sb), ld, C + off(b * sc), ld, n, n, n};
   const int tiles_m = (n + G::BMg - 1) / G::BMg;
   const int tile = blockIdx.y * tiles_m + blockIdx.x;
   int stage = 0;
   unsigned phase = 0;
-  if (warp == CWARPS) {
+  if (warp == G::CW) {
     const long long nk = (n + G::BKg - 1) / G::BKg;
     produce_range_tma<G>(r, p, &map_a, &map_b, tiles_m, tile * nk, (tile + 1) * nk, stage, phase, lane,
                          sa ? b * n : 0, sb ? b * n : 0);
-    produce_end(r, stage, phase, lane);
+    produce_end<G>(r, stage, phase, lane);
   } else {
     consume<G>(r, p, tiles_m, stage, phase, warp, lane, nullptr);
   }
@@ -441,34 +451,21 @@ struct StepCtl {
   unsigned int pad;
 };
 
-__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int target) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    // release-add after the CTA barrier (cumulativity carries the other warps'
-    // stores; no full membar), acquire poll (no trailing fence needed)
-    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(bar) : "memory");
-    while (true) {
-      unsigned int v;
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(bar) : "memory");
-      if (v >= target) break;
-    }
-  }
-  __syncthreads();
-}
 
 template <class G>
-__global__ void __launch_bounds__(THREADS) tiled_evolve_kernel(const double2* __restrict__ P, int n,
+__global__ void __launch_bounds__(G::NT) tiled_evolve_kernel(const double2* __restrict__ P, int n,
                                                                double2* v0, double2* v1,
                                                                int batch, int ldv, int64_t steps,
                                                                StepCtl* ctl, double2* part,
                                                                unsigned int* flags,
+                                                               unsigned long long* trace,
                                                                const __grid_constant__ CUtensorMap map_p,
                                                                const __grid_constant__ CUtensorMap map_v0,
                                                                const __grid_constant__ CUtensorMap map_v1) {
   constexpr int BN = G::BN;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const Ring r = carve<G>(smem_raw);
-  init_ring(r);
+  init_ring<G>(r);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_m = (n + G::BMg - 1) / G::BMg, tiles_n = (batch + BN - 1) / BN;
   const int ntiles = tiles_m * tiles_n;
@@ -477,22 +474,35 @@ __global__ void __launch_bounds__(THREADS) tiled_evolve_kernel(const double2* __
   int stage = 0;
   unsigned phase = 0;
   // stream-K: this CTA's fixed, contiguous share of the step's (tile, K chunk)
-  // iterations; grid <= ntiles keeps every range >= one tile, so a tile is
-  // split across at most two CTAs
+  // iterations; with grid > ntiles (small batches) a tile is split across
+  // several CTAs (HEAD + MIDDLE + TAIL parts)
   const long long nk = (n + G::BKg - 1) / G::BKg, work = (long long)ntiles * nk;
   const long long it0 = work * blockIdx.x / gridDim.x, it1 = work * (blockIdx.x + 1) / gridDim.x;
+  // trace (measurement only, LBG_TILED_TRACE): %globaltimer per step and CTA at
+  // the step start and when each warp leaves its role, first kTraceSteps steps
+  constexpr int kTraceSteps = 64;
+  auto stamp = [&](int64_t s, int slot) {
+    if (trace && s < kTraceSteps && lane == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      trace[((size_t)s * gridDim.x + blockIdx.x) * (G::CW + 2) + slot] = t;
+    }
+  };
   for (int64_t s = 0; s < steps; ++s) {
     const Problem p{P, n, cur, ldv, nxt, ldv, n, batch, n};
-    if (warp == CWARPS) {
+    if (warp == 0) stamp(s, 0);
+    if (warp == G::CW) {
       // generic-proxy stores of the previous step -> async-proxy (bulk copy) reads
       asm volatile("fence.proxy.async.global;\n" ::: "memory");
       produce_range_tma<G>(r, p, &map_p, (s & 1) ? &map_v1 : &map_v0, tiles_m, it0, it1, stage, phase, lane);
-      produce_end(r, stage, phase, lane);
+      produce_end<G>(r, stage, phase, lane);
+      stamp(s, G::CW + 1);
     } else {
-      const SplitK sk{part, flags, unsigned(s + 1)};
+      const SplitK sk{part, flags, unsigned(s + 1), work};
       consume<G>(r, p, tiles_m, stage, phase, warp, lane, &sk);
+      stamp(s, 1 + warp);
     }
-    grid_barrier(&ctl->barrier, unsigned(s + 1) * gridDim.x);
+    grid_barrier_sync(&ctl->barrier, unsigned(s + 1) * gridDim.x);
     double2* tmp = cur;
     cur = nxt;
     nxt = tmp;
@@ -606,7 +616,7 @@ size_t ntiles_of(size_t n, int64_t batch) {
 }
 template <class G>
 constexpr size_t slot_of() {  // double2 per split tile
-  return size_t(CWARPS) * 32 * G::MI * G::NI;
+  return size_t(G::CW) * 32 * G::MI * G::NI;
 }
 // real rows must be 16-byte aligned for the TMA: even leading dimensions
 inline size_t even(size_t x) { return x + (x & 1); }
@@ -614,15 +624,55 @@ template <class G>
 size_t ldv_of(int64_t batch) {
   return G::REAL ? even(size_t(batch)) : size_t(batch);
 }
+// Persistent grid of the stepping engine. With at least as many tiles as
+// resident slots (occupancy x SMs): every slot, stream-K splitting a tile
+// between at most two CTAs. With fewer tiles (small batches: c3 at 128
+// trajectories = 92 tiles): one CTA per SM and several-way tile splits (HEAD +
+// MIDDLE + TAIL parts) instead of idle SMs — 1 CTA / SM measured 4.8 vs 5.0 ms
+// for 3 / SM at c3 B = 128 (the three CTAs of an SM progress unevenly and the
+// HEADs wait for the slowest contributor). With fewer iterations than
+// kMinItersPerCta per SM: one CTA per tile, a whole multiple of the SM count
+// when there are at least as many tiles as SMs.
+// LBG_TILED_GRID overrides (measurement only).
+template <class G>
+int tiled_grid_of(size_t n, int64_t batch) {
+  const auto kern = tiled_evolve_kernel<G>;
+  ensure_max_dyn_smem((const void*)kern, int(G::kSmemBytes));
+  int occ = 0;
+  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, G::NT, G::kSmemBytes), "occupancy");
+  const int sms = sm_count(), slots = std::max(1, occ * sms);
+  const long long nt = (long long)ntiles_of<G>(n, batch), nk = ((long long)n + G::BKg - 1) / G::BKg;
+  constexpr long long kMinItersPerCta = 3;
+  int grid;
+  if (nt >= slots) {
+    grid = slots;
+  } else if (nt < sms && nt * nk >= kMinItersPerCta * sms) {
+    grid = sms;
+  } else {
+    grid = int(nt);
+    if (grid >= sms) grid -= grid % sms;
+  }
+  static const int forced = [] {
+    const char* e = std::getenv("LBG_TILED_GRID");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced > 0) grid = std::min(forced, slots);
+  return std::max(1, grid);
+}
+template <class G>
+size_t aux_workspace_of(size_t n, int64_t batch) {
+  const size_t g = size_t(tiled_grid_of<G>(n, batch));
+  return align_up(sizeof(StepCtl)) + align_up(g * slot_of<G>() * sizeof(double2)) + align_up(g * sizeof(unsigned int));
+}
 template <class G>
 size_t workspace_of(size_t n, int64_t batch) {
-  const size_t nt = ntiles_of<G>(n, batch);
   const size_t vbytes = size_t(G::CPX) * 8 * n * ldv_of<G>(batch);
-  return 2 * align_up(vbytes) + align_up(sizeof(StepCtl)) + align_up(nt * slot_of<G>() * sizeof(double2)) +
-         align_up(nt * sizeof(unsigned int));
+  return 2 * align_up(vbytes) + aux_workspace_of<G>(n, batch);
 }
 
-size_t tiled_workspace(size_t n, int64_t batch) { return workspace_of<StepGeo>(n, batch); }
+size_t tiled_workspace(size_t n, int64_t batch) {
+  return workspace_of<StepGeo>(n, batch);
+}
 size_t tiled_real_workspace(size_t n, int64_t batch) {
   return workspace_of<StepGeoR>(n, batch) + align_up(8 * n * even(n));  // + an even-stride copy of P_R
 }
@@ -670,14 +720,6 @@ __global__ void convert_real_kernel(double* __restrict__ x, double* __restrict__
   }
 }
 
-// persistent cooperative stepping for geometry G; v0 already holds V[k][b]
-// stream-K control, split-tile partials and flags (after the two state buffers)
-template <class G>
-size_t aux_workspace_of(size_t n, int64_t batch) {
-  const size_t nt = ntiles_of<G>(n, batch);
-  return align_up(sizeof(StepCtl)) + align_up(nt * slot_of<G>() * sizeof(double2)) + align_up(nt * sizeof(unsigned int));
-}
-
 // the persistent stream-K engine on caller-given state buffers: v0 holds V_0,
 // step s reads V_s and writes V_{s+1} into the other buffer (v1 after an odd
 // count). aux: aux_workspace_of<G>(n, batch) bytes.
@@ -686,24 +728,14 @@ void run_tiled_ext(const double* p_dev, size_t ldp, size_t n, int64_t batch, int
                    void* aux, cudaStream_t s) {
   const size_t ldv = ldv_of<G>(batch);
   StepCtl* ctl = static_cast<StepCtl*>(aux);
-  const size_t nt = ntiles_of<G>(n, batch);
+  const int grid = tiled_grid_of<G>(n, batch);
   double2* part = reinterpret_cast<double2*>(reinterpret_cast<char*>(ctl) + align_up(sizeof(StepCtl)));
-  unsigned int* flags =
-      reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(part) + align_up(nt * slot_of<G>() * sizeof(double2)));
-  check_cuda(cudaMemsetAsync(flags, 0, nt * sizeof(unsigned int), s), "memset flags");
+  unsigned int* flags = reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(part) +
+                                                        align_up(size_t(grid) * slot_of<G>() * sizeof(double2)));
+  check_cuda(cudaMemsetAsync(flags, 0, size_t(grid) * sizeof(unsigned int), s), "memset flags");
   check_cuda(cudaMemsetAsync(ctl, 0, sizeof(StepCtl), s), "memset ctl");
   if (steps <= 0) return;
   const auto kern = tiled_evolve_kernel<G>;
-  ensure_max_dyn_smem((const void*)kern, int(G::kSmemBytes));
-  int occ = 0;
-  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, THREADS, G::kSmemBytes), "occupancy");
-  // stream-K needs grid <= ntiles; when fewer tiles than resident slots exist,
-  // a whole multiple of the SM count keeps every SM's share equal (384 real
-  // tiles at c3 on 444 slots: 384 CTAs = 3 tiles on some SMs, 2 on others)
-  const int sms = sm_count();
-  int grid = std::min<int>(occ * sms, int(nt));
-  if (grid < occ * sms && grid >= sms) grid -= grid % sms;
-  if (grid < 1) grid = 1;
   const double2* p2 = reinterpret_cast<const double2*>(p_dev);
   int ni = int(n), bi = int(batch), li = int(ldv);
   int64_t st = steps;
@@ -718,11 +750,31 @@ void run_tiled_ext(const double* p_dev, size_t ldp, size_t n, int64_t batch, int
     map_v0 = complex_map(v0, n, size_t(batch), BK, G::SB);
     map_v1 = complex_map(v1, n, size_t(batch), BK, G::SB);
   }
-  void* args[] = {(void*)&p2, (void*)&ni, (void*)&v0, (void*)&v1, (void*)&bi, (void*)&li, (void*)&st,
-                  (void*)&ctl, (void*)&part, (void*)&flags, (void*)&map_p, (void*)&map_v0, (void*)&map_v1};
-  check_cuda(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(THREADS), args, G::kSmemBytes, s),
+  static const char* trace_path = std::getenv("LBG_TILED_TRACE");  // measurement only
+  unsigned long long* trace = nullptr;
+  const size_t trace_n = size_t(64) * grid * (G::CW + 2);
+  if (trace_path) {
+    check_cuda(cudaMalloc(&trace, trace_n * 8), "trace");
+    check_cuda(cudaMemsetAsync(trace, 0, trace_n * 8, s), "trace");
+  }
+  void* args[] = {(void*)&p2,    (void*)&ni,    (void*)&v0,    (void*)&v1,     (void*)&bi,
+                  (void*)&li,    (void*)&st,    (void*)&ctl,   (void*)&part,   (void*)&flags,
+                  (void*)&trace, (void*)&map_p, (void*)&map_v0, (void*)&map_v1};
+  check_cuda(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(G::NT), args, G::kSmemBytes, s),
              "tiled_evolve_kernel (cooperative)");
   note_launch();
+  if (trace) {
+    std::vector<unsigned long long> h(trace_n);
+    check_cuda(cudaMemcpyAsync(h.data(), trace, trace_n * 8, cudaMemcpyDeviceToHost, s), "trace");
+    check_cuda(cudaStreamSynchronize(s), "trace");
+    cudaFree(trace);
+    if (FILE* f = std::fopen(trace_path, "wb")) {
+      const int hdr[3] = {grid, G::CW + 2, int(std::min<int64_t>(steps, 64))};
+      std::fwrite(hdr, sizeof hdr, 1, f);
+      std::fwrite(h.data(), 8, trace_n, f);
+      std::fclose(f);
+    }
+  }
 }
 
 template <class G>
@@ -782,7 +834,7 @@ void launch_zgemm(const double* a, const double* b, double* c, int n, int batch,
                                         size_t(n), BM, SA);
   const CUtensorMap map_b = complex_map(reinterpret_cast<const double2*>(b), size_t(n) * (stride_b ? batch : 1),
                                         size_t(n), BK, Geo<32>::SB);
-  gemm_kernel<Geo<32>><<<grid, THREADS, Geo<32>::kSmemBytes, s>>>(reinterpret_cast<const double2*>(a),
+  gemm_kernel<Geo<32>><<<grid, Geo<32>::NT, Geo<32>::kSmemBytes, s>>>(reinterpret_cast<const double2*>(a),
                                                                    reinterpret_cast<const double2*>(b),
                                                                    reinterpret_cast<double2*>(c), n, n, stride_a,
                                                                    stride_b, stride_c, map_a, map_b, nullptr, 0);
@@ -812,7 +864,7 @@ void launch_dgemm(const double* a, const double* b, double* c, int n, int ld, in
   const dim3 grid((n + G::BMg - 1) / G::BMg, (n + G::BN - 1) / G::BN, batch);
   const CUtensorMap map_a = real_map(a, size_t(n) * (stride_a ? batch : 1), size_t(n), size_t(ld), G::BMg, G::SAg);
   const CUtensorMap map_b = real_map(b, size_t(n) * (stride_b ? batch : 1), size_t(n), size_t(ld), G::BKg, G::SB);
-  gemm_kernel<G><<<grid, THREADS, G::kSmemBytes, s>>>(reinterpret_cast<const double2*>(a),
+  gemm_kernel<G><<<grid, G::NT, G::kSmemBytes, s>>>(reinterpret_cast<const double2*>(a),
                                                       reinterpret_cast<const double2*>(b),
                                                       reinterpret_cast<double2*>(c), n, ld, stride_a, stride_b,
                                                       stride_c, map_a, map_b, cond, cond_idx);
