@@ -43,6 +43,7 @@ extern "C" {
 #define LBG_ALGO_CTA 5     /* K2b: n <= 96, one CTA per trajectory, P in shared memory (few trajectories) */
 #define LBG_ALGO_ROWSPLIT 6 /* K2c: any n, batch <= 4, P's rows spread over all SMs' shared memory */
 #define LBG_ALGO_CLUSTER 7  /* K1b-C: n == 81, 2-CTA clusters share a split n-tile through DSMEM */
+#define LBG_ALGO_KSPLIT 8   /* K1b-K: n == 81, small batches: 2-CTA clusters split K, partials through DSMEM */
 
 const char* lbg_last_error(void);
 const char* lbg_version(void);

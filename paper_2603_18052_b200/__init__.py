@@ -38,7 +38,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liblbg.so")
 SEED = 42  # lb::kDefaultSeed (proj/include/lb/random.hpp:10)
 
-ALGO = {"auto": 0, "chain": 1, "dfma9": 2, "smem": 3, "tiled": 4, "cta": 5, "rowsplit": 6, "cluster": 7}
+ALGO = {"auto": 0, "chain": 1, "dfma9": 2, "smem": 3, "tiled": 4, "cta": 5, "rowsplit": 6, "cluster": 7, "ksplit": 8}
 SWEEP_MODE = {"auto": 0, "complex": 1, "real": 2}
 
 _dp = C.POINTER(C.c_double)

@@ -124,6 +124,8 @@ int choose_algo(size_t n, int64_t batch, int algo, Layout layout = Layout::aos) 
   if (chain_supported(n) && batch <= 512) return LBG_ALGO_CHAIN;
   if (n == 9) return LBG_ALGO_DFMA9;
   if (layout == Layout::aos && cta_chain_supported(n) && batch <= 256) return LBG_ALGO_CTA;
+  if (ksplit_supported(n) && ksplit_cost(n, batch) < std::min(cluster_cost(n, batch), smem81_cost(batch)))
+    return LBG_ALGO_KSPLIT;
   if (cluster_preferred(n, batch)) return LBG_ALGO_CLUSTER;
   if (smem_supported(n)) return LBG_ALGO_SMEM;
   if (layout == Layout::aos && batch <= 2 && rowsplit_supported(n, batch)) return LBG_ALGO_ROWSPLIT;
@@ -166,6 +168,9 @@ void evolve_dev(const double* p, size_t n, double* x_re, double* x_im, double* x
     case LBG_ALGO_CLUSTER:
       if (!cluster_supported(n)) throw invalid_argument("evolve: cluster kernel needs n == 81");
       return launch_smem_cluster(p, x_re, x_im, x_aos, batch, steps, layout, s);
+    case LBG_ALGO_KSPLIT:
+      if (!ksplit_supported(n)) throw invalid_argument("evolve: ksplit kernel needs n == 81");
+      return launch_ksplit(p, n, x_re, x_im, x_aos, batch, steps, layout, s);
     case LBG_ALGO_TILED:
       return launch_tiled_evolve(p, n, x_re, x_im, x_aos, batch, steps, layout, work, s);
     case LBG_ALGO_CTA:

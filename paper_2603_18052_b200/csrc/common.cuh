@@ -89,4 +89,44 @@ __device__ __forceinline__ void grid_barrier_sync(unsigned int* bar, unsigned in
   __syncthreads();
 }
 
+// ---- thread-block cluster / DSMEM primitives (PTX) ----------------------------
+__device__ __forceinline__ unsigned cluster_ctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// shared::cluster address of `local` in the shared memory of CTA `peer`
+__device__ __forceinline__ unsigned mapa_shared(const void* local, unsigned peer) {
+  unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(local)), r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(a), "r"(peer));
+  return r;
+}
+// asynchronous remote store that counts its 16 bytes on the receiver's mbarrier
+__device__ __forceinline__ void st_async_f64x2(unsigned addr, double2 v, unsigned remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(addr),
+               "d"(v.x), "d"(v.y), "r"(remote_bar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
+                   static_cast<unsigned>(__cvta_generic_to_shared(bar))),
+               "r"(bytes)
+               : "memory");
+}
+// wait for phase `parity` of a CTA-local mbarrier whose transaction bytes are
+// the peers' st.async stores: the stores complete on this mbarrier, so the
+// default (CTA-scope acquire) wait orders the reads of the landed bytes; an
+// .acquire.cluster wait compiles to a CCTL.IVALL (L1 invalidate) per poll,
+// measured as 25% of the stall samples of K1b-K.
+__device__ __forceinline__ void mbar_wait_parity_cluster(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n" ::"r"(
+          static_cast<unsigned>(__cvta_generic_to_shared(bar))),
+      "r"(parity)
+      : "memory");
+}
+
 }  // namespace lbg

@@ -52,6 +52,14 @@ void launch_smem(const double* p_dev, std::size_t n, double* x_re, double* x_im,
 // K1b-C — n = 81 on 2-CTA clusters, DSMEM exchange of a split n-tile (k_cluster.cu)
 bool cluster_supported(std::size_t n);
 bool cluster_preferred(std::size_t n, int64_t batch);
+int64_t cluster_cost(std::size_t n, int64_t batch);  // DMMA slots per sub-partition per step
+int64_t smem81_cost(int64_t batch);
+// K1b-K — n = 81 at small batches: 2-CTA clusters split K, P in registers (k_ksplit.cu)
+bool ksplit_supported(std::size_t n);
+int ksplit_group(std::size_t n, int64_t batch);
+int64_t ksplit_cost(std::size_t n, int64_t batch);
+void launch_ksplit(const double* p_dev, std::size_t n, double* x_re, double* x_im, double* x_aos, int64_t batch,
+                   int64_t steps, Layout layout, cudaStream_t s);
 void launch_smem_cluster(const double* p_dev, double* x_re, double* x_im, double* x_aos, int64_t batch,
                          int64_t steps, Layout layout, cudaStream_t s);
 // K1c — any n, persistent DMMA tiles streamed from L2 (k_tiled.cu)

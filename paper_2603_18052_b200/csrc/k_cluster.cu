@@ -19,6 +19,7 @@
 // Layouts are K1b's (k_smem.cu): P real-form A fragments from complex rows
 // (stride 2 mod 8 complex), V[traj][2n] real form (stride 4 mod 16 doubles).
 #include <algorithm>
+#include <cstdint>
 #include <vector>
 
 #include "common.cuh"
@@ -53,39 +54,6 @@ struct ClusterPlan {
   signed char nheavy[2][CWARPS];
 };
 
-__device__ __forceinline__ unsigned cluster_rank() {
-  unsigned r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-__device__ __forceinline__ unsigned peer_addr(const void* local, unsigned peer) {
-  unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(local)), r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(a), "r"(peer));
-  return r;
-}
-// asynchronous remote store that counts its bytes on the PEER's mbarrier
-__device__ __forceinline__ void st_async_v2(unsigned addr, double2 v, unsigned peer_bar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(addr),
-               "d"(v.x), "d"(v.y), "r"(peer_bar)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_expect(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
-                   static_cast<unsigned>(__cvta_generic_to_shared(bar))),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n" ::"r"(
-          static_cast<unsigned>(__cvta_generic_to_shared(bar))),
-      "r"(parity)
-      : "memory");
-}
-
 // One warp's step loop. NH "heavy" m-tiles (3 own n-tiles + the shared one)
 // and NL "light" m-tiles (own n-tiles only) are compile-time counts, so the
 // DMMA sequence has no predicates (a runtime count makes ptxas wrap every
@@ -106,7 +74,7 @@ __device__ __forceinline__ double* warp_steps(const double* __restrict__ pbase, 
   for (int64_t s = 0; s < steps; ++s) {
     // step parity selects the mbarrier: the peer cannot run two steps ahead
     const int par = int(s & 1);
-    if (threadIdx.x == 0) mbar_expect(&xbar[par], in_bytes);
+    if (threadIdx.x == 0) mbar_expect_tx(&xbar[par], in_bytes);
     double acc[NM > 0 ? NM : 1][NQ][2];
 #pragma unroll
     for (int mi = 0; mi < NM; ++mi)
@@ -150,12 +118,12 @@ __device__ __forceinline__ double* warp_steps(const double* __restrict__ pbase, 
         const int t = q * 8 + coff;
         if (i < CN) {
           *reinterpret_cast<double2*>(vb + t * SV + 2 * i) = z;
-          if (q == NQ - 1) st_async_v2(vb_peer + unsigned(t * SV + 2 * i) * 8u, z, peer_bar);
+          if (q == NQ - 1) st_async_f64x2(vb_peer + unsigned(t * SV + 2 * i) * 8u, z, peer_bar);
         }
       }
     }
     __syncthreads();                                    // own results written locally
-    mbar_wait_cluster(&xbar[par], unsigned((s >> 1) & 1));  // the peer's half has landed
+    mbar_wait_parity_cluster(&xbar[par], unsigned((s >> 1) & 1));  // the peer's half has landed
     double* tmp = va;
     va = vb;
     vb = tmp;
@@ -176,7 +144,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * CWARPS, 1)
   double* va = reinterpret_cast<double*>(smem + P_BYTES);
   double* vb = reinterpret_cast<double*>(smem + P_BYTES + V_BYTES);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const unsigned rank = cluster_rank(), peer = rank ^ 1u;
+  const unsigned rank = cluster_ctarank(), peer = rank ^ 1u;
   const int64_t cl = blockIdx.x >> 1;
   constexpr int K = 7, H = 3;
   // n-tile of slot s: own s < 3, shared s == 3
@@ -208,12 +176,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * CWARPS, 1)
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  cluster_sync();  // the peer's buffers and mbarriers exist before any remote store
+  cluster_sync_all();  // the peer's buffers and mbarriers exist before any remote store
 
   const AFragLane af(lane);
   const double* pbase = reinterpret_cast<const double*>(ps) + size_t(af.di) * 2 * SP + 2 * af.dj + af.comp;
-  const unsigned vb_peer0 = peer_addr(vb, peer), va_peer0 = peer_addr(va, peer);
-  const unsigned peer_bar0 = peer_addr(&xbar[0], peer);
+  const unsigned vb_peer0 = mapa_shared(vb, peer), va_peer0 = mapa_shared(va, peer);
+  const unsigned peer_bar0 = mapa_shared(&xbar[0], peer);
   // bytes the peer sends per step: its half's valid complex rows x 8 trajectories x 16 B
   const int prow0 = plan.lo[peer] * 4, prow1 = min(plan.hi[peer] * 4, CN);
   const unsigned in_bytes = unsigned(prow1 - prow0) * 8u * 16u;
@@ -230,7 +198,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * CWARPS, 1)
     default: __trap();
   }
 
-  cluster_sync();  // no CTA exits while its peer may still address its shared memory
+  cluster_sync_all();  // no CTA exits while its peer may still address its shared memory
   // ---- write back: own slots; the shared slot by rank 0 ----
   for (int e = tid; e < SLOTS * 8 * 2 * CN; e += blockDim.x) {
     const int t = e / (2 * CN), r = e - t * 2 * CN;
@@ -323,13 +291,13 @@ const ClusterPlan& plan7() {
 
 bool cluster_supported(std::size_t n) { return n == size_t(CN); }
 
-// Is the cluster kernel's critical path (waves x the busiest warp's DMMAs per
-// k-step per sub-partition) shorter than K1b's (waves x 21: 3 warps x 7)?
-bool cluster_preferred(std::size_t n, int64_t batch) {
-  if (n != size_t(CN) || batch <= 0) return false;
+// Critical paths in DMMA issue slots per sub-partition and step: K1b-C =
+// waves x the busiest sub-partition's DMMAs per k-step x 41 k-steps; K1b =
+// waves x 21 (3 warps x 7 m-tiles) x 41.
+int64_t cluster_cost(std::size_t n, int64_t batch) {
+  if (n != size_t(CN) || batch <= 0) return INT64_MAX;
   const int sms = sm_count();
   const int64_t nt = (batch + 7) / 8;
-  const int64_t k1b = ((((nt + 3) / 4) + sms - 1) / sms) * 21;
   const ClusterPlan& pl = plan7();
   int busiest = 0;
   for (int r = 0; r < 2; ++r)
@@ -339,7 +307,15 @@ bool cluster_preferred(std::size_t n, int64_t batch) {
       busiest = std::max(busiest, load);
     }
   const int64_t clusters = (nt + 6) / 7, per_wave = std::max(1, sms / 2);
-  return ((clusters + per_wave - 1) / per_wave) * busiest < k1b;
+  return ((clusters + per_wave - 1) / per_wave) * busiest * CKT;
+}
+int64_t smem81_cost(int64_t batch) {
+  const int64_t nt = (batch + 7) / 8;
+  return ((((nt + 3) / 4) + sm_count() - 1) / sm_count()) * 21 * CKT;
+}
+// Is the cluster kernel's critical path shorter than K1b's?
+bool cluster_preferred(std::size_t n, int64_t batch) {
+  return n == size_t(CN) && batch > 0 && cluster_cost(n, batch) < smem81_cost(batch);
 }
 
 void launch_smem_cluster(const double* p_dev, double* x_re, double* x_im, double* x_aos, int64_t batch,

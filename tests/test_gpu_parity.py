@@ -21,7 +21,7 @@ TOL_INV = 1e-12
 ALGOS_FOR = {  # which kernel paths can run a given n
     4: ("chain", "smem", "tiled", "cta", "rowsplit"),
     9: ("chain", "dfma9", "smem", "tiled", "cta", "rowsplit"),
-    81: ("smem", "cluster", "tiled", "cta", "rowsplit"),
+    81: ("smem", "cluster", "ksplit", "tiled", "cta", "rowsplit"),
     729: ("tiled", "rowsplit"),
 }
 
@@ -198,16 +198,19 @@ def test_config1_full_size(lbg, torch, oracle):
     _full_run(lbg, torch, 1, 1 << 20, 1000, "dfma9", rng.integers(0, 1 << 20, 64), oracle)
 
 
-@pytest.mark.parametrize("algo", ["smem", "cluster"])
+@pytest.mark.parametrize("algo", ["smem", "cluster", "ksplit"])
 def test_config2_full_size(lbg, torch, oracle, algo):
     rng = np.random.default_rng(1)
     _full_run(lbg, torch, 2, 4096, 1000, algo, list(rng.integers(0, 4096, 24)) + [4095], oracle)
 
 
-@pytest.mark.parametrize("B", [1, 7, 8, 9, 55, 56, 57, 600, 1000, 5000])
-def test_cluster_batch_shapes_vs_smem(lbg, torch, B):
-    """every cluster plan (k = 1..7 n-tiles per 2-CTA cluster, split and unsplit,
-    ragged last cluster) against the single-CTA kernel, both layouts"""
+@pytest.mark.parametrize("algo", ["cluster", "ksplit"])
+@pytest.mark.parametrize("B", [1, 7, 8, 9, 55, 56, 57, 64, 100, 512, 600, 1000, 1024, 2048, 2500, 5000])
+def test_cluster_batch_shapes_vs_smem(lbg, torch, B, algo):
+    """every cluster plan against the single-CTA kernel, both layouts: K1b-C
+    (k = 1..7 n-tiles per 2-CTA cluster, split and unsplit, ragged last cluster)
+    and K1b-K (K split over the 2-CTA cluster, G = 1..4 n-tiles per cluster,
+    ragged last n-tile, more clusters than SM pairs)"""
     rng = np.random.default_rng(B)
     n = 81
     P = (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) / (2 * n)
@@ -215,15 +218,15 @@ def test_cluster_batch_shapes_vs_smem(lbg, torch, B):
     dev = torch.device("cuda")
     pt = torch.from_numpy(P).to(dev)
     outs = {}
-    for algo in ("smem", "cluster"):
+    for a in ("smem", algo):
         xt = torch.from_numpy(x.copy()).to(dev)
-        lbg.evolve_batch_dev(pt, xt, 9, algo=algo)
-        outs[algo] = xt.cpu().numpy()
-    assert np.abs(outs["cluster"] - outs["smem"]).max() <= 1e-13 * max(1.0, np.abs(outs["smem"]).max())
+        lbg.evolve_batch_dev(pt, xt, 9, algo=a)
+        outs[a] = xt.cpu().numpy()
+    assert np.abs(outs[algo] - outs["smem"]).max() <= 1e-13 * max(1.0, np.abs(outs["smem"]).max())
     xr = torch.from_numpy(np.ascontiguousarray(x.real)).to(dev)
     xi = torch.from_numpy(np.ascontiguousarray(x.imag)).to(dev)
     L = lbg.lib()
-    lbg._check(L.lbg_evolve_shared_p_soa_dev(lbg._tp(pt), n, lbg._tp(xr), lbg._tp(xi), B, 9, lbg.ALGO["cluster"],
+    lbg._check(L.lbg_evolve_shared_p_soa_dev(lbg._tp(pt), n, lbg._tp(xr), lbg._tp(xi), B, 9, lbg.ALGO[algo],
                                              None, None), "soa")
     got = xr.cpu().numpy() + 1j * xi.cpu().numpy()
     assert np.abs(got - outs["smem"]).max() <= 1e-13 * max(1.0, np.abs(outs["smem"]).max())
