@@ -142,7 +142,8 @@ int lbg_evolve_density(const double* p, size_t d, const double* rho0, int64_t ba
  *   H_b = h0 + delta[b] * hd + scale[b] * hs,   L_k fixed,
  *   L_b = build_lindbladian(H_b, L_k),  P_b = exp(L_b dt),
  *   rho_b <- P_b^steps rho0      (fused on the GPU: assembly K5, expm K4,
- *                                  P_b-resident stepping K3; P_b never leaves the chip)
+ *                                  stepping K3; in the default REAL mode P_R (52 KB per
+ *                                  trajectory) passes through HBM once between K4 and K3)
  * Outputs: pops[b*d + i] = Re rho_b[i][i]; ens_sum (d*d AoS) += sum_b rho_b.
  * Replaces, per trajectory, the make_model + build_lindbladian + expm + step
  * sequence of lb::grape_chain (propagate.cpp:130-160). Device pointers.
@@ -185,6 +186,25 @@ int lbg_grape_chain(size_t d, const double* h0, const double* hc, const double* 
  * ------------------------------------------------------------------------ */
 int lbg_check_state_batched_dev(const double* x, size_t d, int64_t batch, double* out3,
                                 void* stream);
+
+/* ------------------------------------------------------------------------
+ * Invariant checks with host buffers (validate.hpp:20-31, validate.cpp:10-45).
+ * lbg_check_state: lb::check_state over `batch` d x d AoS states on the GPU
+ *   (K6); out3 = {max |Tr rho - 1|, max |rho_ij - conj rho_ji|, min Re rho_ii}.
+ * lbg_check_generator: lb::check_generator (validate.cpp:32-45): the states
+ *   rho_t = lb::random_density(lb::make_rng(42), dim), t < trials, drawn in
+ *   sequence as the reference does; *passed = 1 iff |Tr unvec(L vec(rho_t))|
+ *   <= tol for all t (trace sums on the GPU); *worst (optional) = the largest
+ *   |Tr|. L: rows x cols AoS; rows or cols != dim^2 -> LBG_EINVAL.
+ * lbg_random_density_batch: lb::random_density drawn `count` times from
+ *   lb::make_rng(seed) (random.hpp:12-37), count x d x d AoS.
+ * lbg_validate_last_error(): message of the last failed call of this group.
+ * ------------------------------------------------------------------------ */
+const char* lbg_validate_last_error(void);
+int lbg_check_state(const double* rho, size_t d, int64_t batch, double* out3);
+int lbg_check_generator(size_t dim, const double* l, size_t rows, size_t cols, size_t trials, double tol,
+                        int* passed, double* worst);
+int lbg_random_density_batch(uint64_t seed, size_t d, int64_t count, double* out);
 
 /* ------------------------------------------------------------------------
  * Ensemble reduction across ranks (config 4): in-place sum of `count` doubles

@@ -172,6 +172,8 @@ class Reference:
         L.ref_evolve_batch.argtypes = [_dp, sz, _dp, C.c_int64, sz, _dp, C.c_int, _dp]
         L.ref_sweep_batch.argtypes = [_dp, _dp, C.c_int64, sz, _dp, _dp, C.c_int, _dp]
         L.ref_check_state.argtypes = [_dp, sz, C.c_double, _dp, _dp, _dp]
+        L.ref_check_generator.argtypes = [sz, _dp, sz, sz, sz, C.c_double, C.POINTER(C.c_int)]
+        L.ref_random_density.argtypes = [C.c_uint64, sz, C.c_int64, _dp]
 
     def _rc(self, rc, what):
         if rc == 1:
@@ -267,6 +269,20 @@ class Reference:
         te, he, md = C.c_double(), C.c_double(), C.c_double()
         rc = self.lib.ref_check_state(_ptr(rho), rho.shape[0], tol, C.byref(te), C.byref(he), C.byref(md))
         return rc == 0, te.value, he.value, md.value
+
+    def check_generator(self, l, dim, trials, tol=1e-10):
+        """lb::check_generator (validate.cpp:32-45) on the generator matrix l."""
+        l = np.ascontiguousarray(l, np.complex128)
+        ok = C.c_int()
+        self._rc(self.lib.ref_check_generator(dim, _ptr(l), l.shape[0], l.shape[1], trials, tol, C.byref(ok)),
+                 "check_generator")
+        return bool(ok.value)
+
+    def random_density(self, seed, d, count):
+        """count states lb::random_density(make_rng(seed), d), drawn in sequence."""
+        out = np.zeros((count, d, d), np.complex128)
+        self._rc(self.lib.ref_random_density(seed, d, count, _ptr(out)), "random_density")
+        return out
 
     def sweep_batch(self, deltas, scales, steps=500, threads=1):
         """Config 4 through the reference. Returns (pops (B,9), ens_sum (9,9), seconds)."""

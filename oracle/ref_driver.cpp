@@ -335,6 +335,27 @@ int ref_check_state(const double* rho, std::size_t d, double tol, double* trace_
     });
 }
 
+// lb::check_generator (validate.cpp:32-45) on a caller-given generator matrix
+int ref_check_generator(std::size_t dim, const double* l, std::size_t rows, std::size_t cols, std::size_t trials,
+                        double tol, int* passed) {
+  return guarded([&] {
+    lb::Lindbladian g{dim, from_buf(l, rows, cols)};
+    *passed = lb::check_generator(g, trials, tol) ? 1 : 0;
+  });
+}
+
+// lb::random_density drawn `count` times from lb::make_rng(seed) (random.hpp:12-37):
+// the state sequence lb::check_generator uses
+int ref_random_density(std::uint64_t seed, std::size_t d, std::int64_t count, double* out) {
+  return guarded([&] {
+    auto rng = lb::make_rng(seed);
+    for (std::int64_t t = 0; t < count; ++t) {
+      const lb::MatrixAoS r = lb::random_density(rng, d);
+      std::memcpy(out + std::size_t(t) * d * d * 2, r.data.data(), d * d * sizeof(lb::cplx));
+    }
+  });
+}
+
 // The benchmark harness's inputs exactly as lb::run_bench draws them
 // (bench.cpp:81-86): lb::make_rng + lb::random_matrix, P scaled by 1/d^2.
 int ref_bench_inputs(std::size_t dim, std::uint64_t seed, double* p, double* v0) {

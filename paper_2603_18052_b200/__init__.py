@@ -10,7 +10,8 @@ reference's operator interface for the hot path (lindbench, /root/reference):
     evolve(p, rho0, n_steps)         lb::evolve             (propagate.cpp:75-109)  -> GPU K1/K2
     evolve_batch(p, rho0s, n_steps)  batched evolve over trajectories               -> GPU K1/K2
     evolve_sweep_dev(...)            per-trajectory build+expm+steps (config 4)     -> GPU K3-K5
-    check_state(rho)                 lb::check_state        (validate.cpp:10-30)
+    check_state(rho)                 lb::check_state        (validate.cpp:10-30)      -> GPU K6
+    check_generator(l, dim, trials)  lb::check_generator    (validate.cpp:32-45)      -> GPU
 
 Errors map like the reference: ValueError <- std::invalid_argument,
 RuntimeError <- std::runtime_error. There is no CPU fallback: if the
@@ -30,7 +31,8 @@ __all__ = [
     "lib", "LbgError", "ALGO", "config_dims", "config_model", "config_sweep_terms",
     "ginibre_batch", "sweep_params", "build_lindbladian", "expm", "step_soa", "step_aos",
     "evolve", "evolve_batch", "evolve_batch_dev", "evolve_workspace", "evolve_sweep_dev",
-    "sweep_workspace", "check_state", "check_state_batched_dev", "launch_count",
+    "sweep_workspace", "check_state", "check_state_batch", "check_generator", "random_density_batch",
+    "check_state_batched_dev", "launch_count",
     "reset_launch_count", "SEED",
 ]
 
@@ -305,17 +307,62 @@ def grape_chain(h0, hc, amplitudes, steps_per_segment: int, dt: float, dissipato
                      steps_per_segment=int(steps_per_segment), points_per_s=1000.0 / (bm + cm))
 
 
+def _vcheck(rc: int, what: str) -> None:
+    if rc == 0:
+        return
+    L = lib()
+    L.lbg_validate_last_error.restype = C.c_char_p
+    msg = f"{what}: {L.lbg_validate_last_error().decode()}"
+    if rc == 1:
+        raise ValueError(msg)
+    if rc == 2:
+        raise RuntimeError(msg)
+    raise LbgError(msg)
+
+
+def check_state_batch(rho) -> tuple[float, float, float]:
+    """lb::check_state (validate.cpp:10-30) over a batch (B, d, d) on the GPU (K6):
+    (max |Tr rho - 1|, max |rho_ij - conj rho_ji|, min Re rho_ii)."""
+    rho = _c128(rho)
+    if rho.ndim != 3 or rho.shape[1] != rho.shape[2]:
+        raise ValueError("check_state: states must be (B, d, d)")
+    out = np.zeros(3)
+    L = lib()
+    L.lbg_check_state.argtypes = [_dp, _sz, C.c_int64, _dp]
+    _vcheck(L.lbg_check_state(_p(rho), rho.shape[1], rho.shape[0], _p(out)), "check_state")
+    return float(out[0]), float(out[1]), float(out[2])
+
+
 def check_state(rho, tol: float = 1e-8) -> dict:
-    """validate.cpp:10-30 on the host (a d x d density matrix)."""
+    """lb::check_state (validate.cpp:10-30) for one d x d density matrix, on the GPU (K6)."""
     rho = _c128(rho)
     if rho.ndim != 2 or rho.shape[0] != rho.shape[1]:
         raise ValueError("check_state: state must be square")
-    tr = np.trace(rho)
-    herm = float(np.abs(rho - rho.conj().T).max()) if rho.size else 0.0
-    mind = float(np.real(np.diag(rho)).min()) if rho.size else 0.0
-    te = float(abs(tr - 1.0))
+    te, herm, mind = check_state_batch(rho[None])
     return dict(trace_error=te, hermiticity_error=herm, min_diagonal=mind,
                 passed=te <= tol and herm <= tol and mind >= -tol)
+
+
+def check_generator(l, dim: int, trials: int, tol: float = 1e-10) -> tuple[bool, float]:
+    """lb::check_generator (validate.cpp:32-45): trace annihilation of the generator
+    l (dim^2 x dim^2) on lb::random_density states from the reference's fixed seed;
+    the traces are summed on the GPU. Returns (passed, worst |Tr|)."""
+    l = _c128(np.atleast_2d(l))
+    ok, worst = C.c_int(), C.c_double()
+    L = lib()
+    L.lbg_check_generator.argtypes = [_sz, _dp, _sz, _sz, _sz, C.c_double, C.POINTER(C.c_int), _dp]
+    _vcheck(L.lbg_check_generator(dim, _p(l), l.shape[0], l.shape[1], trials, tol, C.byref(ok), C.byref(worst)),
+            "check_generator")
+    return bool(ok.value), worst.value
+
+
+def random_density_batch(seed: int, d: int, count: int):
+    """lb::random_density drawn count times from lb::make_rng(seed) (random.hpp:12-37)."""
+    out = np.zeros((count, d, d), np.complex128)
+    L = lib()
+    L.lbg_random_density_batch.argtypes = [C.c_uint64, _sz, C.c_int64, _dp]
+    _vcheck(L.lbg_random_density_batch(seed, d, count, _p(out)), "random_density_batch")
+    return out
 
 
 # -------------------------------------------------- device (stream-ordered) ---

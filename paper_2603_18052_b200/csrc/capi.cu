@@ -60,50 +60,6 @@ struct DevBuf {
   }
 };
 
-// Device buffers and streams reused across lbg_evolve_shared_p calls (grown
-// on demand), so the end-to-end call pays no cudaMalloc/cudaFree per call.
-struct Grow {
-  void* ptr = nullptr;
-  size_t cap = 0;
-  void ensure(size_t bytes) {
-    if (bytes <= cap) return;
-    if (ptr) check_cuda(cudaFree(ptr), "cudaFree");
-    ptr = nullptr;
-    check_cuda(cudaMalloc(&ptr, bytes), "cudaMalloc");
-    cap = bytes;
-  }
-};
-constexpr int kMaxChunks = 16;
-struct EvolvePool {
-  std::mutex mu;
-  Grow p, x, chk, w[2];
-  cudaStream_t st[4] = {nullptr, nullptr, nullptr, nullptr};  // H2D, compute x2, D2H
-  cudaEvent_t ev_h[kMaxChunks] = {}, ev_c[kMaxChunks] = {};
-  void ensure(size_t pb, size_t xb, size_t cb, size_t wb) {
-    if (!st[0]) {
-      for (auto& s : st) check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
-      for (int i = 0; i < kMaxChunks; ++i) {
-        check_cuda(cudaEventCreateWithFlags(&ev_h[i], cudaEventDisableTiming), "event");
-        check_cuda(cudaEventCreateWithFlags(&ev_c[i], cudaEventDisableTiming), "event");
-      }
-    }
-    p.ensure(pb);
-    x.ensure(xb);
-    chk.ensure(cb);
-    w[0].ensure(wb);
-    w[1].ensure(wb);
-  }
-};
-EvolvePool& evolve_pool() {  // one per device (buffers and streams belong to it)
-  static std::mutex mu;
-  static std::map<int, EvolvePool*>* pools = new std::map<int, EvolvePool*>;  // leaked: outlives CUDA teardown
-  const int dev = current_device();
-  std::lock_guard<std::mutex> lk(mu);
-  EvolvePool*& p = (*pools)[dev];
-  if (!p) p = new EvolvePool;
-  return *p;
-}
-
 // reference is_hermitian (lindblad.cpp:13-20): relative 1e-12 on max |h|
 bool is_hermitian(const double* h, size_t d) {
   double worst = 0.0, scale = 0.0;
@@ -383,80 +339,6 @@ int lbg_evolve_shared_p_aos_dev(const double* p, size_t n, double* x, int64_t ba
 }  // extern "C"
 
 namespace {
-// Host-buffer evolve shared by lbg_evolve_shared_p and lbg_evolve_density.
-// Three-stage pipeline over chunks of the batch: H2D on one stream, validation
-// + steps on two compute streams (alternating chunks, so one chunk's kernel
-// tail overlaps the next chunk's start), D2H on a fourth, chained by events —
-// the copy engines run both directions underneath the compute and only the
-// first chunk's H2D and the last chunk's D2H are exposed. `single` forces one
-// chunk (the cooperative tiled kernel).
-template <class WorkBytes, class Step>
-void host_evolve_impl(const double* p, size_t d, const double* rho0, int64_t batch, double* out, bool single,
-                      WorkBytes work_bytes, Step step) {
-  if (d == 0) throw invalid_argument("evolve: state dimension must be positive");
-  if (batch < 0) throw invalid_argument("evolve: negative batch or steps");
-  if (batch == 0) return;
-  const size_t n = d * d;
-  const int64_t min_chunk = 32768;
-  // measured at c1 (ms per call), equal chunks: 4 -> 21.1, 8 -> 20.4, 16 -> 21.6-27 (+ outliers); one
-  // compute stream instead of two: 21.2 at 8 (kernel tails no longer overlap). Chunk sizes ramp
-  // 1, 2, 4, ..., 4, 2, 1 (10 chunks) so only a small first H2D and a small last D2H are exposed:
-  // 20.19 vs 20.48 ms for 8 equal chunks in the same run (1, 2, 4, 8 ramp over 12: no better).
-  constexpr int64_t max_chunks = 10;
-  static_assert(max_chunks <= kMaxChunks, "events per chunk");
-  const int nchunks = (single || batch < 2 * min_chunk) ? 1 : int(std::min<int64_t>(max_chunks, batch / min_chunk));
-  int64_t bounds[kMaxChunks + 1];
-  {
-    int64_t wsum = 0, wts[kMaxChunks];
-    for (int c = 0; c < nchunks; ++c) {
-      wts[c] = int64_t(1) << std::min(std::min(c, nchunks - 1 - c), 2);
-      wsum += wts[c];
-    }
-    int64_t acc = 0;
-    bounds[0] = 0;
-    for (int c = 0; c < nchunks; ++c) {
-      acc += wts[c];
-      bounds[c + 1] = batch * acc / wsum;
-    }
-  }
-  int64_t chunk = 0;
-  for (int c = 0; c < nchunks; ++c) chunk = std::max(chunk, bounds[c + 1] - bounds[c]);
-  EvolvePool& pool = evolve_pool();
-  std::lock_guard<std::mutex> lk(pool.mu);
-  pool.ensure(n * n * 16, size_t(batch) * n * 16, size_t(nchunks) * 3 * 8, work_bytes(chunk));
-  double* dp = static_cast<double*>(pool.p.ptr);
-  double* dx = static_cast<double*>(pool.x.ptr);
-  double* dchk = static_cast<double*>(pool.chk.ptr);
-  cudaStream_t sh = pool.st[0], sd = pool.st[3];
-  check_cuda(cudaMemcpyAsync(dp, p, n * n * 16, cudaMemcpyHostToDevice, sh), "H2D P");
-  int used = 0;
-  for (int c = 0; c < nchunks; ++c) {
-    const int64_t b0 = bounds[c], nb = bounds[c + 1] - bounds[c];
-    if (nb <= 0) break;
-    double* xc = dx + size_t(b0) * n * 2;
-    const size_t bytes = size_t(nb) * n * 16;
-    check_cuda(cudaMemcpyAsync(xc, rho0 + size_t(b0) * n * 2, bytes, cudaMemcpyHostToDevice, sh), "H2D rho0");
-    check_cuda(cudaEventRecord(pool.ev_h[c], sh), "event");
-    cudaStream_t sc = pool.st[1 + (c & 1)];
-    check_cuda(cudaStreamWaitEvent(sc, pool.ev_h[c], 0), "wait");
-    // propagate.cpp:79 — every rho0 must pass check_state at 1e-8
-    launch_check_state(xc, d, nb, dchk + 3 * c, sc);
-    step(dp, xc, nb, pool.w[c & 1].ptr, sc);
-    check_cuda(cudaEventRecord(pool.ev_c[c], sc), "event");
-    check_cuda(cudaStreamWaitEvent(sd, pool.ev_c[c], 0), "wait");
-    check_cuda(cudaMemcpyAsync(out + size_t(b0) * n * 2, xc, bytes, cudaMemcpyDeviceToHost, sd), "D2H rho");
-    used = c + 1;
-  }
-  std::vector<double> chk(size_t(used) * 3);
-  check_cuda(cudaMemcpyAsync(chk.data(), dchk, chk.size() * 8, cudaMemcpyDeviceToHost, sd), "D2H");
-  check_cuda(cudaStreamSynchronize(sd), "sync");
-  for (int c = 0; c < used; ++c)
-    if (!(chk[3 * c] <= 1e-8 && chk[3 * c + 1] <= 1e-8 && chk[3 * c + 2] >= -1e-8))
-      throw invalid_argument("evolve: initial state fails physical-state checks");
-}
-}  // namespace
-
-namespace {
 // 1-norm (max column sum) of a d x d complex matrix (interleaved doubles)
 double norm1(const double* a, size_t d) {
   double best = 0.0;
@@ -528,12 +410,12 @@ int lbg_evolve_shared_p(const double* p, size_t d, const double* rho0, int64_t b
   return guarded([&] {
     if (steps < 0) throw invalid_argument("evolve: negative batch or steps");
     const size_t n = d * d;
+    // the cooperative tile engine needs the whole device: one chunk, one stream
     const bool single = d > 0 && batch > 0 && choose_algo(n, batch, algo) == LBG_ALGO_TILED;
-    host_evolve_impl(p, d, rho0, batch, out, single,
-                     [&](int64_t chunk) { return lbg_evolve_workspace(n, chunk, algo); },
-                     [&](const double* dp, double* xc, int64_t nb, void* w, cudaStream_t s) {
-                       evolve_dev(dp, n, nullptr, nullptr, xc, nb, steps, algo, w, s, Layout::aos);
-                     });
+    host_evolve(p, d, rho0, batch, out, single, [&](int64_t chunk) { return lbg_evolve_workspace(n, chunk, algo); },
+                [&](const double* dp, double* xc, int64_t nb, void* w, cudaStream_t s) {
+                  evolve_dev(dp, n, nullptr, nullptr, xc, nb, steps, algo, w, s, Layout::aos);
+                });
   });
 }
 
@@ -541,12 +423,12 @@ int lbg_evolve_density(const double* p, size_t d, const double* rho0, int64_t ba
                        double* out) {
   return guarded([&] {
     if (steps < 0) throw invalid_argument("evolve: negative batch or steps");
-    if (d > 0 && !density_supported(d * d)) throw invalid_argument("density mode supports d*d <= 84");
-    host_evolve_impl(p, d, rho0, batch, out, false,
-                     [&](int64_t chunk) { return density_workspace(d * d, chunk); },
-                     [&](const double* dp, double* xc, int64_t nb, void* w, cudaStream_t s) {
-                       launch_density(dp, d, xc, nb, steps, kDensityAuto, w, s);
-                     });
+    // beyond n = 84 the real tile engine (cooperative, the whole device) steps: one chunk, one stream
+    const bool single = d > 0 && density_uses_tile_engine(d * d);
+    host_evolve(p, d, rho0, batch, out, single, [&](int64_t chunk) { return density_workspace(d * d, chunk); },
+                [&](const double* dp, double* xc, int64_t nb, void* w, cudaStream_t s) {
+                  launch_density(dp, d, xc, nb, steps, kDensityAuto, w, s);
+                });
   });
 }
 

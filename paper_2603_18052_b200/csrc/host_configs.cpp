@@ -11,6 +11,7 @@
 #include <complex>
 #include <cstdint>
 #include <cstring>
+#include <random>
 #include <thread>
 #include <vector>
 
@@ -240,6 +241,34 @@ int lbg_ginibre_batch(uint64_t seed, uint32_t cfg, uint64_t first, int64_t count
   parallel(count, threads, [&](int64_t lo, int64_t hi) {
     for (int64_t b = lo; b < hi; ++b) ginibre(seed, cfg, first + uint64_t(b), d, out + 2 * d * d * size_t(b));
   });
+  return LBG_OK;
+}
+
+// lb::random_density (random.hpp:31-37) drawn `count` times in sequence from
+// lb::make_rng(seed) (random.hpp:12-14): G with std::uniform_real_distribution
+// (-1, 1) re / im per element in row-major order (random.hpp:17-21), rho =
+// G G^dag (i-k-j matmul), then (1 / tr) * rho in complex arithmetic.
+int lbg_random_density_batch(uint64_t seed, size_t d, int64_t count, double* out) {
+  if (d == 0 || count < 0 || (count && !out)) return LBG_EINVAL;
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> u(-1.0, 1.0);
+  for (int64_t t = 0; t < count; ++t) {
+    Mat g(d * d);
+    for (auto& z : g) {
+      const double re = u(rng);
+      const double im = u(rng);
+      z = cplx{re, im};
+    }
+    const Mat rho = matmul(g, dagger(g, d), d);
+    cplx tr{0.0, 0.0};
+    for (size_t i = 0; i < d; ++i) tr += rho[i * d + i];
+    const cplx inv = cplx{1.0, 0.0} / tr;
+    for (size_t e = 0; e < d * d; ++e) {
+      const cplx z = inv * rho[e];
+      out[(size_t(t) * d * d + e) * 2] = z.real();
+      out[(size_t(t) * d * d + e) * 2 + 1] = z.imag();
+    }
+  }
   return LBG_OK;
 }
 

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstddef>
+#include <functional>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -86,6 +87,7 @@ void evolve_dev_aos(const double* p, std::size_t n, double* x_aos, int64_t batch
                     cudaStream_t s);
 // density-matrix mode: shared P applied to the real coordinates (k_density.cu)
 bool density_supported(std::size_t n);
+bool density_uses_tile_engine(std::size_t n);  // n > 84: the cooperative real K1c
 std::size_t density_workspace(std::size_t n, int64_t batch);
 constexpr int kDensityHermitian = 0, kDensityGeneral = 1, kDensityAuto = 2;  // LBG_DENSITY_*
 void launch_density(const double* p, std::size_t d, double* rho, int64_t batch, int64_t steps,
@@ -159,6 +161,13 @@ void launch_ptm_sweep_small(std::size_t d, const double* h0, const double* hd, c
                             std::size_t n_ops, const double* ops, const double* delta, const double* scale,
                             double dt, const double* rho0, int64_t batch, int64_t steps, double* pops,
                             double* ens_sum, void* work, cudaStream_t s);
+
+// end-to-end host-buffer evolve (host_pipeline.cu): chunked H2D / validation /
+// steps / D2H pipeline; `step` runs one chunk on a compute stream
+using ChunkWork = std::function<std::size_t(int64_t chunk)>;
+using ChunkStep = std::function<void(const double* p_dev, double* x_dev, int64_t nb, void* work, cudaStream_t s)>;
+void host_evolve(const double* p, std::size_t d, const double* rho0, int64_t batch, double* out, bool single,
+                 const ChunkWork& work_bytes, const ChunkStep& step);
 
 int sm_count();       // of the current device
 int current_device();

@@ -181,7 +181,10 @@ SlotPool& pool() {  // per device: events and the constant bank belong to one de
 // ---- K1b-R: n <= 84, real DMMA, P_R in shared memory ---------------------------
 // 8 warps = 4 n-tiles x 2 row halves. The SMSP of warp w is w % 4, so each SMSP
 // runs both halves of one n-tile: every SMSP issues exactly mt x kt DMMAs per
-// step (n = 81: 11 m-tiles -> 6 + 5), no SMSP waits on a heavier one.
+// step, no SMSP waits on a heavier one. Generic n (N == 0 instances): mt =
+// ceil(n / 8) m-tiles split 6 + 5 at 11. n = 81 (the FRINGE specialisation):
+// 10 DMMA m-tiles (real rows 0..79) split 5 + 5 over 20 k-steps (k < 80); the
+// k = 80 rank-1 term and row 80 run on DFMA.
 constexpr int kVec = 32, kWarpsR = 8;
 struct RGeom {  // P_R: mt*8 rows x sp cols; V: kVec x sv
   int n, mt, kt, sp, sv;
@@ -349,6 +352,7 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 constexpr size_t kDirectMaxN = 84;  // K1a-R / K1b-R up to here, the real K1c tile engine beyond
 
 bool density_supported(size_t n) { return n >= 1; }
+bool density_uses_tile_engine(size_t n) { return n > kDirectMaxN; }
 
 size_t density_workspace(size_t n, int64_t batch) {
   const size_t base = align_up(n * n * 8) + align_up(2 * size_t(batch) * n * 8) + 256;

@@ -1,0 +1,79 @@
+"""The reference's invariant checks on the GPU (validate.cpp:10-45) against the
+reference itself: lb::check_state through K6 with host buffers, and
+lb::check_generator (trace annihilation) with the reference's own state
+sequence (lb::random_density from lb::make_rng(42))."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_check_state_host_contract(lbg, reference):
+    """test_validate.cpp-style cases: valid, trace-broken, non-Hermitian,
+    negative diagonal, and the tolerance edge; GPU == lb::check_state."""
+    cases = [np.diag([0.25, 0.75]).astype(complex), np.eye(2, dtype=complex)]
+    r = np.diag([0.5, 0.5]).astype(complex)
+    r[0, 1] = 3e-8
+    cases.append(r)
+    r = np.diag([1.0 + 2e-8, -2e-8]).astype(complex)
+    cases.append(r)
+    r = np.diag([0.6, 0.4]).astype(complex)
+    r[0, 1], r[1, 0] = 0.1 + 0.2j, 0.1 - 0.2j + 5e-9
+    cases.append(r)
+    for rho in cases:
+        got = lbg.check_state(rho)
+        ok, te, he, md = reference.check_state(rho)
+        assert got["passed"] == ok
+        assert (got["trace_error"], got["hermiticity_error"], got["min_diagonal"]) == (te, he, md)
+    with pytest.raises(ValueError):
+        lbg.check_state(np.zeros((2, 3), complex))
+
+
+def test_check_state_batch_equals_per_state(lbg, reference):
+    rng = np.random.default_rng(5)
+    g = rng.normal(size=(300, 9, 9)) + 1j * rng.normal(size=(300, 9, 9))
+    rho = g @ np.conj(np.swapaxes(g, 1, 2))
+    rho /= np.trace(rho, axis1=1, axis2=2)[:, None, None]
+    rho[17, 2, 3] += 4e-9
+    te, he, md = lbg.check_state_batch(rho)
+    want = [reference.check_state(r)[1:] for r in rho]
+    assert te == max(w[0] for w in want)
+    assert he == max(w[1] for w in want)
+    assert md == min(w[2] for w in want)
+
+
+@pytest.mark.parametrize("cfg", [0, 2, 3])
+def test_check_generator_config_models(lbg, reference, cfg):
+    """Built generators annihilate the trace: same verdict as lb::check_generator,
+    worst |Tr| at unit roundoff (the reference's own bound is 1e-10)."""
+    h, ops = reference.config_model(cfg)
+    d = h.shape[0]
+    L = reference.build_lindbladian(h, ops)
+    ok, worst = lbg.check_generator(L, d, 25)
+    assert ok == reference.check_generator(L, d, 25) is True
+    assert worst <= 1e-12
+    # a tolerance below the achieved bound flips both the same way
+    assert lbg.check_generator(L, d, 25, tol=0.0)[0] == reference.check_generator(L, d, 25, tol=0.0)
+
+
+def test_check_generator_flags_trace_leak(lbg, reference):
+    """test_validate.cpp:98-102: L(0, 0) += 1e-6 leaks trace."""
+    h, ops = reference.config_model(0)
+    L = reference.build_lindbladian(h, ops)
+    L[0, 0] += 1e-6
+    ok, worst = lbg.check_generator(L, 3, 10)
+    assert not ok and not reference.check_generator(L, 3, 10)
+    assert worst > 1e-10
+
+
+def test_check_generator_zero_and_shapes(lbg, reference):
+    """test_validate.cpp:84-86, 104-107: the zero generator passes; a matrix that
+    is not dim^2 x dim^2 is rejected (std::invalid_argument -> ValueError)."""
+    z = np.zeros((4, 4), complex)
+    assert lbg.check_generator(z, 2, 10) == (True, 0.0)
+    assert reference.check_generator(z, 2, 10)
+    with pytest.raises(ValueError, match="dim\\^2"):
+        lbg.check_generator(z, 3, 5)
+    with pytest.raises(ValueError):
+        reference.check_generator(z, 3, 5)
+    assert lbg.check_generator(z, 2, 0) == (True, 0.0)

@@ -86,10 +86,15 @@ def test_python_validation_before_gpu(lbg):
         lbg.evolve(np.eye(4), np.diag([1.0, 0.0]).astype(complex), 1, layout="avx512")
 
 
-def test_check_state_host_contract(lbg):
-    r = lbg.check_state(np.diag([0.25, 0.75]))
-    assert r["passed"]
-    assert not lbg.check_state(np.eye(2))["passed"]
+def test_random_density_sequence_matches_reference_bitwise(lbg):
+    """lbg_random_density_batch reproduces lb::random_density(make_rng(seed), d)
+    drawn in sequence (the states lb::check_generator uses), bit for bit."""
+    from oracle.bindings import Reference
+    ref = Reference()
+    for seed, d, k in ((42, 2, 25), (42, 3, 10), (7, 9, 3)):
+        got = lbg.random_density_batch(seed, d, k)
+        want = ref.random_density(seed, d, k)
+        assert np.array_equal(got.view(np.float64), want.view(np.float64)), (seed, d)
 
 
 def test_kernel_sources_have_no_fallback_paths():
