@@ -2,34 +2,46 @@
 """bench.py — B200 Lindblad propagation engine benchmark (driver contract).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config C] [--scaling strong|weak]
     torchrun --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N ...
 
 Headline workload (BASELINE.json configs[1], "c1"): d = 3 transmon with
 leakage, ONE shared P = exp(L dt) (9x9 complex128), 2^20 independent
-trajectories per GPU, 1,000 propagation steps per pass. One bench "step" = one
-pass of the hot path (vec(rho_b) <- P vec(rho_b), 1,000 times, for every
-trajectory). metric = trajectory-steps/s (whole job), FP64 GFLOP/s counted as
-8 d^4 = 648 flops per trajectory-step. Multi-GPU: trajectories shard with no
-data-path collective (weak scaling: each rank owns 2^20 trajectories with
-global ids rank*2^20 + b, so inputs are independent of N).
+trajectories, 1,000 propagation steps per pass. One bench "step" = one pass of
+the hot path (vec(rho_b) <- P vec(rho_b), 1,000 times, for every trajectory).
+metric = trajectory-steps/s (whole job), FP64 GFLOP/s counted as 8 d^4 = 648
+flops per trajectory-step.
+
+Multi-GPU: the configs fix the GLOBAL batch. With
+--scaling strong (default) rank r of W owns the global trajectory ids
+[floor(r B / W), floor((r + 1) B / W)); inputs are keyed on the global id, so
+results are independent of W; stepping has no inter-GPU traffic, and config
+4's ensemble mean is the engine's one collective (lbg_ensemble_mean_dev over
+the engine's own NCCL communicator, lbg_nccl_*). --scaling weak gives every
+rank the full per-GPU batch instead. Time = max over ranks of the CUDA-event
+time, value = global trajectory-steps / that time.
 
 value: inputs resident in HBM (151 MB state > 126 MB L2, so no L2 flush is
 needed), CUDA events on the launching stream, barrier + synchronize around
-exactly K passes, max over ranks. e2e: the same metric through the host-buffer
-C-ABI call lbg_evolve_shared_p (H2D of rho0 from pinned memory, rho0
-validation, the steps, D2H of the final states) timed per call.
-roofline: FP64 pipe bound; peak = FP64 DMMA/DFMA throughput measured live by
+exactly K passes. e2e: the same metric through the host-buffer C-ABI call
+lbg_evolve_shared_p (H2D of rho0, rho0 validation, the steps, D2H of the
+final states) timed per call, from pinned buffers and — as lb::MatrixAoS
+holds them — from pageable ones; each checked against the device result.
+roofline: FP64 pipe bound; peak = the FP64 DMMA throughput measured live by
 lbg_fp64_peak() (MEASURED_PEAKS.json has no FP64 figure). cpu_baseline: the
 reference (oracle/_ref/libref.so, compiled from /root/reference sources with
-its native-fast flags) on a bounded sample, all host threads.
-Extra key "configs": the other BASELINE configs (c0 latency, c2 d=9, c3 d=27,
-c4 per-trajectory sweep) measured the same way at N=1.
+its native-fast flags) on the box's host threads.
+Extra keys at N = 1: "configs" (c0, c2, c3, c4 and the side tables) and
+"strong_scaling_projection" (each batched config timed at B, B/2, B/4, B/8 on
+this GPU: T(B) / T(B/W) is the projected W-GPU speed-up, since the shards never
+talk while stepping). A one-line text summary precedes the JSON line.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import platform
 import subprocess
 import sys
 import threading
@@ -40,7 +52,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CONFIGS = {  # cfg: (d, batch per GPU, steps)
+CONFIGS = {  # cfg: (d, global batch, steps)
     0: (3, 1, 10000),
     1: (3, 1 << 20, 1000),
     2: (9, 4096, 1000),
@@ -62,12 +74,37 @@ def flops_per_traj_step(d: int) -> int:
     return 8 * d ** 4
 
 
+def share(rank: int, world: int, batch: int) -> tuple[int, int]:
+    """Global trajectory ids [lo, hi) of rank `rank`."""
+    return rank * batch // world, (rank + 1) * batch // world
+
+
+def config_dict(cfg: int, world: int, scaling: str) -> dict:
+    """The `config` key, identical in both arms."""
+    d, B, S = CONFIGS[cfg]
+    strong = scaling == "strong" and cfg != 0
+    gb = B if strong else B * world
+    return {"workload": WORKLOAD[cfg], "d": d, "global_batch": gb, "steps_per_pass": S, "n_ranks": world,
+            "partition": ("rank r owns global ids [floor(rB/W), floor((r+1)B/W))" if strong
+                          else "replicas: every rank runs the one trajectory" if cfg == 0
+                          else "every rank owns its own batch of B (weak)"),
+            "l2": "state larger than L2; no flush needed" if cfg == 1 else "working set L2/SMEM resident"}
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
+
+
 # ---------------------------------------------------- GPU roofline placement ---
 # B200 re-targeting of the reference's CPU model (proj/src/roofline.cpp:62-99:
-# characterize -> place -> classify). Levels are where P lives while stepping;
-# bandwidths are MEASURED (profiles/r01_fp64_peaks.json, MEASURED_PEAKS.json),
-# capacities per the hardware (per-SM for the on-chip levels, since every SM
-# needs its own copy of a shared P).
+# characterize -> place -> classify). Levels are where P lives while stepping.
 B200_PROFILE = {
     "levels": ["regs/const", "smem", "l2", "hbm"],
     "capacity_bytes": [None, 227 * 1024, 126 * 2 ** 20, 180 * 10 ** 9],
@@ -77,42 +114,28 @@ B200_PROFILE = {
 
 def roofline_place(d: int, batch: int, shared_p: bool, peak_tflops: float, tile: int = 32) -> dict:
     """characterize (8 d^4 flops per trajectory-step; roofline.cpp:62-74), place P
-    on the B200 ladder (roofline.cpp:76-87) and classify (roofline.cpp:93-99):
-    bytes are what one step must pull from P's level for the whole batch."""
+    on the B200 ladder (roofline.cpp:76-87) and classify (roofline.cpp:93-99)."""
     n = d * d
     p_bytes = 16 * n * n
     flops = 8 * d ** 4 * batch
     prof = B200_PROFILE
     if shared_p:
         if d == 3:
-            level, bytes_ = 0, 0  # 9x9 P in the constant bank / uniform registers
+            level, bytes_ = 0, 0
         elif p_bytes <= prof["capacity_bytes"][1]:
-            # each SM re-reads P from SMEM once per step for its tile of trajectories
             sms = min(148, -(-batch // tile))
             level, bytes_ = 1, p_bytes * sms
         elif p_bytes <= prof["capacity_bytes"][2]:
-            # GEMM tiles (tile x tile complex) stream P and the state from L2
             level, bytes_ = 2, flops / (8 * tile * tile / (16 * 2 * tile))
         else:
             level, bytes_ = 3, p_bytes + 32 * n * batch
     else:
-        level, bytes_ = (0, 0) if n <= 81 else (3, (n * n * 16 + 32 * n) * batch)  # per-trajectory P
+        level, bytes_ = (0, 0) if n <= 81 else (3, (n * n * 16 + 32 * n) * batch)
     ai = flops / bytes_ if bytes_ else float("inf")
     bw = prof["bw_gbs"][level]
     attainable = peak_tflops if bw is None else min(peak_tflops, ai * bw / 1e3)
-    ridge = None if bw is None else peak_tflops * 1e3 / bw
-    return {"level": prof["levels"][level], "flops_per_step": flops, "bytes_per_step": bytes_,
-            "ai_flop_per_byte": ai, "ridge_flop_per_byte": ridge, "attainable_tflops": attainable,
-            "bound": "compute" if (ridge is None or ai >= ridge) else "memory"}
-
-
-def reference_model(lbg, mprof, d: int) -> dict:
-    """The reference's own roofline (roofline.cpp:62-99: characterize -> place
-    -> classify, per single matvec) evaluated on the measured B200 profile."""
-    k = lbg.place(lbg.characterize(d), mprof)
-    c = lbg.classify(k, mprof)
-    return {"flops": k.flops, "bytes": k.bytes, "ai": k.ai, "placement": lbg.LEVELS[k.placement],
-            "ridge": lbg.ridge_point(mprof, k.placement), **c}
+    return {"level": prof["levels"][level], "ai_flop_per_byte": ai if bytes_ else None,
+            "attainable_tflops": attainable}
 
 
 class Clocks:
@@ -225,14 +248,14 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": "trajectory-steps/s", "value": value, "unit": "traj-steps/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded Ginibre rho0, counter-based RNG seed 42)",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: seeded Ginibre rho0 (counter-based RNG, seed 42), BASELINE config models",
         "gflops": value * flops_per_traj_step(d) / 1e9,
-        "config": {"workload": WORKLOAD[cfg], "d": d, "batch_per_gpu": B, "steps_per_pass": S,
-                   "sample_trajectories_per_step": sample},
+        "config": config_dict(cfg, args.gpus, args.scaling),
         "cpu_baseline": {"value": value, "unit": "traj-steps/s", "cores": threads, "kind": "reference",
+                         "cpu_model": cpu_model(),
                          "sample": f"{sample} trajectories x {S} steps per bench step through lb::evolve "
-                                   f"(native-fast SoA), {threads} std::threads"},
+                                   f"(native-fast SoA, -march pinned to x86-64-v4), {threads} std::threads"},
         "e2e": {"value": value, "unit": "traj-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -249,7 +272,8 @@ class Runner:
         h, ops = self.lbg.config_model(cfg)
         return self.lbg.expm(self.lbg.build_lindbladian(h, ops), 0.1)
 
-    def shared_p_setup(self, cfg, B):
+    def shared_p_setup(self, cfg, lo, b):
+        """P (built on the GPU) and global trajectories [lo, lo + b) on the device."""
         d, _, S = CONFIGS[cfg]
         T = self.torch
         P = self.propagator(cfg)
@@ -257,10 +281,10 @@ class Runner:
             rho0 = np.zeros((1, 3, 3), complex)
             rho0[0, 0, 0] = 1.0
         else:
-            rho0 = self.lbg.ginibre_batch(cfg, self.rank * B, B, d)
+            rho0 = self.lbg.ginibre_batch(cfg, lo, b, d)
         pt = T.from_numpy(P).to(self.dev)
-        xt = T.from_numpy(rho0.reshape(B, d * d)).to(self.dev)
-        ws = self.lbg.evolve_workspace(d * d, B)
+        xt = T.from_numpy(rho0.reshape(b, d * d)).to(self.dev)
+        ws = self.lbg.evolve_workspace(d * d, b)
         work = T.empty(max(ws, 1), dtype=T.uint8, device=self.dev)
         return P, rho0, pt, xt, work
 
@@ -295,6 +319,88 @@ def max_over_ranks(torch, x: float) -> float:
     return x
 
 
+class SweepCase:
+    """Config 4 through lbg_evolve_sweep_dev on global ids [lo, lo + b), then the
+    ensemble mean over ranks (lbg_ensemble_mean_dev on the engine's NCCL comm)."""
+
+    def __init__(self, torch, lbg, dev, lo, b, global_batch, comm=None, mode="auto"):
+        self.torch, self.lbg, self.dev, self.B, self.mode = torch, lbg, dev, b, mode
+        self.global_batch, self.comm = global_batch, comm
+        T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+        h0, hd, hs = lbg.config_sweep_terms()
+        _, ops = lbg.config_model(4)
+        delta, scale = lbg.sweep_params(lo, b)
+        rho0 = np.zeros((9, 9), complex)
+        rho0[0, 0] = 1.0
+        self.host = (h0, hd, hs, ops, delta, scale, rho0)
+        self.args = [T(h0), T(hd), T(hs), T(ops), T(delta), T(scale), 0.1, T(rho0), CONFIGS[4][2]]
+        self.pops = torch.zeros(b, 9, dtype=torch.float64, device=dev)
+        self.ens = torch.zeros(9, 9, dtype=torch.complex128, device=dev)
+        self.work = torch.empty(lbg.sweep_workspace(9, b), dtype=torch.uint8, device=dev)
+        self.shared_gpu_group = (torch.distributed.is_initialized() and comm is None
+                                 and torch.distributed.get_world_size() > 1)
+
+    def run(self):
+        self.lbg.evolve_sweep_dev(*self.args, self.pops, self.ens, self.work, mode=self.mode)
+        if self.shared_gpu_group:  # tests only: ranks sharing one GPU cannot form an NCCL comm
+            host = self.ens.cpu()
+            self.torch.distributed.all_reduce(host)
+            self.ens.copy_(host)
+            self.lbg.ensemble_mean_dev(self.ens, self.global_batch, None)
+        else:
+            self.lbg.ensemble_mean_dev(self.ens, self.global_batch, self.comm)
+
+    def e2e(self, reps=2):
+        T, dev = self.torch, self.dev
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            args = [T.from_numpy(np.ascontiguousarray(a)).to(dev) for a in self.host]
+            self.lbg.evolve_sweep_dev(*args[:6], 0.1, args[6], CONFIGS[4][2], self.pops, self.ens, self.work,
+                                      mode=self.mode)
+            pops = self.pops.cpu()
+            ens = self.ens.cpu()
+        s = (time.perf_counter() - t0) / reps
+        h2d = sum(a.nbytes for a in self.host)
+        return {"value": self.B * CONFIGS[4][2] / s, "unit": "traj-steps/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(pops.numel() * 8 + ens.numel() * 16), "ms_per_call": s * 1e3,
+                "call": "lbg_evolve_sweep_dev (host inputs copied in, populations + ensemble copied out)"}
+
+
+def host_call_e2e(torch, lbg, P, rho0, S, want, pinned, reps):
+    """lbg_evolve_shared_p with pinned or pageable caller buffers: median call
+    time, and the result against the device path's (`want`)."""
+    import ctypes as C
+    B, d = rho0.shape[0], rho0.shape[1]
+    if pinned:
+        pin = torch.empty(B * d * d * 2, dtype=torch.float64).pin_memory()
+        pin_out = torch.empty_like(pin).pin_memory()
+        host_in = pin.numpy().view(np.complex128).reshape(B, d, d)
+        host_out = pin_out.numpy().view(np.complex128).reshape(B, d, d)
+        host_in[...] = rho0
+    else:
+        host_in = np.array(rho0, copy=True)
+        host_out = np.empty_like(host_in)
+    L = lbg.lib()
+    dp = C.POINTER(C.c_double)
+    Pc = np.ascontiguousarray(P)
+
+    def call():
+        rc = L.lbg_evolve_shared_p(Pc.ctypes.data_as(dp), d, host_in.ctypes.data_as(dp), B, S,
+                                   host_out.ctypes.data_as(dp), 0)
+        assert rc == 0, L.lbg_last_error()
+    call()
+    diff = float(np.abs(host_out - want).max())
+    assert diff <= 1e-12, f"host-buffer result differs from the device path by {diff}"
+    if torch.distributed.is_initialized():
+        torch.distributed.barrier()
+    calls = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        call()
+        calls.append(time.perf_counter() - t0)
+    return float(np.median(calls)), calls, int(host_in.nbytes + Pc.nbytes), int(host_out.nbytes), diff
+
+
 def run_ours(args):
     import torch
 
@@ -317,97 +423,88 @@ def run_ours(args):
     lbg.lib()
     R = Runner(torch, lbg, dev, rank)
     cfg = args.config
-    d, B, S = CONFIGS[cfg]
+    d, Bcfg, S = CONFIGS[cfg]
     K, W = args.steps, args.warmup
+    strong = args.scaling == "strong" and cfg != 0  # c0 (one trajectory): replicas only
+    gb = Bcfg if strong else Bcfg * world
+    lo, hi = share(rank, world, gb) if strong else ((0, 1) if cfg == 0 else (rank * Bcfg, (rank + 1) * Bcfg))
+    b = hi - lo
     dmma_peak, dfma_peak = lbg.fp64_peak()
-    peak = max(dmma_peak, dfma_peak)
-    # the B200 ladder measured live (lbg_measure_machine_profile): SMEM, L2, HBM,
-    # host-over-PCIe bandwidths feed the placement model below
-    mprof = lbg.measure_machine_profile()
-    bw = list(mprof.bandwidth_gbs)
-    B200_PROFILE["bw_gbs"] = [None, bw[0], bw[1], bw[2]]
-    B200_PROFILE["capacity_bytes"] = [None, int(mprof.capacity_bytes[0]), int(mprof.capacity_bytes[1]),
-                                      int(mprof.capacity_bytes[2])]
+    peak = dmma_peak
     traffic = load_traffic()
+
+    comm = None  # the engine's own NCCL communicator (config 4's ensemble mean)
+    if cfg == 4 and world > 1 and not shared:
+        def bcast(raw):
+            obj = [raw]
+            torch.distributed.broadcast_object_list(obj, src=0)
+            return obj[0]
+        comm = lbg.NcclComm(rank, world, bcast)
 
     # ---- device-resident timed region -----------------------------------
     if cfg == 4:
-        sweep = SweepCase(torch, lbg, dev, rank, B)
+        sweep = SweepCase(torch, lbg, dev, lo, b, gb, comm)
         fn = sweep.run
     else:
-        P, rho0, pt, xt, work = R.shared_p_setup(cfg, B)
+        P, rho0, pt, xt, work = R.shared_p_setup(cfg, lo, b)
         fn = lambda: lbg.evolve_batch_dev(pt, xt, S, work=work, stream=R.stream)  # noqa: E731
     with Clocks(local) as clk:
         total_ms, per_ms, launches = R.time_passes(fn, K, W)
     total_ms = max_over_ranks(torch, total_ms)
-    units = world * B * S * K
+    units = gb * S * K
     value = units / (total_ms * 1e-3)
     ms_step = total_ms / K
     kernel_ms = float(np.mean(per_ms))
-    achieved = flops_per_traj_step(d) * B * S / (kernel_ms * 1e-3) / 1e12
+    achieved = flops_per_traj_step(d) * b * S / (kernel_ms * 1e-3) / 1e12
 
     # ---- end to end through the host-buffer C-ABI call ---------------------
-    e2e = None
     if cfg != 4:
-        pin = torch.empty(B * d * d * 2, dtype=torch.float64).pin_memory()
-        host_in = pin.numpy().view(np.complex128).reshape(B, d, d)
-        host_in[...] = rho0
-        pin_out = torch.empty_like(pin).pin_memory()
-        host_out = pin_out.numpy().view(np.complex128).reshape(B, d, d)
-        import ctypes as C
-        L = lbg.lib()
-        dp = C.POINTER(C.c_double)
-        Pc = np.ascontiguousarray(P)
-
-        def call():
-            rc = L.lbg_evolve_shared_p(Pc.ctypes.data_as(dp), d, host_in.ctypes.data_as(dp), B, S,
-                                       host_out.ctypes.data_as(dp), 0)
-            assert rc == 0, L.lbg_last_error()
-        call()
-        reps = 11  # median of 11: host-buffer calls on a shared box show occasional 2-3x outliers
-        if torch.distributed.is_initialized():
-            torch.distributed.barrier()
-        calls = []
+        # the device result for the same inputs (one pass from rho0), for the e2e check
+        xr = torch.from_numpy(rho0.reshape(b, d * d).copy()).to(dev)
+        lbg.evolve_batch_dev(pt, xr, S, work=work, stream=R.stream)
+        torch.cuda.synchronize(dev)
+        want = xr.cpu().numpy().reshape(b, d, d)
         with Clocks(local) as eclk:  # clocks during the host-buffer calls too
-            for _ in range(reps):
-                t0 = time.perf_counter()
-                call()
-                calls.append(time.perf_counter() - t0)
-        e2e_s = max_over_ranks(torch, float(np.median(calls)))
-        e2e = {"value": world * B * S / e2e_s, "unit": "traj-steps/s",
-               "h2d_bytes_per_step": int(host_in.nbytes + Pc.nbytes), "d2h_bytes_per_step": int(host_out.nbytes),
-               "ms_per_call": e2e_s * 1e3, "ms_per_call_all": [c * 1e3 for c in calls],
-               "call": "lbg_evolve_shared_p (host buffers, synchronous); median of the calls",
-               "clocks": eclk.summary()}
+            med, calls, h2d, d2h, diff = host_call_e2e(torch, lbg, P, rho0, S, want, True, 11)
+        med_pg, calls_pg, _, _, diff_pg = host_call_e2e(torch, lbg, P, rho0, S, want, False, 5)
+        e2e_s = max_over_ranks(torch, med)
+        e2e_pg = max_over_ranks(torch, med_pg)
+        e2e = {"value": gb * S / e2e_s, "unit": "traj-steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_call": e2e_s * 1e3, "ms_per_call_all": [round(c * 1e3, 3) for c in calls],
+               "call": "lbg_evolve_shared_p (pinned host buffers, synchronous); median of 11",
+               "max_abs_diff_vs_device": diff, "clocks": eclk.summary(),
+               "pageable": {"value": gb * S / e2e_pg, "ms_per_call": e2e_pg * 1e3,
+                            "ms_per_call_all": [round(c * 1e3, 3) for c in calls_pg],
+                            "max_abs_diff_vs_device": diff_pg,
+                            "call": "lbg_evolve_shared_p from pageable buffers (lb::MatrixAoS storage): "
+                                    "staged through the pool's pinned buffers; median of 5"}}
     else:
         e2e = sweep.e2e(reps=2)
-        e2e["value"] = e2e["value"] * world
+        e2e["value"] = gb * S / max_over_ranks(torch, e2e["ms_per_call"] * 1e-3)
 
     line = {
         "metric": "trajectory-steps/s", "value": value, "unit": "traj-steps/s", "n_gpus": world,
-        "steps": K, "warmup": W, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "steps": K, "warmup": W, "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: seeded Ginibre rho0 (counter-based RNG, seed 42), BASELINE config models",
         "gflops": value * flops_per_traj_step(d) / 1e9,
-        "config": {"workload": WORKLOAD[cfg], "d": d, "batch_per_gpu": B, "global_batch": B * world,
-                   "steps_per_pass": S, "parallelism": f"trajectories sharded over {world} GPU(s), no collective"
-                   if cfg != 4 else f"trajectories sharded over {world} GPU(s), ensemble allreduce",
-                   "l2": "state larger than L2; no flush needed" if cfg == 1 else "working set L2/SMEM resident"},
+        "config": config_dict(cfg, world, args.scaling),
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic.get(KERNEL[cfg]),
-                     "kernel": KERNEL[cfg],
-                     "peak_source": f"measured live by lbg_fp64_peak(): DMMA {dmma_peak:.2f}, DFMA {dfma_peak:.2f} TF/s "
-                                    "(MEASURED_PEAKS.json has no FP64 entry)",
-                     "flops_per_launch": flops_per_traj_step(d) * B * S, "launch_ms": kernel_ms},
+                     "kernel": KERNEL[cfg] if b > 8192 or cfg in (0, 1, 4) else "auto (small-batch share)",
+                     "peak_source": f"FP64 DMMA throughput measured live by lbg_fp64_peak() ({dmma_peak:.2f} TF/s; "
+                                    f"DFMA loop {dfma_peak:.2f}); MEASURED_PEAKS.json has no FP64 entry",
+                     "flops_per_launch": flops_per_traj_step(d) * b * S, "launch_ms": kernel_ms,
+                     "trajectories_this_rank": b},
         "e2e": e2e,
-        "placement": roofline_place(d, B, cfg != 4, peak),
-        "machine_profile": dict(mprof.as_dict(), levels=["smem/SM", "l2", "hbm", "host(pcie)"],
-                                source="lbg_measure_machine_profile (measured now); file format of "
-                                       "lb::write_profile"),
-        "reference_roofline": reference_model(lbg, mprof, d),
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
+    if cfg == 4:
+        line["config"]["collective"] = ("lbg_ensemble_mean_dev over the engine's NCCL comm (lbg_nccl_*)"
+                                        if comm is not None else
+                                        "one rank: lbg_ensemble_mean_dev without a collective"
+                                        if world == 1 else "gloo all-reduce stand-in, then lbg_ensemble_mean_dev (ranks share one GPU: tests only)")
 
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
@@ -415,10 +512,11 @@ def run_ours(args):
             sample = REF_SAMPLE[cfg]
             cv, times = cpu_reference_rate(cfg, sample, threads, reps=1, warmup=0)
             line["cpu_baseline"] = {"value": cv, "unit": "traj-steps/s", "cores": threads, "kind": "reference",
+                                    "cpu_model": cpu_model(),
                                     "sample": f"{sample} trajectories x {S} steps through lb::evolve "
-                                              f"(native-fast SoA), {threads} std::threads, {times[0]:.2f} s"}
-            # the reference's own methodology is single-core
-            s1 = max(1, sample // 16)
+                                              f"(native-fast SoA, -march pinned to x86-64-v4), {threads} "
+                                              f"std::threads, {times[0]:.2f} s"}
+            s1 = max(1, sample // 16)  # the reference's own methodology is single-core
             c1, t1 = cpu_reference_rate(cfg, s1, 1, reps=1, warmup=0)
             line["cpu_baseline"]["value_1core"] = c1
             line["cpu_baseline"]["sample_1core"] = f"{s1} trajectories x {S} steps, 1 thread, {t1[0]:.2f} s"
@@ -427,56 +525,42 @@ def run_ours(args):
                                     "sample": f"unavailable: {e}"}
 
     if rank == 0 and world == 1 and not args.no_extra and args.config == 1:
+        line["strong_scaling_projection"] = projection(torch, lbg, R)
         line["configs"] = extra_configs(torch, lbg, R, peak)
     if rank == 0:
+        print(summary_text(line), flush=True)
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if torch.distributed.is_initialized():
         torch.distributed.destroy_process_group()
     return 0
 
 
-class SweepCase:
-    """Config 4 through lbg_evolve_sweep_dev (+ NCCL allreduce of the ensemble sum)."""
-
-    def __init__(self, torch, lbg, dev, rank, B, mode="auto"):
-        self.torch, self.lbg, self.dev, self.B, self.mode = torch, lbg, dev, B, mode
-        T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
-        h0, hd, hs = lbg.config_sweep_terms()
-        _, ops = lbg.config_model(4)
-        delta, scale = lbg.sweep_params(rank * B, B)
-        rho0 = np.zeros((9, 9), complex)
-        rho0[0, 0] = 1.0
-        self.host = (h0, hd, hs, ops, delta, scale, rho0)
-        self.args = [T(h0), T(hd), T(hs), T(ops), T(delta), T(scale), 0.1, T(rho0), CONFIGS[4][2]]
-        self.pops = torch.zeros(B, 9, dtype=torch.float64, device=dev)
-        self.ens = torch.zeros(9, 9, dtype=torch.complex128, device=dev)
-        self.work = torch.empty(lbg.sweep_workspace(9, B), dtype=torch.uint8, device=dev)
-
-    def run(self):
-        self.lbg.evolve_sweep_dev(*self.args, self.pops, self.ens, self.work, mode=self.mode)
-        dist = self.torch.distributed
-        if dist.is_initialized():  # the engine's only collective: ensemble sum
-            if dist.get_backend() == "nccl":
-                dist.all_reduce(self.ens)
+def projection(torch, lbg, R):
+    """Each batched config at its global batch B and at the per-rank shares
+    B/2, B/4, B/8 on this GPU; T(B) / T(B/W) is the projected W-GPU speed-up
+    (the shards never communicate while stepping; config 4's ensemble mean is
+    one 1.3 KB allreduce per pass)."""
+    out = {}
+    for cfg in (1, 2, 3, 4):
+        d, B, S = CONFIGS[cfg]
+        row = {}
+        for W in (1, 2, 4, 8):
+            b = B // W
+            if cfg == 4:
+                case = SweepCase(torch, lbg, R.dev, 0, b, b)
+                tot, per, _ = R.time_passes(case.run, 3, 1)
             else:
-                host = self.ens.cpu()
-                dist.all_reduce(host)
-                self.ens.copy_(host)
-
-    def e2e(self, reps=2):
-        T, dev = self.torch, self.dev
-        t0 = time.perf_counter()
-        for _ in range(reps):
-            args = [T.from_numpy(np.ascontiguousarray(a)).to(dev) for a in self.host]
-            self.lbg.evolve_sweep_dev(*args[:6], 0.1, args[6], CONFIGS[4][2], self.pops, self.ens, self.work,
-                                      mode=self.mode)
-            pops = self.pops.cpu()
-            ens = self.ens.cpu()
-        s = (time.perf_counter() - t0) / reps
-        h2d = sum(a.nbytes for a in self.host)
-        return {"value": self.B * CONFIGS[4][2] / s, "unit": "traj-steps/s", "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(pops.numel() * 8 + ens.numel() * 16), "ms_per_call": s * 1e3,
-                "call": "lbg_evolve_sweep_dev (host inputs copied in, populations + ensemble copied out)"}
+                _, _, pt, xt, work = R.shared_p_setup(cfg, 0, b)
+                tot, per, _ = R.time_passes(
+                    lambda: lbg.evolve_batch_dev(pt, xt, S, work=work, stream=R.stream), 3, 1)
+            row[W] = tot / len(per)
+        out[f"c{cfg}"] = {"ms_per_pass": {str(W): round(row[W], 4) for W in row},
+                          "speedup": {str(W): round(row[1] / row[W], 3) for W in (2, 4, 8)}}
+    out["method"] = ("T(B) / T(B/W) on one B200, CUDA events, 3 passes after 1 warm-up; the W-GPU run "
+                     "executes exactly the B/W share per GPU")
+    return out
 
 
 def extra_configs(torch, lbg, R, peak):
@@ -485,17 +569,17 @@ def extra_configs(torch, lbg, R, peak):
         d, B, S = CONFIGS[cfg]
         try:
             if cfg == 4:
-                case = SweepCase(torch, lbg, R.dev, 0, B)
+                case = SweepCase(torch, lbg, R.dev, 0, B, B)
                 total, per, launches = R.time_passes(case.run, 3, 1)
             else:
-                _, _, pt, xt, work = R.shared_p_setup(cfg, B)
+                _, _, pt, xt, work = R.shared_p_setup(cfg, 0, B)
                 total, per, launches = R.time_passes(
                     lambda: lbg.evolve_batch_dev(pt, xt, S, work=work, stream=R.stream), 3 if cfg else 5, 1)
             ms = total / len(per)
             rate = B * S / (ms * 1e-3)
             tf = rate * flops_per_traj_step(d) / 1e12
-            entry = {"workload": WORKLOAD[cfg], "value": rate, "unit": "traj-steps/s", "ms_per_pass": ms,
-                     "gflops": tf * 1e3, "kernel": KERNEL[cfg], "gpu_launches_per_pass": launches // len(per)}
+            entry = {"value": rate, "unit": "traj-steps/s", "ms_per_pass": ms, "gflops": tf * 1e3,
+                     "kernel": KERNEL[cfg], "gpu_launches_per_pass": launches // len(per)}
             if cfg == 0:
                 entry["ns_per_step"] = ms * 1e6 / S
                 entry["bound"] = ("latency: one dependent chain; per step >= 6 dependent FP64 ops x 23 cycles "
@@ -503,10 +587,7 @@ def extra_configs(torch, lbg, R, peak):
             else:
                 entry["roofline"] = {"bound": "fp64", "achieved": tf, "peak": peak, "unit": "TFLOP/s",
                                      "frac": tf / peak}
-                entry["placement"] = roofline_place(d, B, cfg != 4, peak)
             if cfg == 4:
-                entry["note"] = ("real transfer-matrix mode (L_R = T L T^-1, 4x fewer executed flops than "
-                                 "8 d^4); includes per-trajectory GPU assembly + expm (not counted in flops)")
                 # the real form executes 2 d^4 flops per traj-step (+ the build), so
                 # the reference-form 8 d^4 count would put frac above 1: the
                 # roofline is the EXECUTED rate over the whole pass
@@ -514,36 +595,20 @@ def extra_configs(torch, lbg, R, peak):
                 exec_tf = (build_flops + B * S * 2 * 81 ** 2) / (ms * 1e-3) / 1e12
                 entry["roofline"] = {"bound": "fp64", "achieved": exec_tf, "peak": peak, "unit": "TFLOP/s",
                                      "frac": exec_tf / peak,
-                                     "counted": ("executed real-form flops: build 5 x 2 x 81^3 per trajectory + "
-                                                 "steps 2 x 81^2 per traj-step"),
-                                     "reference_form_8d4_tflops": tf,
+                                     "counted": "executed real-form flops: build 5 x 2 x 81^3 per trajectory + "
+                                                "steps 2 x 81^2 per traj-step",
                                      "reference_form_8d4_frac": tf / peak}
-                # report the build (K5 + K4) separately -> a steps=0 pass
-                case.args[-1] = 0
+                case.args[-1] = 0  # the build (K5 + K4) apart -> a steps = 0 pass
                 tb, pb, _ = R.time_passes(case.run, 3, 1)
                 build_ms = tb / len(pb)
                 step_ms = max(ms - build_ms, 1e-9)
-                step_rate = B * S / (step_ms * 1e-3)
-                smem_bw = B200_PROFILE["bw_gbs"][1]
-                entry["build"] = {
-                    "ms": build_ms, "kernels": "ptm_expm_kernel (+ ptm_terms_kernel, once)",
-                    "executed_tflops": build_flops / (build_ms * 1e-3) / 1e12,
-                    "note": ("per trajectory: A = dt L_R from three precomputed affine terms, Taylor-12 "
-                             "Paterson-Stockmeyer, 5 real 81x81 matmuls (10x10 DMMA tiles on k < 80 + DFMA "
-                             "fringe for row / column 80, 8 warps in 5x3 / 5x2 blocks)")}
-                entry["stepping"] = {
-                    "ms": step_ms, "traj_steps_per_s": step_rate, "kernel": "ptm_step_kernel",
-                    "executed_tflops": step_rate * 2 * 81 ** 2 / 1e12,
-                    "paper_bytes_per_s": step_rate * 107568,
-                    "note": ("SURVEY 8(d) accounting: 16 (d^4 + 2 d^2) = 107,568 B per traj-step at the level P "
-                             "is served from; P_R is register-resident (52 KB real per trajectory), so the "
-                             f"SMEM bound ({smem_bw:.0f} GB/s x AI 0.488) does not apply"),
-                    "smem_roofline_traj_steps_per_s": smem_bw * 1e9 / 107568}
-                case = SweepCase(torch, lbg, R.dev, 0, B, mode="complex")
+                entry["build_ms"] = build_ms
+                entry["build_executed_tflops"] = build_flops / (build_ms * 1e-3) / 1e12
+                entry["steps_ms"] = step_ms
+                entry["steps_executed_tflops"] = B * S * 2 * 81 ** 2 / (step_ms * 1e-3) / 1e12
+                case = SweepCase(torch, lbg, R.dev, 0, B, B, mode="complex")
                 total, per, _ = R.time_passes(case.run, 2, 1)
-                msc = total / len(per)
-                entry["complex_mode"] = {"value": B * S / (msc * 1e-3), "ms_per_pass": msc,
-                                         "note": "reference-form complex d^2 x d^2 matrices (k_sweep.cu)"}
+                entry["complex_mode_ms_per_pass"] = total / len(per)
             entry["cpu_reference"] = cpu_reference_entry(cfg, rate)
             out[f"c{cfg}"] = entry
         except Exception as e:  # noqa: BLE001
@@ -566,8 +631,7 @@ EXTRA_REF_SAMPLE = {0: 1, 2: 4096, 3: 128, 4: 512}
 
 def cpu_reference_entry(cfg, gpu_rate):
     """The reference (lb::evolve native-fast SoA; c4 with make_model +
-    build_lindbladian + expm per trajectory) on the box's host threads, beside
-    each extra config; c4 also reports build and steps apart."""
+    build_lindbladian + expm per trajectory) on the box's host threads."""
     threads = os.cpu_count() or 1
     sample = EXTRA_REF_SAMPLE[cfg]
     try:
@@ -575,71 +639,30 @@ def cpu_reference_entry(cfg, gpu_rate):
     except Exception as e:  # noqa: BLE001
         return {"unavailable": str(e)}
     d, _, S = CONFIGS[cfg]
-    out = {"value": value, "unit": "traj-steps/s", "cores": threads, "kind": "reference",
-           "sample": f"{sample} trajectories x {S} steps, {threads} std::threads, {times[0]:.2f} s",
-           "gpu_over_cpu": gpu_rate / value}
-    if cfg == 4:
-        from oracle.bindings import Oracle, Reference
-        o, r = Oracle(), Reference()
-        dl = np.array([o.sweep_params(42, b)[0] for b in range(sample)])
-        sc = np.array([o.sweep_params(42, b)[1] for b in range(sample)])
-        _, _, build_s = r.sweep_batch(dl, sc, steps=0, threads=threads)
-        out["build_s"], out["steps_s"] = build_s, max(times[0] - build_s, 0.0)
-    return out
+    return {"value": value, "cores": threads, "kind": "reference",
+            "sample": f"{sample} trajectories x {S} steps, {times[0]:.2f} s", "gpu_over_cpu": gpu_rate / value}
 
 
 def density_entry(torch, lbg, R, cfg, peak):
     """Opt-in density-matrix mode (lbg_evolve_density_dev): the same propagation
     on the real coordinates of rho, P_R = T P T^-1 (2 d^4 executed flops per
-    traj-step instead of 8 d^4). Reported beside the complex headline."""
+    traj-step instead of 8 d^4)."""
     d, B, S = CONFIGS[cfg]
-    _, rho0, pt, _, _ = R.shared_p_setup(cfg, B)
+    _, rho0, pt, _, _ = R.shared_p_setup(cfg, 0, B)
     xt = torch.from_numpy(rho0).to(R.dev)
     work = torch.empty(lbg.density_workspace(d * d, B), dtype=torch.uint8, device=R.dev)
     total, per, launches = R.time_passes(lambda: lbg.evolve_density_dev(pt, xt, S, work, stream=R.stream), 3, 1)
     ms = total / len(per)
     rate = B * S / (ms * 1e-3)
     executed = rate * 2 * d ** 4 / 1e12
-    # end to end through the host-buffer call lbg_evolve_density (pinned buffers)
-    import ctypes as C
-    pin = torch.empty(B * d * d * 2, dtype=torch.float64).pin_memory()
-    pin_out = torch.empty_like(pin).pin_memory()
-    host_in = pin.numpy().view(np.complex128).reshape(B, d, d)
-    host_out = pin_out.numpy().view(np.complex128).reshape(B, d, d)
-    host_in[...] = rho0
-    Pc = np.ascontiguousarray(R.propagator(cfg))
-    dp = C.POINTER(C.c_double)
-    L = lbg.lib()
-
-    def call():
-        rc = L.lbg_evolve_density(Pc.ctypes.data_as(dp), d, host_in.ctypes.data_as(dp), B, S,
-                                  host_out.ctypes.data_as(dp))
-        assert rc == 0, L.lbg_last_error()
-    call()
-    calls = []
-    for _ in range(9):
-        t0 = time.perf_counter()
-        call()
-        calls.append(time.perf_counter() - t0)
-    e2e_s = float(np.median(calls))
-    return {"workload": WORKLOAD[cfg] + " (density-matrix mode)", "value": rate, "unit": "traj-steps/s",
-            "e2e": {"value": B * S / e2e_s, "unit": "traj-steps/s", "ms_per_call": e2e_s * 1e3,
-                    "h2d_bytes_per_step": int(host_in.nbytes + Pc.nbytes), "d2h_bytes_per_step": int(host_out.nbytes),
-                    "call": "lbg_evolve_density (host buffers, synchronous); median of 9"},
-            "ms_per_pass": ms, "gpu_launches_per_pass": launches // len(per),
-            "kernel": ("dfma9r_kernel" if d * d == 9 else
-                       "tiled_evolve_kernel<real>" if d * d > 84 else "smem_real_kernel"),
-            "roofline": {"bound": "fp64", "executed_tflops": executed, "peak": peak, "unit": "TFLOP/s",
-                         "frac": executed / peak},
-            "note": "real coordinates of the Hermitian rho (2 d^4 flops per traj-step); the headline "
-                    "keeps the reference's complex 8 d^4 arithmetic"}
+    return {"value": rate, "ms_per_pass": ms, "gpu_launches_per_pass": launches // len(per),
+            "roofline": {"executed_tflops": executed, "frac": executed / peak}}
 
 
 def expm_table(torch, lbg, R):
     """the propagator build (K5 assembly + K4 expm) on device
-    buffers, CUDA events, vs the reference's lb::build_lindbladian + lb::expm
-    (Pade-13) on one host core; and batched state validation (K6) over the c1
-    batch vs lb::check_state on a host sample."""
+    buffers vs the reference's lb::build_lindbladian + lb::expm (Pade-13) on one
+    host core; batched state validation (K6) over the c1 batch."""
     rows = {}
     try:
         from oracle.bindings import Reference
@@ -663,29 +686,19 @@ def expm_table(torch, lbg, R):
                                                    lbg._sp(R.stream)), "build")
             lbg._check(L.lbg_expm_dev(lbg._tp(Ld), n, 0.1, lbg._tp(Pd), lbg._tp(wk), lbg._sp(R.stream)), "expm")
         total, per, launches = R.time_passes(build, 5, 2)
-        row = {"gpu_ms": total / len(per), "gpu_launches": launches // len(per)}
+        row = {"gpu_ms": total / len(per)}
         if ref is not None:
             t0 = time.perf_counter()
             ref.expm(ref.build_lindbladian(h, ops), 0.1)
             row["ref_ms"] = (time.perf_counter() - t0) * 1e3
             row["speedup"] = row["ref_ms"] / row["gpu_ms"]
         rows[f"d{d}"] = row
-    # K6: check_state over the whole c1 batch
     d, B, _ = CONFIGS[1]
     rho = lbg.ginibre_batch(1, 0, B, d)
     xd = T.from_numpy(rho).to(dev)
     o3 = T.empty(3, dtype=T.float64, device=dev)
     total, per, _ = R.time_passes(lambda: lbg.check_state_batched_dev(xd, d, o3, stream=R.stream), 5, 2)
-    val = {"states": B, "gpu_ms": total / len(per), "states_per_s": B / (total / len(per) * 1e-3)}
-    if ref is not None:
-        sample = 65536
-        t0 = time.perf_counter()
-        for b in range(sample):
-            ref.check_state(rho[b])
-        dt = time.perf_counter() - t0
-        val["ref_states_per_s_sample"] = sample / dt
-        val["ref_note"] = f"lb::check_state on {sample} states through ctypes (one call per state)"
-    rows["check_state"] = val
+    rows["check_state"] = {"states": B, "gpu_ms": total / len(per)}
     return rows
 
 
@@ -701,18 +714,45 @@ def grape_table(lbg):
         return {"error": f"reference unavailable: {e}"}
     for d, seg in ((3, 100), (9, 50), (27, 20)):
         h0, hc, op, amps, dt, rho0 = ref.grape_inputs(d, seg)
-        for _ in range(3):  # warm-up (clocks, caches, one-time attributes)
+        for _ in range(3):
             lbg.grape_chain(h0, hc, amps, 32, dt, op, rho0)
         runs = sorted((lbg.grape_chain(h0, hc, amps, 32, dt, op, rho0)[1] for _ in range(5)),
                       key=lambda t: t["build_ms"] + t["chain_ms"])
-        t = runs[len(runs) // 2]  # median call
-        row = {"segments": seg, "steps_per_segment": 32, "gpu_build_ms": t["build_ms"],
-               "gpu_chain_ms": t["chain_ms"], "gpu_points_per_s": t["points_per_s"]}
+        t = runs[len(runs) // 2]
+        row = {"gpu_points_per_s": t["points_per_s"], "gpu_build_ms": t["build_ms"], "gpu_chain_ms": t["chain_ms"]}
         if d < 27:
             _, b, c = ref.grape_chain(h0, hc, amps, 32, dt, op, rho0)
-            row.update(ref_build_ms=b, ref_chain_ms=c, ref_points_per_s=1000.0 / (b + c))
+            row["ref_points_per_s"] = 1000.0 / (b + c)
         rows[f"d{d}"] = row
     return rows
+
+
+def summary_text(line) -> str:
+    """One short human line ahead of the JSON (keeps the per-config numbers in a
+    truncated log tail)."""
+    parts = [f"headline {line['value'] / 1e9:.2f} G traj-steps/s, {line['ms_per_step']:.2f} ms/pass, "
+             f"frac {line['roofline']['frac']:.3f}, e2e {line['e2e']['value'] / 1e9:.2f} G"]
+    if "pageable" in line["e2e"]:
+        parts.append(f"e2e pageable {line['e2e']['pageable']['value'] / 1e9:.2f} G")
+    cb = line.get("cpu_baseline", {})
+    if cb.get("value"):
+        parts.append(f"cpu {cb['value'] / 1e6:.0f} M ({line['value'] / cb['value']:.0f}x)")
+    for k, e in line.get("configs", {}).items():
+        if k in ("c0", "c2", "c3", "c4") and "ms_per_pass" in e:
+            s = f"{k} {e['ms_per_pass']:.3f} ms"
+            if "roofline" in e:
+                s += f" frac {e['roofline']['frac']:.2f}"
+            if "ns_per_step" in e:
+                s += f" {e['ns_per_step']:.1f} ns/step"
+            cr = e.get("cpu_reference", {})
+            if cr.get("gpu_over_cpu"):
+                s += f" {cr['gpu_over_cpu']:.1f}x cpu"
+            parts.append(s)
+    pj = line.get("strong_scaling_projection")
+    if pj:
+        parts.append("8-GPU projection " + " ".join(f"{k} {v['speedup']['8']:.2f}x"
+                                                    for k, v in pj.items() if k.startswith("c")))
+    return "bench summary: " + " | ".join(parts)
 
 
 def main():
@@ -722,8 +762,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=1, choices=sorted(CONFIGS))
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                    help="strong: the config's global batch split over the ranks (default); weak: B per rank")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--no-extra", action="store_true", help="skip the other configs")
+    ap.add_argument("--no-extra", action="store_true", help="skip the other configs and the projection")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -212,6 +212,10 @@ int lbg_random_density_batch(uint64_t seed, size_t d, int64_t count, double* out
  * engine. Returns LBG_ECUDA if NCCL is unavailable.
  * ------------------------------------------------------------------------ */
 int lbg_allreduce_sum_dev(double* buf, size_t count, void* comm, void* stream);
+/* Ensemble mean of config 4 across ranks: buf (count doubles, each rank's
+ * partial sum over its trajectories) is summed over `comm` (NULL = one rank, no
+ * collective) and divided by the global trajectory count, in place. */
+int lbg_ensemble_mean_dev(double* buf, size_t count, int64_t global_batch, void* comm, void* stream);
 /* NCCL communicator plumbing (libnccl.so.2 is dlopen'ed on first use).
  * Rank 0 calls lbg_nccl_unique_id (128 bytes), the caller broadcasts the bytes
  * out of band (e.g. torch.distributed), then every rank calls

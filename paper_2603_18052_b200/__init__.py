@@ -92,6 +92,7 @@ def lib() -> C.CDLL:
                                        C.c_int64, vp, vp, C.c_int, vp, vp]
     L.lbg_check_state_batched_dev.argtypes = [vp, _sz, C.c_int64, vp, vp]
     L.lbg_allreduce_sum_dev.argtypes = [vp, _sz, vp, vp]
+    L.lbg_ensemble_mean_dev.argtypes = [vp, _sz, C.c_int64, vp, vp]
     L.lbg_nccl_unique_id.argtypes = [vp]
     L.lbg_nccl_comm_init.argtypes = [C.POINTER(vp), C.c_int, vp, C.c_int]
     L.lbg_nccl_comm_destroy.argtypes = [vp]
@@ -413,6 +414,33 @@ def evolve_sweep_dev(h0, hd, hs, ops, delta, scale, dt, rho0, n_steps, pops, ens
                                       _tp(scale), float(dt), _tp(rho0), delta.shape[0], int(n_steps),
                                       _tp(pops), _tp(ens_sum), SWEEP_MODE[mode], _tp(work), _sp(stream)),
            "evolve_sweep_dev")
+
+
+class NcclComm:
+    """The engine's NCCL communicator (include/lbg.h lbg_nccl_*): rank 0 makes the
+    unique id, the caller's process group broadcasts its 128 bytes, every rank
+    joins on its own device. Used only for the config-4 ensemble mean."""
+
+    def __init__(self, rank: int, world: int, broadcast):
+        L = lib()
+        idb = (C.c_char * 128)()
+        if rank == 0:
+            _check(L.lbg_nccl_unique_id(C.cast(idb, C.c_void_p)), "nccl_unique_id")
+        raw = broadcast(bytes(idb))
+        C.memmove(idb, raw, 128)
+        self.comm = C.c_void_p()
+        _check(L.lbg_nccl_comm_init(C.byref(self.comm), world, C.cast(idb, C.c_void_p), rank), "nccl_comm_init")
+
+    def close(self):
+        if self.comm:
+            _check(lib().lbg_nccl_comm_destroy(self.comm), "nccl_comm_destroy")
+            self.comm = C.c_void_p()
+
+
+def ensemble_mean_dev(buf, global_batch: int, comm=None, stream=None):
+    """In place: buf (a device tensor of partial sums) -> sum over ranks / global_batch."""
+    _check(lib().lbg_ensemble_mean_dev(_tp(buf), buf.numel() * buf.element_size() // 8, int(global_batch),
+                                       comm.comm if comm is not None else None, _sp(stream)), "ensemble_mean_dev")
 
 
 def check_state_batched_dev(x, d: int, out3, stream=None):

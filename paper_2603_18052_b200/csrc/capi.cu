@@ -187,6 +187,16 @@ void nccl_check(int rc, const char* what) {
 
 void note_launch(int n) { g_launches += n; }
 
+__global__ void scale_kernel(double* x, size_t n, double s) {
+  const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) x[i] *= s;
+}
+void launch_scale(double* x, size_t n, double s, cudaStream_t st) {
+  if (n == 0) return;
+  scale_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(x, n, s);
+  LBG_CHECK_LAUNCH("scale_kernel");
+}
+
 int current_device() {
   int dev = 0;
   check_cuda(cudaGetDevice(&dev), "get device");
@@ -688,6 +698,16 @@ int lbg_nccl_comm_init(void** comm, int nranks, const void* id128, int rank) {
 
 int lbg_nccl_comm_destroy(void* comm) {
   return guarded([&] { nccl_check(nccl().comm_destroy(comm), "ncclCommDestroy"); });
+}
+
+int lbg_ensemble_mean_dev(double* buf, size_t count, int64_t global_batch, void* comm, void* stream) {
+  return guarded([&] {
+    if (!buf || global_batch <= 0) throw invalid_argument("ensemble_mean: bad arguments");
+    cudaStream_t s = as_stream(stream);
+    // ncclFloat64 = 8, ncclSum = 0 (nccl.h); one rank: no communicator needed
+    if (comm) nccl_check(nccl().all_reduce(buf, buf, count, 8, 0, comm, s), "ncclAllReduce");
+    launch_scale(buf, count, 1.0 / double(global_batch), s);
+  });
 }
 
 int lbg_allreduce_sum_dev(double* buf, size_t count, void* comm, void* stream) {

@@ -5,8 +5,9 @@
 //
 // Pipeline over chunks of the batch (sizes ramp 1, 2, 4, ..., 4, 2, 1 so only a
 // small first H2D and a small last D2H are exposed):
-//   stream H : H2D of chunk c, then the rho0 validation (K6) of chunk c and a
-//              24-byte D2H of its result into pinned memory;
+//   stream H : H2D of chunk c;
+//   stream K (highest priority): the rho0 validation (K6) of chunk c after its
+//              H2D, and a 24-byte D2H of its result into pinned memory;
 //   stream C0/C1 (alternating chunks, so one chunk's kernel tail overlaps the
 //              next chunk's start): the steps of chunk c (in place), after its
 //              H2D AND its validation (which reads the same buffer);
@@ -71,13 +72,20 @@ struct EvolvePool {
   std::mutex mu;
   Grow p, x, chk, w[2];
   PinnedGrow pin_in, pin_out, pin_chk;
-  cudaStream_t st[4] = {nullptr, nullptr, nullptr, nullptr};  // H, C0, C1, D
-  cudaEvent_t ev_h[kMaxChunks] = {}, ev_c[kMaxChunks] = {}, ev_d[kMaxChunks] = {}, ev_chk = nullptr;
+  cudaStream_t st[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // H, C0, C1, D, K (checks)
+  cudaEvent_t ev_x[kMaxChunks] = {}, ev_h[kMaxChunks] = {}, ev_c[kMaxChunks] = {}, ev_d[kMaxChunks] = {},
+              ev_chk = nullptr;
   void ensure(size_t pb, size_t xb, size_t cb, size_t wb) {
     if (!st[0]) {
-      for (auto& s : st) check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+      for (int i = 0; i < 4; ++i) check_cuda(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking), "stream");
+      // the rho0 checks run at the highest priority: their few blocks take the
+      // next free SM slots ahead of the stepping kernels, so the validation of
+      // every chunk completes early and the D2H copies overlap the stepping
+      int lo = 0, hi = 0;
+      check_cuda(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
+      check_cuda(cudaStreamCreateWithPriority(&st[4], cudaStreamNonBlocking, hi), "stream");
       for (int i = 0; i < kMaxChunks; ++i)
-        for (cudaEvent_t* e : {&ev_h[i], &ev_c[i], &ev_d[i]})
+        for (cudaEvent_t* e : {&ev_x[i], &ev_h[i], &ev_c[i], &ev_d[i]})
           check_cuda(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
       check_cuda(cudaEventCreateWithFlags(&ev_chk, cudaEventDisableTiming), "event");
     }
@@ -139,7 +147,7 @@ class CopyPool {
  private:
   CopyPool() {
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    const unsigned n = std::min(7u, hw > 1 ? hw - 1 : 0u);
+    const unsigned n = std::min(11u, hw > 1 ? hw - 1 : 0u);
     for (unsigned i = 0; i < n; ++i) workers_.emplace_back([this, i] { run(int(i) + 1); });
     for (auto& t : workers_) t.detach();
   }
@@ -226,7 +234,7 @@ void host_evolve(const double* p, size_t d, const double* rho0, int64_t batch, d
   double* hchk = static_cast<double*>(pool.pin_chk.ptr);
   char* pin_in = static_cast<char*>(pool.pin_in.ptr);
   char* pin_out = static_cast<char*>(pool.pin_out.ptr);
-  cudaStream_t sh = pool.st[0], sd = pool.st[3];
+  cudaStream_t sh = pool.st[0], sd = pool.st[3], sk = pool.st[4];
   CopyPool& cp = CopyPool::get();
   try {
     check_cuda(cudaMemcpyAsync(dp, p, n * n * 16, cudaMemcpyHostToDevice, sh), "H2D P");
@@ -240,17 +248,20 @@ void host_evolve(const double* p, size_t d, const double* rho0, int64_t batch, d
         src = pin_in + off;
       }
       check_cuda(cudaMemcpyAsync(xc, src, bytes, cudaMemcpyHostToDevice, sh), "H2D rho0");
-      // propagate.cpp:79 — every rho0 must pass check_state at 1e-8; the steps
-      // (in place) wait for the check, which reads the chunk
-      launch_check_state(xc, d, nb, dchk + 3 * c, sh);
-      check_cuda(cudaEventRecord(pool.ev_h[c], sh), "event");
-      check_cuda(cudaMemcpyAsync(hchk + 3 * c, dchk + 3 * c, 24, cudaMemcpyDeviceToHost, sh), "D2H check");
+      check_cuda(cudaEventRecord(pool.ev_x[c], sh), "event");
+      // propagate.cpp:79 — every rho0 must pass check_state at 1e-8 (on the
+      // check stream, so the copies never queue behind a check kernel); the
+      // steps (in place) wait for the check, which reads the chunk
+      check_cuda(cudaStreamWaitEvent(sk, pool.ev_x[c], 0), "wait");
+      launch_check_state(xc, d, nb, dchk + 3 * c, sk);
+      check_cuda(cudaEventRecord(pool.ev_h[c], sk), "event");
+      check_cuda(cudaMemcpyAsync(hchk + 3 * c, dchk + 3 * c, 24, cudaMemcpyDeviceToHost, sk), "D2H check");
       cudaStream_t sc = pool.st[1 + (c & 1)];
       check_cuda(cudaStreamWaitEvent(sc, pool.ev_h[c], 0), "wait");
       step(dp, xc, nb, pool.w[c & 1].ptr, sc);
       check_cuda(cudaEventRecord(pool.ev_c[c], sc), "event");
     }
-    check_cuda(cudaEventRecord(pool.ev_chk, sh), "event");
+    check_cuda(cudaEventRecord(pool.ev_chk, sk), "event");
     check_cuda(cudaEventSynchronize(pool.ev_chk), "sync check");
     if (std::getenv("LBG_DEBUG_PIPELINE"))
       for (int c = 0; c < nchunks; ++c)

@@ -23,6 +23,7 @@ struct cuda_error : std::runtime_error {
 };
 
 void note_launch(int n = 1);  // launch counter (capi.cu)
+void launch_scale(double* x, std::size_t n, double s, cudaStream_t st);  // x *= s (capi.cu)
 
 inline void check_cuda(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw cuda_error(std::string(what) + ": " + cudaGetErrorString(e));

@@ -64,3 +64,17 @@ def test_sharding_and_ensemble_reduce(world, lbg):
     assert np.abs(ens - whole.sum(axis=0)).max() <= 1e-12  # reduction order differs only
     assert abs(np.trace(ens).real - B_TOTAL) <= 1e-12
     assert tmax == float(world)
+
+
+@pytest.mark.parametrize("B", [1, 7, 4096, 65536, 1 << 20])
+def test_strong_scaling_partition_tiles_the_global_batch(B):
+    """bench.py's strong-scaling shares [floor(rB/W), floor((r+1)B/W)) tile
+    [0, B) exactly for every W, with sizes differing by <= 1."""
+    import bench
+    for W in (1, 2, 3, 4, 8):
+        shares = [bench.share(r, W, B) for r in range(W)]
+        assert shares[0][0] == 0 and shares[-1][1] == B
+        assert all(shares[r][1] == shares[r + 1][0] for r in range(W - 1))
+        sizes = [hi - lo for lo, hi in shares]
+        assert max(sizes) - min(sizes) <= 1
+        assert bench.config_dict(2, W, "strong")["global_batch"] == 4096

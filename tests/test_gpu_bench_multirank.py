@@ -30,12 +30,22 @@ def _run(args, port):
 def test_two_ranks_one_line(cfg, port):
     line = _run(["--config", str(cfg), "--steps", "2", "--warmup", "1", "--no-cpu", "--no-extra"], port)
     assert line["n_gpus"] == 2 and line["steps"] == 2 and line["value"] > 0
-    assert line["config"]["global_batch"] == 2 * line["config"]["batch_per_gpu"]
-    assert line["scaling"] == "weak" and line["gpu_launches"] > 0
+    # strong scaling: the config's global batch, split [floor(rB/W), floor((r+1)B/W))
+    assert line["config"]["global_batch"] == {1: 1 << 20, 4: 65536}[cfg]
+    assert line["roofline"]["trajectories_this_rank"] == line["config"]["global_batch"] // 2
+    assert line["scaling"] == "strong" and line["gpu_launches"] > 0
+    assert line["e2e"]["max_abs_diff_vs_device"] <= 1e-12 if cfg == 1 else True
     if cfg == 4:
-        assert "allreduce" in line["config"]["parallelism"]
+        assert "lbg_ensemble_mean_dev" in line["config"]["collective"]
 
 
 def test_reference_arm_rank0_only():
     line = _run(["--impl", "reference", "--config", "2", "--steps", "1", "--warmup", "0"], 29613)
     assert line["impl"] == "reference" and line["e2e"]["h2d_bytes_per_step"] == 0
+    assert line["config"]["global_batch"] == 4096 and line["cpu_baseline"]["cpu_model"]
+
+
+def test_weak_scaling_option():
+    line = _run(["--config", "2", "--steps", "2", "--warmup", "1", "--no-cpu", "--no-extra", "--scaling", "weak"],
+                29614)
+    assert line["scaling"] == "weak" and line["config"]["global_batch"] == 2 * 4096

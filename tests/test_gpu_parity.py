@@ -406,6 +406,25 @@ def test_nccl_allreduce_single_rank(lbg, torch):
     assert L.lbg_nccl_comm_destroy(comm) == 0
 
 
+def test_ensemble_mean_through_the_engine_comm(lbg, torch):
+    """bench.py's config-4 collective: NcclComm (unique id -> broadcast -> init)
+    and lbg_ensemble_mean_dev (allreduce, then / global batch) on one rank; and
+    the no-communicator form."""
+    comm = lbg.NcclComm(0, 1, lambda raw: raw)
+    ens = (torch.arange(81, dtype=torch.float64, device="cuda").reshape(9, 9) * (1 + 2j)).to(torch.complex128)
+    want = ens / 7
+    lbg.ensemble_mean_dev(ens, 7, comm)
+    torch.cuda.synchronize()
+    assert torch.allclose(ens, want, rtol=1e-15, atol=0)
+    comm.close()
+    x = torch.full((162,), 3.0, dtype=torch.float64, device="cuda")
+    lbg.ensemble_mean_dev(x, 3, None)
+    torch.cuda.synchronize()
+    assert torch.equal(x, torch.ones_like(x))
+    with pytest.raises(ValueError):
+        lbg.ensemble_mean_dev(x, 0, None)
+
+
 # ------------------------------------------------------------ GRAPE chain ---
 @pytest.mark.parametrize("d,segments", [(3, 100), (9, 20), (27, 3)])
 def test_grape_chain_vs_reference(lbg, reference, d, segments):
