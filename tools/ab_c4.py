@@ -14,7 +14,7 @@ out = sys.argv[1]
 passes = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 dev = torch.device("cuda", 0)
 _, B, S = bench.CONFIGS[4]
-case = bench.SweepCase(torch, lbg, dev, 0, B)
+case = bench.SweepCase(torch, lbg, dev, 0, B, B)
 for _ in range(2):
     case.run()
 torch.cuda.synchronize()

@@ -8,6 +8,6 @@ dev = torch.device("cuda", 0)
 R = bench.Runner(torch, lbg, dev, 0)
 B, S = int(sys.argv[1]), int(sys.argv[2])
 algo = sys.argv[3] if len(sys.argv) > 3 else "auto"
-_, _, pt, xt, work = R.shared_p_setup(2, B)
+_, _, pt, xt, work = R.shared_p_setup(2, 0, B)
 lbg.evolve_batch_dev(pt, xt, S, algo=algo, work=work, stream=R.stream)
 torch.cuda.synchronize()

@@ -9,7 +9,7 @@ R = bench.Runner(torch, lbg, dev, 0)
 algo = sys.argv[2] if len(sys.argv) > 2 else "auto"
 res = {}
 for B in [int(b) for b in sys.argv[1].split(",")]:
-    _, _, pt, xt, work = R.shared_p_setup(2, B)
+    _, _, pt, xt, work = R.shared_p_setup(2, 0, B)
     tot, per, _ = R.time_passes(lambda: lbg.evolve_batch_dev(pt, xt, 1000, algo=algo, work=work, stream=R.stream), 3, 1)
     res[B] = tot / len(per)
 print(algo, json.dumps(res))

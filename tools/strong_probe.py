@@ -20,10 +20,10 @@ for cfg in (1, 2, 3, 4):
     for W in (1, 2, 4, 8):
         b = B // W
         if cfg == 4:
-            case = bench.SweepCase(torch, lbg, dev, 0, b)
+            case = bench.SweepCase(torch, lbg, dev, 0, b, b)
             tot, per, _ = R.time_passes(case.run, 3, 1)
         else:
-            _, _, pt, xt, work = R.shared_p_setup(cfg, b)
+            _, _, pt, xt, work = R.shared_p_setup(cfg, 0, b)
             tot, per, _ = R.time_passes(lambda: lbg.evolve_batch_dev(pt, xt, S, algo=algo, work=work,
                                                                      stream=R.stream), 3, 1)
         row[W] = tot / len(per)
