@@ -390,6 +390,7 @@ def host_call_e2e(torch, lbg, P, rho0, S, want, pinned, reps):
         assert rc == 0, L.lbg_last_error()
     call()
     diff = float(np.abs(host_out - want).max())
+    call()  # a second untimed call: the first timed one otherwise absorbs one-off host costs
     assert diff <= 1e-12, f"host-buffer result differs from the device path by {diff}"
     if torch.distributed.is_initialized():
         torch.distributed.barrier()
