@@ -571,6 +571,20 @@ int lbg_evolve_sweep_dev(size_t d, const double* h0, const double* hd, const dou
       throw invalid_argument("sweep: null pointer");
     if (!work) throw invalid_argument("sweep: workspace required");
     cudaStream_t s = as_stream(stream);
+    if (batch == 0) return;
+    {  // propagate.cpp:79-80: lb::evolve validates rho0 before any work (K6, 24-byte D2H)
+      double* dchk = nullptr;
+      check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&dchk), 3 * sizeof(double), s), "malloc check");
+      launch_check_state(rho0, d, 1, dchk, s);
+      double chk[3];
+      const cudaError_t e1 = cudaMemcpyAsync(chk, dchk, sizeof chk, cudaMemcpyDeviceToHost, s);
+      const cudaError_t e2 = cudaFreeAsync(dchk, s);
+      check_cuda(e1, "D2H check");
+      check_cuda(e2, "free check");
+      check_cuda(cudaStreamSynchronize(s), "sync check");
+      if (!(chk[0] <= 1e-8 && chk[1] <= 1e-8 && chk[2] >= -1e-8))
+        throw invalid_argument("evolve: initial state fails physical-state checks");
+    }
     bool real = false;
     if (mode == LBG_SWEEP_REAL || mode == LBG_SWEEP_AUTO) {
       bool herm = false;

@@ -117,8 +117,20 @@ __device__ __forceinline__ unsigned long long okey(double v) {
   return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 __device__ __forceinline__ double ounkey(unsigned long long k) {
+  if (k == 0ull || k == ~0ull) return __longlong_as_double(0x7ff8000000000000ll);  // a NaN that won
   return __longlong_as_double((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k);
 }
+// NaN semantics of lb::check_state (validate.cpp:10-30): a NaN trace error or a
+// NaN minimum diagonal (rho(0,0) NaN: std::min keeps its first operand) fails
+// the state, so in the batch max / min a NaN must WIN (fmax / fmin would drop
+// it); the Hermiticity max drops NaN like std::max does. NaN takes the keys 0
+// and ~0, which no other double maps to.
+__device__ __forceinline__ unsigned long long okey_max(double v) { return isnan(v) ? ~0ull : okey(v); }
+__device__ __forceinline__ unsigned long long okey_min(double v) { return isnan(v) ? 0ull : okey(v); }
+__device__ __forceinline__ double nanmax(double a, double b) { return isnan(a) ? a : (isnan(b) ? b : fmax(a, b)); }
+__device__ __forceinline__ double nanmin(double a, double b) { return isnan(a) ? a : (isnan(b) ? b : fmin(a, b)); }
+// std::min(m, x) = (x < m) ? x : m: a NaN x is dropped, a NaN m is kept
+__device__ __forceinline__ double std_min(double m, double x) { return x < m ? x : m; }
 
 // K6: validate.cpp:10-30 per trajectory, reduced over the batch.
 __global__ void check_state_kernel(const double2* __restrict__ x, int d, long long batch,
@@ -132,7 +144,7 @@ __global__ void check_state_kernel(const double2* __restrict__ x, int d, long lo
     for (int i = 0; i < d; ++i) {
       tre += r[i * d + i].x;
       tim += r[i * d + i].y;
-      mind = fmin(mind, r[i * d + i].x);
+      mind = std_min(mind, r[i * d + i].x);
       for (int j = 0; j < d; ++j) {
         const double2 a = r[i * d + j], c = r[j * d + i];
         herm = fmax(herm, hypot(a.x - c.x, a.y + c.y));
@@ -141,14 +153,14 @@ __global__ void check_state_kernel(const double2* __restrict__ x, int d, long lo
     tr_err = hypot(tre - 1.0, tim);
   }
   for (int o = 16; o > 0; o >>= 1) {
-    tr_err = fmax(tr_err, __shfl_xor_sync(0xffffffffu, tr_err, o));
+    tr_err = nanmax(tr_err, __shfl_xor_sync(0xffffffffu, tr_err, o));
     herm = fmax(herm, __shfl_xor_sync(0xffffffffu, herm, o));
-    mind = fmin(mind, __shfl_xor_sync(0xffffffffu, mind, o));
+    mind = nanmin(mind, __shfl_xor_sync(0xffffffffu, mind, o));
   }
   if ((threadIdx.x & 31) == 0) {
-    atomicMax(&keys[0], okey(tr_err));
+    atomicMax(&keys[0], okey_max(tr_err));
     atomicMax(&keys[1], okey(herm));
-    atomicMin(&keys[2], okey(mind));
+    atomicMin(&keys[2], okey_min(mind));
   }
 }
 
@@ -173,20 +185,20 @@ __global__ void check_state_warp_kernel(const double2* __restrict__ x, int d, lo
       for (int i = 0; i < d; ++i) {
         tre += r[i * d + i].x;
         tim += r[i * d + i].y;
-        mind = fmin(mind, r[i * d + i].x);
+        mind = std_min(mind, r[i * d + i].x);
       }
       tr_err = hypot(tre - 1.0, tim);
     }
   }
   for (int o = 16; o > 0; o >>= 1) {
-    tr_err = fmax(tr_err, __shfl_xor_sync(0xffffffffu, tr_err, o));
+    tr_err = nanmax(tr_err, __shfl_xor_sync(0xffffffffu, tr_err, o));
     herm = fmax(herm, __shfl_xor_sync(0xffffffffu, herm, o));
-    mind = fmin(mind, __shfl_xor_sync(0xffffffffu, mind, o));
+    mind = nanmin(mind, __shfl_xor_sync(0xffffffffu, mind, o));
   }
   if (lane == 0) {
-    atomicMax(&keys[0], okey(tr_err));
+    atomicMax(&keys[0], okey_max(tr_err));
     atomicMax(&keys[1], okey(herm));
-    atomicMin(&keys[2], okey(mind));
+    atomicMin(&keys[2], okey_min(mind));
   }
 }
 

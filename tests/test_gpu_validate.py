@@ -77,3 +77,60 @@ def test_check_generator_zero_and_shapes(lbg, reference):
     with pytest.raises(ValueError):
         reference.check_generator(z, 3, 5)
     assert lbg.check_generator(z, 2, 0) == (True, 0.0)
+
+
+def test_non_finite_inputs_follow_the_reference(lbg, reference):
+    """Non-finite states meet lb::check_state's own semantics (validate.cpp:10-30,
+    std::max / std::min drop a NaN operand): an Inf anywhere, or a NaN on the
+    diagonal (trace), fails it, so lb::evolve throws std::invalid_argument
+    (propagate.cpp:79-80) and so does the engine; a NaN OFF the diagonal passes
+    the reference's check (its hermiticity max ignores NaN) and the engine's K6
+    reproduces that verdict and its three numbers. lb::expm rejects non-finite
+    input (expm.cpp:110-112), as does the engine."""
+    h, ops = lbg.config_model(1)
+    P = lbg.expm(lbg.build_lindbladian(h, ops), 0.1)
+    rho = lbg.ginibre_batch(1, 0, 70000, 3)
+    for pos, bad in (((1, 2), np.inf), ((1, 2), -np.inf), ((1, 1), np.nan), ((0, 0), np.inf), ((1, 2), np.nan)):
+        r = rho.copy()
+        r[69998][pos] = bad
+        ok, te, he, md = reference.check_state(r[69998])
+        got = lbg.check_state(r[69998])
+        assert got["passed"] == ok, (pos, bad)
+        for a, b in ((got["trace_error"], te), (got["hermiticity_error"], he), (got["min_diagonal"], md)):
+            assert a == b or (np.isnan(a) and np.isnan(b)), (pos, bad, a, b)
+        if ok:
+            lbg.evolve_batch(P, r, 3)  # accepted, as lb::evolve accepts it
+        else:
+            with pytest.raises(ValueError, match="physical-state"):
+                lbg.evolve_batch(P, r, 3)
+    L = lbg.build_lindbladian(h, ops)
+    L[3, 4] = np.nan
+    with pytest.raises(ValueError, match="non-finite"):
+        lbg.expm(L, 0.1)
+    with pytest.raises(ValueError):
+        reference.expm(L, 0.1)
+
+
+def test_sweep_validates_rho0_like_evolve(lbg):
+    """lbg_evolve_sweep_dev checks rho0 as lb::evolve does (propagate.cpp:79-80)
+    before building any propagator; an unphysical rho0 raises in every mode."""
+    import torch
+    dev = torch.device("cuda")
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    h0, hd, hs = lbg.config_sweep_terms()
+    _, ops = lbg.config_model(4)
+    delta, scale = lbg.sweep_params(0, 4)
+    pops = torch.zeros(4, 9, dtype=torch.float64, device=dev)
+    ens = torch.zeros(9, 9, dtype=torch.complex128, device=dev)
+    work = torch.empty(lbg.sweep_workspace(9, 4), dtype=torch.uint8, device=dev)
+    for bad in ("trace", "nan"):
+        r0 = np.zeros((9, 9), complex)
+        r0[0, 0] = 1.0
+        if bad == "trace":
+            r0[1, 1] = 0.5
+        else:
+            r0[0, 0] = np.nan
+        for mode in ("auto", "real", "complex"):
+            with pytest.raises(ValueError, match="physical-state"):
+                lbg.evolve_sweep_dev(T(h0), T(hd), T(hs), T(ops), T(delta), T(scale), 0.1, T(r0), 5, pops, ens, work,
+                                     mode=mode)
