@@ -192,3 +192,25 @@ def test_config4_every_trajectory(lbg, torch, c4_reference, mode):
     assert np.abs(got_ens - want_ens).max() <= TOL_RHO * B
     assert abs(np.trace(got_ens).real - B) <= TOL_INV * B
     assert np.abs(got_ens - got_ens.conj().T).max() <= TOL_INV * B
+
+
+@pytest.mark.parametrize("d", [1, 2, 3, 4, 5, 7, 9, 10, 12, 16])
+def test_every_dimension_and_regime_against_the_reference(lbg, reference, d):
+    """Random Lindblad models (random Hermitian H, two random collapse operators,
+    built and exponentiated by the reference) at every d = 1..16 class, batches
+    that select each automatic regime (chain / CTA / K1a / K1b / K1b-C / K1b-K /
+    tiled / rowsplit), through the host-buffer call: every trajectory against
+    lb::evolve."""
+    rng = np.random.default_rng(100 + d)
+    a = rng.normal(size=(d, d)) + 1j * rng.normal(size=(d, d))
+    h = (a + a.conj().T) / (2 * d)
+    ops = (rng.normal(size=(2, d, d)) + 1j * rng.normal(size=(2, d, d))) * 0.05
+    P = reference.expm(reference.build_lindbladian(h, ops), 0.05)
+    for B in (1, 3, 40, 300, 1100):
+        g = rng.normal(size=(B, d, d)) + 1j * rng.normal(size=(B, d, d))
+        rho0 = g @ np.conj(np.swapaxes(g, 1, 2))
+        rho0 /= np.trace(rho0, axis1=1, axis2=2)[:, None, None]
+        want, _ = reference.evolve_batch(P, rho0, 17, threads=THREADS)
+        got = lbg.evolve_batch(P, rho0, 17)
+        err = float(np.abs(got - want).max())
+        assert err <= TOL_RHO, (d, B, err)
