@@ -236,7 +236,17 @@ void host_evolve(const double* p, size_t d, const double* rho0, int64_t batch, d
   char* pin_out = static_cast<char*>(pool.pin_out.ptr);
   cudaStream_t sh = pool.st[0], sd = pool.st[3], sk = pool.st[4];
   CopyPool& cp = CopyPool::get();
+  // LBG_PIPELINE_TIMING (measurement only): device timestamps of each chunk's
+  // H2D end, steps start / end and D2H end, printed relative to the call start
+  static const bool timing = std::getenv("LBG_PIPELINE_TIMING") != nullptr;
+  cudaEvent_t te[4 * kMaxChunks + 1] = {};
+  if (timing)
+    for (auto& e : te) check_cuda(cudaEventCreate(&e), "event");
+  auto mark = [&](int i, cudaStream_t st) {
+    if (timing) check_cuda(cudaEventRecord(te[i], st), "event");
+  };
   try {
+    mark(4 * kMaxChunks, sh);
     check_cuda(cudaMemcpyAsync(dp, p, n * n * 16, cudaMemcpyHostToDevice, sh), "H2D P");
     for (int c = 0; c < nchunks; ++c) {
       const int64_t b0 = bounds[c], nb = bounds[c + 1] - bounds[c];
@@ -248,6 +258,7 @@ void host_evolve(const double* p, size_t d, const double* rho0, int64_t batch, d
         src = pin_in + off;
       }
       check_cuda(cudaMemcpyAsync(xc, src, bytes, cudaMemcpyHostToDevice, sh), "H2D rho0");
+      mark(4 * c, sh);
       check_cuda(cudaEventRecord(pool.ev_x[c], sh), "event");
       // propagate.cpp:79 — every rho0 must pass check_state at 1e-8 (on the
       // check stream, so the copies never queue behind a check kernel); the
@@ -258,7 +269,9 @@ void host_evolve(const double* p, size_t d, const double* rho0, int64_t batch, d
       check_cuda(cudaMemcpyAsync(hchk + 3 * c, dchk + 3 * c, 24, cudaMemcpyDeviceToHost, sk), "D2H check");
       cudaStream_t sc = pool.st[1 + (c & 1)];
       check_cuda(cudaStreamWaitEvent(sc, pool.ev_h[c], 0), "wait");
+      mark(4 * c + 1, sc);
       step(dp, xc, nb, pool.w[c & 1].ptr, sc);
+      mark(4 * c + 2, sc);
       check_cuda(cudaEventRecord(pool.ev_c[c], sc), "event");
     }
     check_cuda(cudaEventRecord(pool.ev_chk, sk), "event");
@@ -281,6 +294,7 @@ void host_evolve(const double* p, size_t d, const double* rho0, int64_t batch, d
       void* dst = out_pinned ? static_cast<void*>(reinterpret_cast<char*>(out) + off) : pin_out + off;
       check_cuda(cudaStreamWaitEvent(sd, pool.ev_c[c], 0), "wait");
       check_cuda(cudaMemcpyAsync(dst, dx + size_t(b0) * n * 2, bytes, cudaMemcpyDeviceToHost, sd), "D2H rho");
+      mark(4 * c + 3, sd);
       check_cuda(cudaEventRecord(pool.ev_d[c], sd), "event");
     }
     if (!out_pinned)
@@ -290,6 +304,14 @@ void host_evolve(const double* p, size_t d, const double* rho0, int64_t batch, d
         cp.copy(reinterpret_cast<char*>(out) + off, pin_out + off, bytes);
       }
     check_cuda(cudaStreamSynchronize(sd), "sync");
+    if (timing) {
+      for (int c = 0; c < nchunks; ++c) {
+        float t[4];
+        for (int k = 0; k < 4; ++k) check_cuda(cudaEventElapsedTime(&t[k], te[4 * kMaxChunks], te[4 * c + k]), "t");
+        std::fprintf(stderr, "chunk %d: h2d end %.3f  steps %.3f-%.3f  d2h end %.3f ms\n", c, t[0], t[1], t[2], t[3]);
+      }
+      for (auto& e : te) cudaEventDestroy(e);
+    }
   } catch (...) {
     pool.drain();
     throw;
