@@ -309,10 +309,6 @@ int64_t cluster_cost(std::size_t n, int64_t batch) {
   const int64_t clusters = (nt + 6) / 7, per_wave = std::max(1, sms / 2);
   return ((clusters + per_wave - 1) / per_wave) * busiest * CKT;
 }
-int64_t smem81_cost(int64_t batch) {
-  const int64_t nt = (batch + 7) / 8;
-  return ((((nt + 3) / 4) + sm_count() - 1) / sm_count()) * 21 * CKT;
-}
 // Is the cluster kernel's critical path shorter than K1b's?
 bool cluster_preferred(std::size_t n, int64_t batch) {
   return n == size_t(CN) && batch > 0 && cluster_cost(n, batch) < smem81_cost(batch);

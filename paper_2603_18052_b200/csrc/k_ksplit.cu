@@ -420,10 +420,13 @@ int ksplit_group(std::size_t n, int64_t batch) {
 bool ksplit_supported(std::size_t n) { return n == size_t(KN); }
 
 // per-step critical path in DMMA issue slots per sub-partition (x 41 k-steps
-// units for K1b / K1b-C): 5 m-tiles x G n-tiles x 21 k-steps (+ the DFMA row)
+// units for K1b / K1b-C): 5 m-tiles x G n-tiles x 21 k-steps (+ the DFMA row),
+// weighted by 4/3: measured, this kernel issues its DMMAs at 67-70% of the pipe
+// at every G (the two-phase step, the exchange, the 3-vs-2 m-tile warps)
+// against K1b's 94%, so equal slot counts are not equal times.
 int64_t ksplit_cost(std::size_t n, int64_t batch) {
   const int g = ksplit_group(n, batch);
-  return g ? int64_t(5) * g * 21 + 2 * g : INT64_MAX;
+  return g ? (int64_t(5) * g * 21 + 2 * g) * 4 / 3 : INT64_MAX;
 }
 
 void launch_ksplit(const double* p_dev, std::size_t n, double* x_re, double* x_im, double* x_aos, int64_t batch,

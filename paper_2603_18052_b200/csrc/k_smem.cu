@@ -14,6 +14,8 @@
 //
 // Replaces step_soa_kernel (proj/src/kernels_variants.cpp:26-41) inside
 // evolve (proj/src/propagate.cpp:85-92), batched over trajectories.
+#include <cstdint>
+
 #include "common.cuh"
 #include "internal.hpp"
 
@@ -154,6 +156,143 @@ __global__ void __launch_bounds__(32 * kWarps, 1)
   }
 }
 
+// K1b at the per-rank shares of config 2 (2,048 / 1,024 trajectories): NT = 2
+// or 1 n-tiles per CTA instead of 4, so 256 / 128 n-tiles still fill 128 SMs.
+// The 12 warps are 12 / NT row groups x NT n-tiles; the 21 m-tiles are dealt
+// to the row groups as evenly as possible (NT = 2: 4,4,4,3,3,3; NT = 1: nine
+// groups of 2 and three of 1), and warp w runs on sub-partition w % 4, so the
+// busiest sub-partition issues 11 (NT = 2) / 6 (NT = 1) DMMAs per k-step
+// (NT = 4: 21). The m-tile count is a template parameter (no predicated
+// mma.sync; two code paths per kernel).
+template <int MC>
+__device__ __forceinline__ double* nt_steps(const double* __restrict__ pa, int mstride, double* va, double* vb,
+                                            int bn, int bk, int sv, int i0, int t0, int lane, int64_t steps) {
+  constexpr int KT = 41;
+  for (int64_t s = 0; s < steps; ++s) {
+    double acc[MC][2];
+#pragma unroll
+    for (int mi = 0; mi < MC; ++mi) acc[mi][0] = acc[mi][1] = 0.0;
+    const double* vrow = va + bn * sv + bk;
+    const AFragLane af(lane);
+    double a_cur[MC], b_cur = vrow[0];
+#pragma unroll
+    for (int mi = 0; mi < MC; ++mi) a_cur[mi] = af.sign(pa[mi * mstride]);
+#pragma unroll
+    for (int ks = 0; ks < KT; ++ks) {
+      double a_nxt[MC], b_nxt = 0.0;
+      if (ks + 1 < KT) {
+        b_nxt = vrow[(ks + 1) * 4];
+#pragma unroll
+        for (int mi = 0; mi < MC; ++mi) a_nxt[mi] = af.sign(pa[mi * mstride + 4 * (ks + 1)]);
+      }
+#pragma unroll
+      for (int mi = 0; mi < MC; ++mi) dmma(acc[mi], a_cur[mi], b_cur);
+      if (ks + 1 < KT) {
+        b_cur = b_nxt;
+#pragma unroll
+        for (int mi = 0; mi < MC; ++mi) a_cur[mi] = a_nxt[mi];
+      }
+    }
+#pragma unroll
+    for (int mi = 0; mi < MC; ++mi) {
+      int coff;
+      const double2 z = pair_complex(acc[mi], lane, coff);
+      const int i = i0 + mi * 4 + (lane >> 3);
+      if (i < 81) *reinterpret_cast<double2*>(vb + (t0 + coff) * sv + 2 * i) = z;
+    }
+    __syncthreads();
+    double* tmp = va;
+    va = vb;
+    vb = tmp;
+  }
+  return va;
+}
+
+template <int NT, Layout L>
+__global__ void __launch_bounds__(32 * kWarps, 1)
+    smem81_nt_kernel(const double2* __restrict__ p, double* __restrict__ x_re, double* __restrict__ x_im,
+                     double* __restrict__ x_aos, int64_t batch, int64_t steps) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int n = 81, T = 8 * NT, RG = kWarps / NT, MT = 21, BASE = MT / RG, REM = MT % RG;
+  const SmemGeom g(n);
+  double2* ps = reinterpret_cast<double2*>(smem);
+  double* va = reinterpret_cast<double*>(smem + g.p_bytes);
+  double* vb = reinterpret_cast<double*>(smem + g.p_bytes + g.v_bytes);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t b0 = int64_t(blockIdx.x) * T;
+  for (int e = tid; e < g.mt * 4 * g.sp; e += blockDim.x) {
+    const int i = e / g.sp, j = e - i * g.sp;
+    ps[e] = (i < n && j < n) ? p[size_t(i) * n + j] : make_double2(0.0, 0.0);
+  }
+  for (int e = tid; e < T * g.sv; e += blockDim.x) {
+    const int t = e / g.sv, r = e - t * g.sv;
+    const int64_t b = b0 + t;
+    double v = 0.0;
+    if (b < batch && r < 2 * n) {
+      if (L == Layout::soa)
+        v = (r & 1) ? x_im[b * n + (r >> 1)] : x_re[b * n + (r >> 1)];
+      else
+        v = x_aos[b * 2 * n + r];
+    }
+    va[e] = v;
+    vb[e] = 0.0;
+  }
+  __syncthreads();
+  const AFragLane af(lane);
+  const int rg = warp / NT, nt = warp % NT;
+  const int m_begin = rg * BASE + (rg < REM ? rg : REM);
+  const double* pa =
+      reinterpret_cast<const double*>(ps) + size_t(m_begin * 4 + af.di) * 2 * g.sp + 2 * af.dj + af.comp;
+  const int mstride = 4 * 2 * g.sp, bn = nt * 8 + (lane >> 2), bk = lane & 3;
+  double* fin;
+  if (rg < REM)
+    fin = nt_steps<BASE + 1>(pa, mstride, va, vb, bn, bk, g.sv, m_begin * 4, nt * 8, lane, steps);
+  else
+    fin = nt_steps<BASE>(pa, mstride, va, vb, bn, bk, g.sv, m_begin * 4, nt * 8, lane, steps);
+  for (int e = tid; e < T * 2 * n; e += blockDim.x) {
+    const int t = e / (2 * n), r = e - t * 2 * n;
+    const int64_t b = b0 + t;
+    if (b >= batch) continue;
+    const double v = fin[t * g.sv + r];
+    if (L == Layout::soa) {
+      if (r & 1)
+        x_im[b * n + (r >> 1)] = v;
+      else
+        x_re[b * n + (r >> 1)] = v;
+    } else {
+      x_aos[b * 2 * n + r] = v;
+    }
+  }
+}
+
+template <int NT>
+void launch_nt(const double* p, double* x_re, double* x_im, double* x_aos, int64_t batch, int64_t steps,
+               Layout layout, cudaStream_t s) {
+  const SmemGeom g(81);
+  const unsigned blocks = static_cast<unsigned>((batch + 8 * NT - 1) / (8 * NT));
+  const double2* p2 = reinterpret_cast<const double2*>(p);
+  auto k = layout == Layout::soa ? smem81_nt_kernel<NT, Layout::soa> : smem81_nt_kernel<NT, Layout::aos>;
+  ensure_max_dyn_smem((const void*)k, int(g.total));
+  k<<<blocks, 32 * kWarps, g.total, s>>>(p2, x_re, x_im, x_aos, batch, steps);
+  LBG_CHECK_LAUNCH("smem81_nt_kernel");
+}
+
+// n = 81: n-tiles per CTA (4, 2 or 1) with the shortest critical path, in DMMA
+// issue slots per sub-partition and step: waves x busiest sub-partition's
+// DMMAs per k-step x 41 k-steps (NT = 4 first: ties keep the measured kernel)
+constexpr int kBusiest[3][2] = {{4, 21}, {2, 11}, {1, 6}};
+int smem81_nt(int64_t batch) {
+  int64_t best = INT64_MAX;
+  int nt_best = 4;
+  const int64_t ntiles = (batch + 7) / 8;
+  for (const auto& c : kBusiest) {
+    const int64_t ctas = (ntiles + c[0] - 1) / c[0];
+    const int64_t cost = ((ctas + sm_count() - 1) / sm_count()) * c[1] * 41;
+    if (cost < best) best = cost, nt_best = c[0];
+  }
+  return nt_best;
+}
+
 template <int N, int MG>
 void launch_mg(const double* p, int n, double* x_re, double* x_im, double* x_aos, int64_t batch,
                int64_t steps, Layout layout, cudaStream_t s) {
@@ -176,11 +315,25 @@ void launch_mg(const double* p, int n, double* x_re, double* x_im, double* x_aos
 
 bool smem_supported(std::size_t n) { return n >= 1 && n <= kMaxN; }
 
+int64_t smem81_cost(int64_t batch) {
+  const int nt = smem81_nt(batch);
+  int busiest = 21;
+  for (const auto& c : kBusiest)
+    if (c[0] == nt) busiest = c[1];
+  const int64_t ctas = ((batch + 7) / 8 + nt - 1) / nt;
+  return ((ctas + sm_count() - 1) / sm_count()) * busiest * 41;
+}
+
 void launch_smem(const double* p_dev, std::size_t n, double* x_re, double* x_im, double* x_aos,
                  int64_t batch, int64_t steps, Layout layout, cudaStream_t s) {
   if (batch <= 0) return;
   if (!smem_supported(n)) throw invalid_argument("smem kernel supports n <= 84");
-  if (n == 81) return launch_mg<81, 7>(p_dev, 81, x_re, x_im, x_aos, batch, steps, layout, s);
+  if (n == 81) {
+    const int nt = smem81_nt(batch);
+    if (nt == 2) return launch_nt<2>(p_dev, x_re, x_im, x_aos, batch, steps, layout, s);
+    if (nt == 1) return launch_nt<1>(p_dev, x_re, x_im, x_aos, batch, steps, layout, s);
+    return launch_mg<81, 7>(p_dev, 81, x_re, x_im, x_aos, batch, steps, layout, s);
+  }
   const int mt = (int(n) + 3) / 4;
   const int mg = (mt + 2) / 3;
   switch (mg) {

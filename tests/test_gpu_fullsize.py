@@ -113,17 +113,18 @@ def test_full_config_host_pipeline_pinned_and_pageable(lbg, torch, reference, cf
 
 @pytest.mark.parametrize("cfg", [1, 2, 3])
 def test_strong_scaling_shares_every_trajectory(lbg, torch, reference, cfg):
-    """The per-rank shares of the global batch at W = 8 (rank r owns
-    [floor(r B / 8), floor((r + 1) B / 8))) run on the small-batch kernels
-    (K1a, K1b-K, several-way stream-K K1c); each share against the
-    reference's trajectories of the same global ids."""
+    """The per-rank shares of the global batch at W = 2, 4, 8 (rank r owns
+    [floor(r B / W), floor((r + 1) B / W))) run on the small-batch kernels
+    (K1a; K1b with 2 / 1 n-tiles per CTA and K1b-K for config 2; several-way
+    stream-K K1c); each share against the reference's trajectories of the same
+    global ids."""
     P, rho0, want = ref_case(lbg, reference, cfg)
     d, B, S = CFG[cfg]
-    W = 8
-    for r in (0, 3, W - 1):
-        lo, hi = r * B // W, (r + 1) * B // W
-        got = device_run(lbg, torch, P, rho0[lo:hi], S, "auto")
-        assert_parity(got, want[lo:hi], (cfg, "share", r))
+    for W in (2, 4, 8):
+        for r in sorted({0, W // 2, W - 1}):
+            lo, hi = r * B // W, (r + 1) * B // W
+            got = device_run(lbg, torch, P, rho0[lo:hi], S, "auto")
+            assert_parity(got, want[lo:hi], (cfg, "share", W, r))
 
 
 def test_pipeline_rejects_before_any_output(lbg, torch):

@@ -232,6 +232,33 @@ def test_cluster_batch_shapes_vs_smem(lbg, torch, B, algo):
     assert np.abs(got - outs["smem"]).max() <= 1e-13 * max(1.0, np.abs(outs["smem"]).max())
 
 
+@pytest.mark.parametrize("B", [1, 8, 9, 100, 1000, 1024, 1184, 1185, 1200, 2000, 2048, 2368, 2400, 4096])
+def test_smem_n_tiles_per_cta_vs_torch(lbg, torch, B):
+    """K1b at n = 81 picks 4, 2 or 1 n-tiles per CTA from the batch (2 / 1 for
+    the 2,048 / 1,024 shares of config 2): every choice, ragged last CTA, more
+    CTAs than SMs, AoS and SoA, against a plain torch complex128 reference."""
+    rng = np.random.default_rng(300 + B)
+    n, S = 81, 9
+    P = (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) / (2 * n)
+    x = rng.standard_normal((B, n)) + 1j * rng.standard_normal((B, n))
+    dev = torch.device("cuda")
+    pt = torch.from_numpy(P).to(dev)
+    want = torch.from_numpy(x).to(dev)
+    for _ in range(S):
+        want = want @ pt.T
+    want = want.cpu().numpy()
+    tol = 1e-13 * max(1.0, np.abs(want).max())
+    xt = torch.from_numpy(x.copy()).to(dev)
+    lbg.evolve_batch_dev(pt, xt, S, algo="smem")
+    assert np.abs(xt.cpu().numpy() - want).max() <= tol
+    xr = torch.from_numpy(np.ascontiguousarray(x.real)).to(dev)
+    xi = torch.from_numpy(np.ascontiguousarray(x.imag)).to(dev)
+    L = lbg.lib()
+    lbg._check(L.lbg_evolve_shared_p_soa_dev(lbg._tp(pt), n, lbg._tp(xr), lbg._tp(xi), B, S, lbg.ALGO["smem"],
+                                             None, None), "soa")
+    assert np.abs(xr.cpu().numpy() + 1j * xi.cpu().numpy() - want).max() <= tol
+
+
 def test_config3_full_size(lbg, torch, oracle):
     _full_run(lbg, torch, 3, 1024, 200, "tiled", [0, 517, 1023], oracle)
 

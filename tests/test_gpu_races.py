@@ -35,6 +35,8 @@ SHAPES = [
     (729, 100, 2, "tiled"),       # ragged columns, several-way
     (300, 2, 6, "rowsplit"),      # K2c: P rows over all SMs, grid barrier per step
     (81, 3, 9, "cta"),            # K2b
+    (81, 2000, 4, "smem"),        # K1b, 2 n-tiles per CTA (12 warps, two m-tile counts)
+    (81, 1000, 4, "smem"),        # K1b, 1 n-tile per CTA
 ]
 
 
