@@ -239,9 +239,16 @@ void host_evolve(const double* p, size_t d, const double* rho0, int64_t batch, d
   // LBG_PIPELINE_TIMING (measurement only): device timestamps of each chunk's
   // H2D end, steps start / end and D2H end, printed relative to the call start
   static const bool timing = std::getenv("LBG_PIPELINE_TIMING") != nullptr;
-  cudaEvent_t te[4 * kMaxChunks + 1] = {};
+  struct TimingEvents {
+    cudaEvent_t e[4 * kMaxChunks + 1] = {};
+    ~TimingEvents() {
+      for (auto& x : e)
+        if (x) (void)cudaEventDestroy(x);
+    }
+  } tev;
+  cudaEvent_t* te = tev.e;
   if (timing)
-    for (auto& e : te) check_cuda(cudaEventCreate(&e), "event");
+    for (auto& e : tev.e) check_cuda(cudaEventCreate(&e), "event");
   auto mark = [&](int i, cudaStream_t st) {
     if (timing) check_cuda(cudaEventRecord(te[i], st), "event");
   };
@@ -310,7 +317,6 @@ void host_evolve(const double* p, size_t d, const double* rho0, int64_t batch, d
         for (int k = 0; k < 4; ++k) check_cuda(cudaEventElapsedTime(&t[k], te[4 * kMaxChunks], te[4 * c + k]), "t");
         std::fprintf(stderr, "chunk %d: h2d end %.3f  steps %.3f-%.3f  d2h end %.3f ms\n", c, t[0], t[1], t[2], t[3]);
       }
-      for (auto& e : te) cudaEventDestroy(e);
     }
   } catch (...) {
     pool.drain();
