@@ -283,15 +283,6 @@ void host_evolve(const double* p, size_t d, const double* rho0, int64_t batch, d
     }
     check_cuda(cudaEventRecord(pool.ev_chk, sk), "event");
     check_cuda(cudaEventSynchronize(pool.ev_chk), "sync check");
-    if (std::getenv("LBG_DEBUG_PIPELINE"))
-      for (int c = 0; c < nchunks; ++c)
-        std::fprintf(stderr, "chunk %d [%lld, %lld) pinned in %d out %d: %g %g %g staged-equal %d\n", c,
-                     (long long)bounds[c], (long long)bounds[c + 1], int(in_pinned), int(out_pinned), hchk[3 * c],
-                     hchk[3 * c + 1], hchk[3 * c + 2],
-                     in_pinned ? -1
-                               : int(std::memcmp(pin_in + size_t(bounds[c]) * n * 16,
-                                                 reinterpret_cast<const char*>(rho0) + size_t(bounds[c]) * n * 16,
-                                                 size_t(bounds[c + 1] - bounds[c]) * n * 16) == 0));
     for (int c = 0; c < nchunks; ++c)
       if (!(hchk[3 * c] <= 1e-8 && hchk[3 * c + 1] <= 1e-8 && hchk[3 * c + 2] >= -1e-8))
         throw invalid_argument("evolve: initial state fails physical-state checks");

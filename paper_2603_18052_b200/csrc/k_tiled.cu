@@ -652,11 +652,6 @@ int tiled_grid_of(size_t n, int64_t batch) {
     grid = int(nt);
     if (grid >= sms) grid -= grid % sms;
   }
-  static const int forced = [] {
-    const char* e = std::getenv("LBG_TILED_GRID");
-    return e ? std::atoi(e) : 0;
-  }();
-  if (forced > 0) grid = std::min(forced, slots);
   return std::max(1, grid);
 }
 template <class G>
