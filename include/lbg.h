@@ -83,6 +83,28 @@ int lbg_expm_dev(const double* a, size_t n, double dt, double* out, double* work
 size_t lbg_expm_workspace(size_t n); /* bytes */
 
 /* ------------------------------------------------------------------------
+ * Batched building blocks (assemble / expm many independent
+ * models at once, as a per-parameter sweep over arbitrary models needs —
+ * propagate.cpp:137-143 builds one model, L and P per point):
+ * lbg_build_lindbladian_batched_dev: out[b] = L(h[b], ops[b]) for b < batch;
+ *   h: batch x d x d, ops: batch x n_ops x d x d, out: batch x d^2 x d^2
+ *   (complex AoS, device); each out[b] is bit-identical to
+ *   lbg_build_lindbladian_dev on model b (lindblad.cpp:37-59 order).
+ * lbg_expm_batched_dev: out[b] = exp(a[b] dt) for b < batch (n x n each,
+ *   device). n <= 16: one CTA per matrix with its own scaling (each out[b]
+ *   equals lbg_expm_dev(a[b])); larger n: batched DMMA GEMMs with the batch's
+ *   largest squaring count (within ~1e-14 of the per-matrix result). A
+ *   non-finite entry anywhere -> LBG_EINVAL (expm.cpp:110-112); more than 64
+ *   squarings -> LBG_ERUNTIME. Synchronises the stream once (the norm).
+ *   `work` (device): lbg_expm_batched_workspace(n, batch) bytes.
+ * ------------------------------------------------------------------------ */
+int lbg_build_lindbladian_batched_dev(size_t d, const double* h, size_t n_ops, const double* ops,
+                                      int64_t batch, double* out, void* stream);
+size_t lbg_expm_batched_workspace(size_t n, int64_t batch); /* bytes */
+int lbg_expm_batched_dev(const double* a, size_t n, int64_t batch, double dt, double* out, void* work,
+                         void* stream);
+
+/* ------------------------------------------------------------------------
  * Batched shared-P propagation: replaces lb::evolve (propagate.hpp:33-34,
  * propagate.cpp:75-109) over `batch` independent trajectories.
  * P: n x n AoS (n = d^2). X: batch x n complex, trajectory b's vec(rho_b) at

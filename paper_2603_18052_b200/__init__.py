@@ -74,6 +74,10 @@ def lib() -> C.CDLL:
     L.lbg_expm_dev.argtypes = [vp, _sz, C.c_double, vp, vp, vp]
     L.lbg_expm_workspace.argtypes = [_sz]
     L.lbg_expm_workspace.restype = _sz
+    L.lbg_build_lindbladian_batched_dev.argtypes = [_sz, vp, _sz, vp, C.c_int64, vp, vp]
+    L.lbg_expm_batched_workspace.argtypes = [_sz, C.c_int64]
+    L.lbg_expm_batched_workspace.restype = _sz
+    L.lbg_expm_batched_dev.argtypes = [vp, _sz, C.c_int64, C.c_double, vp, vp, vp]
     L.lbg_evolve_workspace.argtypes = [_sz, C.c_int64, C.c_int]
     L.lbg_evolve_workspace.restype = _sz
     L.lbg_evolve_shared_p_soa_dev.argtypes = [vp, _sz, vp, vp, C.c_int64, C.c_int64, C.c_int, vp, vp]
@@ -212,6 +216,26 @@ def expm(a, dt: float):
     out = np.zeros_like(a)
     _check(lib().lbg_expm(_p(a), a.shape[0], float(dt), _p(out)), "expm")
     return out
+
+
+def build_lindbladian_batched_dev(h, ops, out, stream=None):
+    """Batched K5 on device tensors: h (B, d, d), ops (B, n_ops, d, d) complex128
+    -> out (B, d^2, d^2); each out[b] bit-identical to build_lindbladian(h[b], ops[b])."""
+    B, d = h.shape[0], h.shape[-1]
+    n_ops = ops.shape[1] if ops is not None and ops.dim() == 4 else 0
+    _check(lib().lbg_build_lindbladian_batched_dev(d, _tp(h), n_ops, _tp(ops) if n_ops else None, B, _tp(out),
+                                                   _sp(stream)), "build_lindbladian_batched_dev")
+
+
+def expm_batched_workspace(n: int, batch: int) -> int:
+    return int(lib().lbg_expm_batched_workspace(n, batch))
+
+
+def expm_batched_dev(a, dt: float, out, work, stream=None):
+    """Batched P_b = exp(a_b dt) on device tensors a, out (B, n, n) complex128."""
+    B, n = a.shape[0], a.shape[-1]
+    _check(lib().lbg_expm_batched_dev(_tp(a), n, B, float(dt), _tp(out), _tp(work), _sp(stream)),
+           "expm_batched_dev")
 
 
 def step_soa(p, v):

@@ -317,6 +317,32 @@ int lbg_expm(const double* a, size_t n, double dt, double* out) {
   });
 }
 
+// ---- batched building blocks (lbg_assemble_batched / lbg_expm_batched) ----
+int lbg_build_lindbladian_batched_dev(size_t d, const double* h, size_t n_ops, const double* ops, int64_t batch,
+                                      double* out, void* stream) {
+  return guarded([&] {
+    if (d == 0) throw invalid_argument("build_lindbladian: dimension must be positive");
+    if (batch < 0) throw invalid_argument("build_lindbladian: negative batch");
+    if (batch == 0) return;
+    if (!h || !out || (n_ops && !ops)) throw invalid_argument("build_lindbladian: null pointer");
+    launch_build_lindbladian_batched(d, h, n_ops, ops, batch, out, as_stream(stream));
+  });
+}
+
+size_t lbg_expm_batched_workspace(size_t n, int64_t batch) { return expm_batched_workspace(n, batch); }
+
+int lbg_expm_batched_dev(const double* a, size_t n, int64_t batch, double dt, double* out, void* work,
+                         void* stream) {
+  return guarded([&] {
+    if (n == 0) throw invalid_argument("expm: matrix must be square and non-empty");
+    if (batch < 0) throw invalid_argument("expm: negative batch");
+    if (!std::isfinite(dt)) throw invalid_argument("expm: dt must be finite");
+    if (batch == 0) return;
+    if (!a || !out || !work) throw invalid_argument("expm: null pointer");
+    expm_batched_dev(a, n, batch, dt, out, work, as_stream(stream));
+  });
+}
+
 // ---- batched shared-P propagation ----
 size_t lbg_evolve_workspace(size_t n, int64_t batch, int algo) {
   if (n == 0 || batch <= 0) return 0;
@@ -572,11 +598,20 @@ int lbg_evolve_sweep_dev(size_t d, const double* h0, const double* hd, const dou
     if (!work) throw invalid_argument("sweep: workspace required");
     cudaStream_t s = as_stream(stream);
     if (batch == 0) return;
-    {  // propagate.cpp:79-80: lb::evolve validates rho0 before any work (K6, 24-byte D2H)
+    {  // propagate.cpp:79-80: lb::evolve validates rho0 before any work (K6), and
+       // lb::expm rejects a non-finite generator (expm.cpp:110-112): the model
+       // terms and every (delta, s) are checked for NaN / Inf; one 32-byte D2H
       double* dchk = nullptr;
-      check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&dchk), 3 * sizeof(double), s), "malloc check");
+      check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&dchk), 4 * sizeof(double), s), "malloc check");
+      unsigned* flag = reinterpret_cast<unsigned*>(dchk + 3);
+      check_cuda(cudaMemsetAsync(flag, 0, sizeof(unsigned), s), "memset");
       launch_check_state(rho0, d, 1, dchk, s);
-      double chk[3];
+      const long long dd = (long long)(2 * d * d);
+      for (const double* m : {h0, hd, hs}) launch_flag_nonfinite(m, dd, flag, s);
+      launch_flag_nonfinite(ops, dd * (long long)n_ops, flag, s);
+      launch_flag_nonfinite(delta, batch, flag, s);
+      launch_flag_nonfinite(scale, batch, flag, s);
+      double chk[4];
       const cudaError_t e1 = cudaMemcpyAsync(chk, dchk, sizeof chk, cudaMemcpyDeviceToHost, s);
       const cudaError_t e2 = cudaFreeAsync(dchk, s);
       check_cuda(e1, "D2H check");
@@ -584,6 +619,9 @@ int lbg_evolve_sweep_dev(size_t d, const double* h0, const double* hd, const dou
       check_cuda(cudaStreamSynchronize(s), "sync check");
       if (!(chk[0] <= 1e-8 && chk[1] <= 1e-8 && chk[2] >= -1e-8))
         throw invalid_argument("evolve: initial state fails physical-state checks");
+      unsigned bad;
+      std::memcpy(&bad, &chk[3], sizeof bad);
+      if (bad) throw invalid_argument("sweep: non-finite entries in the model terms or sweep parameters");
     }
     bool real = false;
     if (mode == LBG_SWEEP_REAL || mode == LBG_SWEEP_AUTO) {

@@ -108,6 +108,14 @@ void launch_build_lindbladian(std::size_t d, const double* h, std::size_t n_ops,
                               const double* ops, double* out, cudaStream_t s);
 constexpr std::size_t kExpmStreamN = 128;  // expm products on the stream-K engine from here
 std::size_t expm_workspace(std::size_t n);  // bytes (lbg_expm_workspace)
+// flag |= 1 when any of p[0 .. count) is not finite (k_validate.cu)
+void launch_flag_nonfinite(const double* p, long long count, unsigned* flag, cudaStream_t s);
+// batched building blocks (k_model.cu)
+void launch_build_lindbladian_batched(std::size_t d, const double* h, std::size_t n_ops, const double* ops,
+                                      int64_t batch, double* out, cudaStream_t s);
+std::size_t expm_batched_workspace(std::size_t n, int64_t batch);
+void expm_batched_dev(const double* a, std::size_t n, int64_t batch, double dt, double* out, void* work,
+                      cudaStream_t s);
 // one complex GEMM C = A B (n x n) on the persistent stream-K engine (k_tiled.cu)
 std::size_t zgemm_stream_workspace(int n);
 void launch_zgemm_stream(const double* a, const double* b, double* c, int n, void* aux, cudaStream_t s);

@@ -1,7 +1,9 @@
 // k_model.cu — model-side kernels: Kronecker assembly of the vectorised
 // Lindbladian (K5, single model), the GPU propagator P = exp(L dt) (K4,
 // single matrix), the batched invariant check (K6) and the single-step shim.
+#include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <vector>
 
 #include "common.cuh"
@@ -45,12 +47,9 @@ __device__ __forceinline__ double2 ldl_entry(const double2* __restrict__ l, int 
 //                                        - 1/2 I (x) (L_m^dag L_m)^T ]
 // in the reference's evaluation order (lindblad.cpp:46-57): kron entries are
 // a[i][j] * b[k][l] complex products, accumulated with add_scaled.
-__global__ void build_lindbladian_kernel(const double2* __restrict__ h,
-                                         const double2* __restrict__ ops, int n_ops, int d,
-                                         double2* __restrict__ out) {
+__device__ __forceinline__ double2 lindblad_entry(const double2* __restrict__ h, const double2* __restrict__ ops,
+                                                  int n_ops, int d, long long e) {
   const int n = d * d;
-  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (e >= (long long)n * n) return;
   const int R = int(e / n), Cc = int(e - (long long)R * n);
   const int i = R / d, k = R - i * d, j = Cc / d, l = Cc - j * d;
   const double2 one = make_double2(1.0, 0.0), zero = make_double2(0.0, 0.0);
@@ -67,7 +66,24 @@ __global__ void build_lindbladian_kernel(const double2* __restrict__ h,
     const double2 b = (i == j) ? ldl_entry(lm, d, l, k) : zero;
     acc = cadd(acc, cmul(make_double2(-0.5, 0.0), cmul(dij, b)));
   }
-  out[e] = acc;
+  return acc;
+}
+__global__ void build_lindbladian_kernel(const double2* __restrict__ h,
+                                         const double2* __restrict__ ops, int n_ops, int d,
+                                         double2* __restrict__ out) {
+  const long long nn = (long long)(d * d) * (d * d);
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e < nn) out[e] = lindblad_entry(h, ops, n_ops, d, e);
+}
+// batch of models: model b = (h + b d^2, ops + b n_ops d^2) -> out + b d^4
+__global__ void build_lindbladian_batched_kernel(const double2* __restrict__ h, const double2* __restrict__ ops,
+                                                 int n_ops, int d, long long total, double2* __restrict__ out) {
+  const long long nn = (long long)(d * d) * (d * d);
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long b = q / nn, e = q - b * nn;
+    out[q] = lindblad_entry(h + b * d * d, ops + b * n_ops * d * d, n_ops, d, e);
+  }
 }
 
 // out = x + c0*I + c1*a1 + c2*a2 + c3*a3 + c4*a4   (any pointer may be null)
@@ -222,6 +238,108 @@ __global__ void __launch_bounds__(kSmallNN) small_expm_kernel(const double2* __r
   if (e < n * n) out[e] = T[e];
 }
 
+// Batched exp(a_b dt) for n <= 16: one CTA per matrix, each with its own
+// scaling: the 1-norm in colsum_kernel's summation order and expm_dev's
+// squaring rule, then small_taylor — each out_b equals lbg_expm_dev(a_b).
+// bad |= 1 for non-finite input, 2 for more than 64 squarings.
+__global__ void __launch_bounds__(kSmallNN) small_expm_batched_kernel(const double2* __restrict__ a, int n, double dt,
+                                                                      SmallCoef co, double2* __restrict__ out,
+                                                                      unsigned* __restrict__ bad) {
+  __shared__ double2 A[kSmallNN], A2[kSmallNN], A3[kSmallNN], A4[kSmallNN], T[kSmallNN];
+  __shared__ double part[8][kSmallN + 1];
+  __shared__ int s_sq;
+  __shared__ double s_scale;
+  const long long nn = (long long)n * n, b = blockIdx.x;
+  const double2* ab = a + b * nn;
+  const int e = threadIdx.x;
+  {
+    const int c = e & 15, ty = e >> 4;  // 16 columns x 16 row groups; groups 0..7 used
+    if (ty < 8 && c < n) {
+      double sum = 0.0;
+      for (int r = ty; r < n; r += 8) sum += hypot(ab[r * n + c].x, ab[r * n + c].y);
+      part[ty][c] = sum;
+    }
+  }
+  __syncthreads();
+  if (e == 0) {
+    double nrm = 0.0;
+    for (int c = 0; c < n; ++c) {
+      double t = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t += part[k][c];
+      nrm = (isnan(t) || t > nrm) ? t : nrm;
+    }
+    nrm *= fabs(dt);
+    int sq = 0;
+    if (!isfinite(nrm)) {
+      atomicOr(bad, 1u);
+      sq = -1;
+    } else if (nrm > 0.79) {
+      sq = int(ceil(log2(nrm / 0.79)));
+      if (sq > 64) {
+        atomicOr(bad, 2u);
+        sq = -1;
+      }
+    }
+    s_sq = sq;
+    s_scale = sq >= 0 ? dt * ldexp(1.0, -sq) : 0.0;
+  }
+  __syncthreads();
+  const int sq = s_sq;
+  if (sq < 0) return;
+  if (e < nn) A[e] = make_double2(ab[e].x * s_scale, ab[e].y * s_scale);
+  __syncthreads();
+  small_taylor(A, A2, A3, A4, T, n, co.c, sq);
+  if (e < nn) out[b * nn + e] = T[e];
+}
+
+// max over a batch of n x n matrices of the 1-norm (bits of a non-negative
+// double, so unsigned max = double max; NaN sorts above every finite value)
+__global__ void norm_batched_kernel(const double2* __restrict__ a, int n, long long batch,
+                                    unsigned long long* __restrict__ nmax) {
+  __shared__ double part[8][33];
+  const long long nbx = (n + 31) / 32;
+  const long long b = blockIdx.x / nbx;
+  const int tx = threadIdx.x, ty = threadIdx.y, c = int(blockIdx.x - b * nbx) * 32 + tx;
+  const double2* m = a + b * n * (long long)n;
+  double sum = 0.0;
+  if (c < n)
+    for (int r = ty; r < n; r += 8) sum += hypot(m[(long long)r * n + c].x, m[(long long)r * n + c].y);
+  part[ty][tx] = sum;
+  __syncthreads();
+  if (ty == 0) {
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += part[k][tx];
+    for (int o = 16; o > 0; o >>= 1) {  // NaN-propagating max (fmax would drop a NaN column)
+      const double u = __shfl_xor_sync(0xffffffffu, t, o);
+      t = (isnan(t) || isnan(u)) ? __longlong_as_double(-1ll) : fmax(t, u);
+    }
+    if (tx == 0) atomicMax(nmax, (unsigned long long)__double_as_longlong(t));
+  }
+}
+
+// out = x + c0 I + c1 a1 + c2 a2 + c3 a3 + c4 a4 over a batch (flat index)
+__global__ void combo_flat_kernel(double2* __restrict__ out, const double2* __restrict__ x,
+                                  const double2* __restrict__ a1, const double2* __restrict__ a2,
+                                  const double2* __restrict__ a3, const double2* __restrict__ a4, double c0,
+                                  double c1, double c2, double c3, double c4, int n, long long total) {
+  const long long nn = (long long)n * n;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long e = q % nn;
+    double2 v = x ? x[q] : make_double2(0.0, 0.0);
+    if (e / n == e % n) v.x += c0;
+    if (a1) { v.x += c1 * a1[q].x; v.y += c1 * a1[q].y; }
+    if (a2) { v.x += c2 * a2[q].x; v.y += c2 * a2[q].y; }
+    if (a3) { v.x += c3 * a3[q].x; v.y += c3 * a3[q].y; }
+    if (a4) { v.x += c4 * a4[q].x; v.y += c4 * a4[q].y; }
+    out[q] = v;
+  }
+}
+
+unsigned grid_for(long long total) { return unsigned(std::min<long long>((total + 255) / 256, 148LL * 64)); }
+
 // SoA planes <-> AoS (interleaved) for the AoS-only latency kernels
 __global__ void planes_to_aos_kernel(const double* __restrict__ re, const double* __restrict__ im, long long count,
                                      double2* __restrict__ out) {
@@ -266,6 +384,16 @@ void launch_build_lindbladian(size_t d, const double* h, size_t n_ops, const dou
   LBG_CHECK_LAUNCH("build_lindbladian_kernel");
 }
 
+void launch_build_lindbladian_batched(size_t d, const double* h, size_t n_ops, const double* ops, int64_t batch,
+                                      double* out, cudaStream_t s) {
+  if (batch <= 0) return;
+  const long long total = (long long)batch * (long long)(d * d) * (long long)(d * d);
+  build_lindbladian_batched_kernel<<<grid_for(total), 256, 0, s>>>(
+      reinterpret_cast<const double2*>(h), reinterpret_cast<const double2*>(ops), int(n_ops), int(d), total,
+      reinterpret_cast<double2*>(out));
+  LBG_CHECK_LAUNCH("build_lindbladian_batched_kernel");
+}
+
 // Taylor coefficients 1/k!, k = 0..16
 static double inv_fact(int k) {
   double f = 1.0;
@@ -302,7 +430,7 @@ void expm_dev(const double* a, size_t n, double dt, double* out, double* work, c
   check_cuda(cudaMemcpyAsync(cs.data(), colsum, sizeof(double) * n, cudaMemcpyDeviceToHost, s), "D2H norm");
   check_cuda(cudaStreamSynchronize(s), "sync norm");
   double nrm = 0.0;
-  for (double v : cs) nrm = std::max(nrm, v);
+  for (double v : cs) nrm = (std::isnan(v) || v > nrm) ? v : nrm;  // a NaN column must not be dropped
   nrm *= std::fabs(dt);
   if (!std::isfinite(nrm)) throw invalid_argument("expm: non-finite entries in input");
   int sq = 0;
@@ -351,6 +479,90 @@ void expm_dev(const double* a, size_t n, double dt, double* out, double* work, c
   double2* cur = T;
   for (int i = 0; i < sq; ++i) {
     double2* dst = (i == sq - 1) ? P : (cur == T ? M : T);
+    mm(cur, cur, dst);
+    cur = dst;
+  }
+}
+
+// Batched P_b = exp(a_b dt). n <= 16: one CTA per matrix (own scaling, equal
+// to expm_dev per matrix). Larger n: the construction of expm_dev on batched
+// tile GEMMs (launch_zgemm, the batch in chunks of 65,535 along grid z) with the
+// batch's largest squaring count (one host sync for the norm, like expm_dev).
+size_t expm_batched_workspace(size_t n, int64_t batch) {
+  if (n <= size_t(kSmallN) || batch <= 0) return 256;
+  return 6 * ((size_t(batch) * n * n * 16 + 255) & ~size_t(255)) + 256;
+}
+void expm_batched_dev(const double* a, size_t n, int64_t batch, double dt, double* out, void* work, cudaStream_t s) {
+  if (batch <= 0) return;
+  constexpr double kTheta16 = 0.79;
+  const long long nn = (long long)n * (long long)n, total = (long long)batch * nn;
+  char* w = static_cast<char*>(work);
+  double c[17];
+  for (int k = 0; k <= 16; ++k) c[k] = inv_fact(k);
+  if (n <= size_t(kSmallN)) {
+    unsigned* bad = reinterpret_cast<unsigned*>(w);
+    check_cuda(cudaMemsetAsync(bad, 0, 4, s), "memset");
+    SmallCoef co;
+    for (int k = 0; k <= 16; ++k) co.c[k] = c[k];
+    small_expm_batched_kernel<<<unsigned(batch), kSmallNN, 0, s>>>(reinterpret_cast<const double2*>(a), int(n), dt,
+                                                                    co, reinterpret_cast<double2*>(out), bad);
+    LBG_CHECK_LAUNCH("small_expm_batched_kernel");
+    unsigned hbad = 0;
+    check_cuda(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, s), "D2H");
+    check_cuda(cudaStreamSynchronize(s), "sync");
+    if (hbad & 1u) throw invalid_argument("expm: non-finite entries in input");
+    if (hbad & 2u) throw runtime_error("expm: norm of a*dt requires more than 64 squarings");
+    return;
+  }
+  const size_t mb = (size_t(total) * 16 + 255) & ~size_t(255);
+  double2* M[6];
+  for (int q = 0; q < 6; ++q) M[q] = reinterpret_cast<double2*>(w + q * mb);
+  unsigned long long* nmax = reinterpret_cast<unsigned long long*>(w + 6 * mb);
+  check_cuda(cudaMemsetAsync(nmax, 0, 8, s), "memset");
+  norm_batched_kernel<<<unsigned(batch * ((static_cast<long long>(n) + 31) / 32)), dim3(32, 8), 0, s>>>(
+      reinterpret_cast<const double2*>(a), int(n), batch, nmax);
+  LBG_CHECK_LAUNCH("norm_batched_kernel");
+  unsigned long long bits = 0;
+  check_cuda(cudaMemcpyAsync(&bits, nmax, 8, cudaMemcpyDeviceToHost, s), "D2H norm");
+  check_cuda(cudaStreamSynchronize(s), "sync norm");
+  double nrm;
+  std::memcpy(&nrm, &bits, 8);
+  nrm *= std::fabs(dt);
+  if (!std::isfinite(nrm)) throw invalid_argument("expm: non-finite entries in input");
+  int sq = 0;
+  if (nrm > kTheta16) {
+    sq = int(std::ceil(std::log2(nrm / kTheta16)));
+    if (sq > 64) throw runtime_error("expm: norm of a*dt requires more than 64 squarings");
+  }
+  const double scale = dt * std::ldexp(1.0, -sq);
+  double2 *A1 = M[0], *A2 = M[1], *A3 = M[2], *A4 = M[3], *T = M[4], *MM = M[5];
+  double2* P = reinterpret_cast<double2*>(out);
+  const unsigned g = grid_for(total);
+  combo_flat_kernel<<<g, 256, 0, s>>>(A1, nullptr, reinterpret_cast<const double2*>(a), nullptr, nullptr, nullptr,
+                                      0.0, scale, 0.0, 0.0, 0.0, int(n), total);
+  LBG_CHECK_LAUNCH("combo_flat_kernel");
+  auto mm = [&](const double2* x, const double2* y, double2* z) {
+    for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
+      const int cb = int(std::min<int64_t>(65535, batch - b0));
+      launch_zgemm(reinterpret_cast<const double*>(x + b0 * nn), reinterpret_cast<const double*>(y + b0 * nn),
+                   reinterpret_cast<double*>(z + b0 * nn), int(n), cb, nn, nn, nn, s);
+    }
+  };
+  mm(A1, A1, A2);
+  mm(A2, A1, A3);
+  mm(A2, A2, A4);
+  combo_flat_kernel<<<g, 256, 0, s>>>(T, nullptr, A1, A2, A3, A4, c[12], c[13], c[14], c[15], c[16], int(n), total);
+  LBG_CHECK_LAUNCH("combo_flat_kernel");
+  for (int j = 2; j >= 0; --j) {
+    mm(A4, T, MM);
+    double2* dst = (j == 0 && sq == 0) ? P : T;
+    combo_flat_kernel<<<g, 256, 0, s>>>(dst, MM, A1, A2, A3, nullptr, c[4 * j], c[4 * j + 1], c[4 * j + 2],
+                                        c[4 * j + 3], 0.0, int(n), total);
+    LBG_CHECK_LAUNCH("combo_flat_kernel");
+  }
+  double2* cur = T;
+  for (int i = 0; i < sq; ++i) {
+    double2* dst = (i == sq - 1) ? P : (cur == T ? MM : T);
     mm(cur, cur, dst);
     cur = dst;
   }

@@ -93,7 +93,10 @@ __global__ void sweep_norm_kernel(const double2* __restrict__ A, int n, long lon
     double t = 0.0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) t += part[k][tx];
-    for (int o = 16; o > 0; o >>= 1) t = fmax(t, __shfl_xor_sync(0xffffffffu, t, o));
+    for (int o = 16; o > 0; o >>= 1) {  // NaN-propagating max (fmax would drop a NaN column)
+      const double u = __shfl_xor_sync(0xffffffffu, t, o);
+      t = (isnan(t) || isnan(u)) ? __longlong_as_double(-1ll) : fmax(t, u);
+    }
     if (tx == 0) atomicMax(nmax, (unsigned long long)__double_as_longlong(t));
   }
 }

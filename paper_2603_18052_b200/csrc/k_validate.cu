@@ -99,7 +99,23 @@ int vguard(F&& f) {
   }
 }
 
+__global__ void flag_nonfinite_kernel(const double* __restrict__ p, long long count, unsigned* __restrict__ flag) {
+  bool bad = false;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x)
+    bad = bad || !isfinite(p[i]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+}
+
 }  // namespace
+
+// flag |= 1 when any of p[0 .. count) is NaN or infinite (stream-ordered)
+void launch_flag_nonfinite(const double* p, long long count, unsigned* flag, cudaStream_t s) {
+  if (count <= 0) return;
+  const unsigned blocks = unsigned(std::min<long long>((count + 255) / 256, 148LL * 8));
+  flag_nonfinite_kernel<<<blocks, 256, 0, s>>>(p, count, flag);
+  LBG_CHECK_LAUNCH("flag_nonfinite_kernel");
+}
+
 }  // namespace lbg
 
 using namespace lbg;
