@@ -661,6 +661,13 @@ int lbg_grape_chain(size_t d, const double* h0, const double* hc, const double* 
     if (d == 0 || !h0 || !hc || !rho0 || !out) throw invalid_argument("grape_chain: operator shapes do not conform");
     if (steps_per_segment < 0) throw invalid_argument("grape_chain: negative steps");
     if (!std::isfinite(dt)) throw invalid_argument("expm: dt must be finite");
+    {  // lb::expm rejects a non-finite generator (expm.cpp:110-112)
+      bool fin = true;
+      for (size_t e = 0; e < 2 * d * d; ++e) fin = fin && std::isfinite(h0[e]) && std::isfinite(hc[e]);
+      for (int64_t j = 0; j < segments; ++j) fin = fin && std::isfinite(amplitudes[j]);
+      for (size_t e = 0; ops && e < 2 * n_ops * d * d; ++e) fin = fin && std::isfinite(ops[e]);
+      if (!fin) throw invalid_argument("expm: non-finite entries in input");
+    }
     // make_model's Hermiticity check on every segment Hamiltonian (lindblad.cpp:28-29)
     std::vector<double> h(2 * d * d);
     for (int64_t j = 0; j < segments; ++j) {

@@ -156,3 +156,21 @@ def test_sweep_rejects_non_finite_parameters(lbg, torch):
                 lbg.evolve_sweep_dev(T(a0), T(ad), T(as_), T(ops), T(de), T(sc), 0.1, T(r0), 5, pops, ens, work,
                                      mode=mode)
     lbg.evolve_sweep_dev(T(h0), T(hd), T(hs), T(ops), T(delta), T(scale), 0.1, T(r0), 5, pops, ens, work)
+
+
+def test_grape_rejects_non_finite_like_the_reference(lbg, reference):
+    """A NaN / Inf amplitude or operator entry: lb::grape_chain's per-segment
+    expm throws std::invalid_argument (expm.cpp:110-112); so does the engine."""
+    h0, hc, op, amps, dt, rho0 = reference.grape_inputs(3, 10)
+    for what in ("amp", "h0", "op"):
+        a, h, o = amps.copy(), h0.copy(), np.array(op, copy=True)
+        if what == "amp":
+            a[4] = np.nan
+        elif what == "h0":
+            h[0, 0] = np.inf
+        else:
+            o.reshape(-1)[3] = np.nan
+        with pytest.raises(ValueError, match="non-finite"):
+            lbg.grape_chain(h, hc, a, 4, dt, o, rho0)
+        with pytest.raises(ValueError):
+            reference.grape_chain(h, hc, a, 4, dt, o, rho0)
