@@ -466,13 +466,13 @@ def run_ours(args):
         torch.cuda.synchronize(dev)
         want = xr.cpu().numpy().reshape(b, d, d)
         with Clocks(local) as eclk:  # clocks during the host-buffer calls too
-            med, calls, h2d, d2h, diff = host_call_e2e(torch, lbg, P, rho0, S, want, True, 11)
+            med, calls, h2d, d2h, diff = host_call_e2e(torch, lbg, P, rho0, S, want, True, 21)
         med_pg, calls_pg, _, _, diff_pg = host_call_e2e(torch, lbg, P, rho0, S, want, False, 5)
         e2e_s = max_over_ranks(torch, med)
         e2e_pg = max_over_ranks(torch, med_pg)
         e2e = {"value": gb * S / e2e_s, "unit": "traj-steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_call": e2e_s * 1e3, "ms_per_call_all": [round(c * 1e3, 3) for c in calls],
-               "call": "lbg_evolve_shared_p (pinned host buffers, synchronous); median of 11",
+               "call": "lbg_evolve_shared_p (pinned host buffers, synchronous); median of 21 (the shared box throws occasional 35-100 ms calls)",
                "max_abs_diff_vs_device": diff, "clocks": eclk.summary(),
                "pageable": {"value": gb * S / e2e_pg, "ms_per_call": e2e_pg * 1e3,
                             "ms_per_call_all": [round(c * 1e3, 3) for c in calls_pg],
