@@ -633,7 +633,6 @@ size_t ldv_of(int64_t batch) {
 // HEADs wait for the slowest contributor). With fewer iterations than
 // kMinItersPerCta per SM: one CTA per tile, a whole multiple of the SM count
 // when there are at least as many tiles as SMs.
-// LBG_TILED_GRID overrides (measurement only).
 template <class G>
 int tiled_grid_of(size_t n, int64_t batch) {
   const auto kern = tiled_evolve_kernel<G>;
