@@ -134,3 +134,34 @@ def test_sweep_validates_rho0_like_evolve(lbg):
             with pytest.raises(ValueError, match="physical-state"):
                 lbg.evolve_sweep_dev(T(h0), T(hd), T(hs), T(ops), T(delta), T(scale), 0.1, T(r0), 5, pops, ens, work,
                                      mode=mode)
+
+
+def test_no_per_step_allocation(lbg):
+    """test_propagate.cpp:200-214: evolve allocates nothing per step. Device
+    memory in use is the same after 10 and after 2,000 steps, on the device
+    entry point (caller's workspace) and on the pooled host-buffer call, and
+    repeated host calls of one size do not grow it."""
+    import torch
+    dev = torch.device("cuda")
+    h, ops = lbg.config_model(2)
+    P = lbg.expm(lbg.build_lindbladian(h, ops), 0.1)
+    rho0 = lbg.ginibre_batch(2, 0, 512, 9)
+    pt = torch.from_numpy(P).to(dev)
+    x = torch.from_numpy(rho0.reshape(512, 81).copy()).to(dev)
+    work = torch.empty(max(lbg.evolve_workspace(81, 512, "auto"), 1), dtype=torch.uint8, device=dev)
+    lbg.evolve_batch_dev(pt, x, 10, work=work)  # warm: module load, attributes
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    for steps in (10, 2000):
+        lbg.evolve_batch_dev(pt, x, steps, work=work)
+        torch.cuda.synchronize()
+        assert torch.cuda.mem_get_info()[0] == free0, steps
+    hb = lbg.ginibre_batch(1, 0, 70000, 3)
+    P1 = lbg.expm(lbg.build_lindbladian(*lbg.config_model(1)), 0.1)
+    lbg.evolve_batch(P1, hb, 5)  # grows the pool once
+    torch.cuda.synchronize()
+    free1 = torch.cuda.mem_get_info()[0]
+    for steps in (5, 1000, 5):
+        lbg.evolve_batch(P1, hb, steps)
+        torch.cuda.synchronize()
+        assert torch.cuda.mem_get_info()[0] == free1, steps
