@@ -87,6 +87,29 @@ def test_expm_vs_reference(lbg, golden):
         lbg.expm(np.full((2, 2), np.nan), 1.0)
 
 
+@pytest.mark.parametrize("n", [3, 16, 17, 40, 130])
+def test_expm_properties(lbg, n):
+    """test_expm.cpp:27-164 on every expm path (one-CTA n <= 16, tile GEMMs, the
+    stream-K engine for n >= 128): diagonal, semigroup (1e-10), unitary (1e-11),
+    and the scaling-and-squaring branch agreeing with direct evaluation."""
+    rng = np.random.default_rng(n)
+    dg = rng.normal(size=n) + 1j * rng.normal(size=n)
+    got = lbg.expm(np.diag(dg), 0.7)
+    want = np.diag(np.exp(dg * 0.7))
+    assert np.abs(got - want).max() <= 1e-13 * np.abs(want).max()
+    a = (rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))) / np.sqrt(n)
+    s, t = 0.3, 0.45
+    lhs = lbg.expm(a, s + t)
+    rhs = lbg.expm(a, s) @ lbg.expm(a, t)
+    assert np.abs(lhs - rhs).max() <= 1e-10 * np.abs(lhs).max()
+    hm = (a + a.conj().T) / 2
+    u = lbg.expm(-1j * hm, 2.0)
+    assert np.abs(u @ u.conj().T - np.eye(n)).max() <= 1e-11
+    big = lbg.expm(a, 9.0)  # ||a dt|| >> 0.79: several squarings
+    half = lbg.expm(a, 4.5)
+    assert np.abs(big - half @ half).max() <= 1e-10 * np.abs(big).max()
+
+
 def test_expm_d27_vs_oracle(lbg, oracle):
     h, ops = lbg.config_model(3)
     L = lbg.build_lindbladian(h, ops)
