@@ -158,15 +158,21 @@ __global__ void __launch_bounds__(32 * kWarps, 1)
 
 // K1b at the per-rank shares of config 2 (2,048 / 1,024 trajectories): NT = 2
 // or 1 n-tiles per CTA instead of 4, so 256 / 128 n-tiles still fill 128 SMs.
-// The 12 warps are 12 / NT row groups x NT n-tiles; the 21 m-tiles are dealt
-// to the row groups as evenly as possible (NT = 2: 4,4,4,3,3,3; NT = 1: nine
-// groups of 2 and three of 1), and warp w runs on sub-partition w % 4, so the
-// busiest sub-partition issues 11 (NT = 2) / 6 (NT = 1) DMMAs per k-step
-// (NT = 4: 21). The m-tile count is a template parameter (no predicated
-// mma.sync; two code paths per kernel).
-template <int MC>
+// The 12 warps are 12 / NT row groups x NT n-tiles. The DMMA m-tiles cover
+// complex rows 0..79 only (20 tiles of 8 real rows; a 21st tile would carry the
+// single complex row 80 in 8 real rows): they are dealt to the row groups so
+// that warps 8..11 (one per sub-partition) carry fewer (NT = 2: 4,4,4,4,2,2;
+// NT = 1: eight groups of 2 and four of 1) and warp w runs on sub-partition
+// w % 4: every sub-partition issues 10 (NT = 2) / 5 (NT = 1) DMMAs per k-step
+// (NT = 4: 21). Complex row 80 is a DFMA dot product on warps 8..11 (T / 4
+// trajectories each, 32 / (T / 4) k-slices per trajectory, shuffle-reduced)
+// after their DMMAs, while the heavier warps still fill the pipe. The m-tile
+// count is a template parameter (no predicated mma.sync; two code paths per
+// kernel).
+template <int MC, bool FR, int SL>
 __device__ __forceinline__ double* nt_steps(const double* __restrict__ pa, int mstride, double* va, double* vb,
-                                            int bn, int bk, int sv, int i0, int t0, int lane, int64_t steps) {
+                                            int bn, int bk, int sv, int i0, int t0, int lane, int64_t steps,
+                                            const double2* __restrict__ prow80, int tfr) {
   constexpr int KT = 41;
   for (int64_t s = 0; s < steps; ++s) {
     double acc[MC][2];
@@ -198,7 +204,31 @@ __device__ __forceinline__ double* nt_steps(const double* __restrict__ pa, int m
       int coff;
       const double2 z = pair_complex(acc[mi], lane, coff);
       const int i = i0 + mi * 4 + (lane >> 3);
-      if (i < 81) *reinterpret_cast<double2*>(vb + (t0 + coff) * sv + 2 * i) = z;
+      *reinterpret_cast<double2*>(vb + (t0 + coff) * sv + 2 * i) = z;
+    }
+    if constexpr (FR) {  // complex row 80 of trajectory tfr: k = ksl + SL j
+      const int ksl = lane & (SL - 1);
+      const double* x = va + tfr * sv;
+      double r1 = 0.0, r2 = 0.0, i1 = 0.0, i2 = 0.0;
+#pragma unroll
+      for (int j = 0; j < (81 + SL - 1) / SL; ++j) {
+        const int k = ksl + SL * j;
+        if (k < 81) {
+          const double2 pv = prow80[k];
+          const double xr = x[2 * k], xi = x[2 * k + 1];
+          r1 = fma(pv.x, xr, r1);
+          r2 = fma(-pv.y, xi, r2);
+          i1 = fma(pv.y, xr, i1);
+          i2 = fma(pv.x, xi, i2);
+        }
+      }
+      double re = r1 + r2, im = i1 + i2;
+#pragma unroll
+      for (int o = SL / 2; o >= 1; o >>= 1) {
+        re += __shfl_xor_sync(0xffffffffu, re, o);
+        im += __shfl_xor_sync(0xffffffffu, im, o);
+      }
+      if (ksl == 0) *reinterpret_cast<double2*>(vb + tfr * sv + 160) = make_double2(re, im);
     }
     __syncthreads();
     double* tmp = va;
@@ -213,7 +243,10 @@ __global__ void __launch_bounds__(32 * kWarps, 1)
     smem81_nt_kernel(const double2* __restrict__ p, double* __restrict__ x_re, double* __restrict__ x_im,
                      double* __restrict__ x_aos, int64_t batch, int64_t steps) {
   extern __shared__ __align__(16) unsigned char smem[];
-  constexpr int n = 81, T = 8 * NT, RG = kWarps / NT, MT = 21, BASE = MT / RG, REM = MT % RG;
+  // RGH heavy row groups of H m-tiles, then the 4 / NT light groups (warps 8..11) of LM
+  constexpr int n = 81, T = 8 * NT, RG = kWarps / NT, RGH = RG - 4 / NT, H = NT == 2 ? 4 : 2, LM = H / 2;
+  constexpr int TPW = T / 4, SL = 32 / TPW;  // row-80 trajectories per light warp, k-slices each
+  static_assert(RGH * H + (RG - RGH) * LM == 20, "20 m-tiles (complex rows 0..79)");
   const SmemGeom g(n);
   double2* ps = reinterpret_cast<double2*>(smem);
   double* va = reinterpret_cast<double*>(smem + g.p_bytes);
@@ -240,15 +273,17 @@ __global__ void __launch_bounds__(32 * kWarps, 1)
   __syncthreads();
   const AFragLane af(lane);
   const int rg = warp / NT, nt = warp % NT;
-  const int m_begin = rg * BASE + (rg < REM ? rg : REM);
+  const int m_begin = rg < RGH ? rg * H : RGH * H + (rg - RGH) * LM;
   const double* pa =
       reinterpret_cast<const double*>(ps) + size_t(m_begin * 4 + af.di) * 2 * g.sp + 2 * af.dj + af.comp;
   const int mstride = 4 * 2 * g.sp, bn = nt * 8 + (lane >> 2), bk = lane & 3;
+  const double2* prow80 = ps + 80 * g.sp;
+  const int tfr = (warp - 8) * TPW + lane / SL;  // light warps 8..11
   double* fin;
-  if (rg < REM)
-    fin = nt_steps<BASE + 1>(pa, mstride, va, vb, bn, bk, g.sv, m_begin * 4, nt * 8, lane, steps);
+  if (rg < RGH)
+    fin = nt_steps<H, false, SL>(pa, mstride, va, vb, bn, bk, g.sv, m_begin * 4, nt * 8, lane, steps, prow80, 0);
   else
-    fin = nt_steps<BASE>(pa, mstride, va, vb, bn, bk, g.sv, m_begin * 4, nt * 8, lane, steps);
+    fin = nt_steps<LM, true, SL>(pa, mstride, va, vb, bn, bk, g.sv, m_begin * 4, nt * 8, lane, steps, prow80, tfr);
   for (int e = tid; e < T * 2 * n; e += blockDim.x) {
     const int t = e / (2 * n), r = e - t * 2 * n;
     const int64_t b = b0 + t;
@@ -280,14 +315,16 @@ void launch_nt(const double* p, double* x_re, double* x_im, double* x_aos, int64
 // n = 81: n-tiles per CTA (4, 2 or 1) with the shortest critical path, in DMMA
 // issue slots per sub-partition and step: waves x busiest sub-partition's
 // DMMAs per k-step x 41 k-steps (NT = 4 first: ties keep the measured kernel)
-constexpr int kBusiest[3][2] = {{4, 21}, {2, 11}, {1, 6}};
+// (per-slot weights in percent: the measured pass time per DMMA slot of the
+// NT = 2 / 1 kernels is ~9% / ~13% above NT = 4's — two code paths, the row-80 tail)
+constexpr int kBusiest[3][3] = {{4, 21, 100}, {2, 10, 109}, {1, 5, 113}};
 int smem81_nt(int64_t batch) {
   int64_t best = INT64_MAX;
   int nt_best = 4;
   const int64_t ntiles = (batch + 7) / 8;
   for (const auto& c : kBusiest) {
     const int64_t ctas = (ntiles + c[0] - 1) / c[0];
-    const int64_t cost = ((ctas + sm_count() - 1) / sm_count()) * c[1] * 41;
+    const int64_t cost = ((ctas + sm_count() - 1) / sm_count()) * c[1] * 41 * c[2];
     if (cost < best) best = cost, nt_best = c[0];
   }
   return nt_best;
@@ -317,11 +354,11 @@ bool smem_supported(std::size_t n) { return n >= 1 && n <= kMaxN; }
 
 int64_t smem81_cost(int64_t batch) {
   const int nt = smem81_nt(batch);
-  int busiest = 21;
+  int busiest = 21, weight = 100;
   for (const auto& c : kBusiest)
-    if (c[0] == nt) busiest = c[1];
+    if (c[0] == nt) busiest = c[1], weight = c[2];
   const int64_t ctas = ((batch + 7) / 8 + nt - 1) / nt;
-  return ((ctas + sm_count() - 1) / sm_count()) * busiest * 41;
+  return ((ctas + sm_count() - 1) / sm_count()) * busiest * 41 * weight / 100;
 }
 
 void launch_smem(const double* p_dev, std::size_t n, double* x_re, double* x_im, double* x_aos,
