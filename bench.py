@@ -627,7 +627,7 @@ def extra_configs(torch, lbg, R, peak):
     return out
 
 
-EXTRA_REF_SAMPLE = {0: 1, 2: 4096, 3: 128, 4: 512}
+EXTRA_REF_SAMPLE = {0: 1, 2: 4096, 3: 256, 4: 2048}  # ~1 s of host work each
 
 
 def cpu_reference_entry(cfg, gpu_rate):
