@@ -16,14 +16,18 @@
 // the complex one, and a step is n^2 real FMAs instead of 4 n^2.
 //
 // K4 (ptm_expm_kernel): one CTA per trajectory; A_R = dt L_R formed in shared
-//   memory from three precomputed affine terms (ptm_terms_kernel); Taylor in
-//   Paterson-Stockmeyer form with s = 3 (A2, A3, then Horner products in A3,
-//   no solve): degree 12 in 5 real matmuls for ||A||_1 <= 0.36
-//   (truncation <= 2.5e-16; config 4 sits at 0.327-0.342), degree 14 in 6 for
-//   ||A||_1 <= 0.53 (<= 2^-54), scaling and squaring above. Each 81 x 81
-//   product: 10 x 10 DMMA tiles over k < 80 plus a DFMA fringe (k = 80 and
-//   row / column 80), 8 warps in 5x3 / 5x2 tile blocks, A and A^2 kept at the
-//   lanes' own entries. Writes P_R (n x n) to global memory.
+//   memory from three precomputed affine terms (ptm_terms_kernel). Default
+//   (K4-S, when the generator's sparsity pattern fits the device-built plan,
+//   ptm_plan_kernel): Taylor degree 12 in Paterson-Stockmeyer form with s = 6
+//   — five sparse products A^k A on column-grouped DMMA tiles and ONE dense
+//   81 x 81 product; squarings above ||A||_1 = 0.36. Otherwise (dense
+//   generators, LBG_PTM_DENSE=1) s = 3: A2, A3, then Horner products in A3,
+//   no solve — degree 12 in 5 real matmuls for ||A||_1 <= 0.36 (truncation
+//   <= 2.5e-16; config 4 sits at 0.327-0.342), degree 14 in 6 for
+//   ||A||_1 <= 0.53 (<= 2^-54), scaling and squaring above. Each dense
+//   81 x 81 product: 10 x 10 DMMA tiles over k < 80 plus a DFMA fringe (k = 80
+//   and row / column 80), 8 warps in 5x3 / 5x2 tile blocks, A and A^2 kept at
+//   the lanes' own entries. Writes P_R (n x n) to global memory.
 // K3 (ptm_step_kernel): three trajectories per CTA; P_R register resident
 //   (a 4 x 21 block per thread), x in shared memory; per step 84 FMAs in 12
 //   chains, a 4-lane shuffle reduce-scatter, one barrier. The SM register file
@@ -31,6 +35,7 @@
 //   SM. Epilogue: populations + ensemble sum.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.hpp"
@@ -371,17 +376,368 @@ __device__ __forceinline__ void expm_body(double* SA, double* SA2, double* SA3, 
     if (fr.own[i]) out[fr.r[i] * N + fr.c[i]] = B.f[i];
 }
 
+// ---------------------------------------------------------------------------
+// Sparse-generator build (K4-S). A = dt L_R of a Lindbladian is sparse
+// (config 4: 544 of the 6,561 entries; C0 346, Cd 66, Cs 192), so a product
+// X A with X dense costs far less than 81^3. The degree-12 Taylor polynomial
+// is evaluated in Paterson-Stockmeyer form with s = 6:
+//     p(A) = B0 + A^6 (B1 + c12 A^6),   B0 = sum_{k<6} c_k A^k,
+//                                        B1 = sum_{k<6} c_{6+k} A^k,
+// i.e. five sparse products A^(k+1) = A^k A and ONE dense 81 x 81 product
+// (the DMMA routine of K4) against the five dense products of the s = 3 form.
+// ||A||_1 > 0.36 scales A by 2^-sq and squares sq times (dense products).
+//
+// Sparse product on the tensor pipe: the columns of A are grouped in eights
+// (greedy: each group starts at the unassigned column with most non-zeros and
+// adds the columns that grow the union of row indices least). Group J with
+// union rows K_J is one DMMA n-tile: (X A)[:, J] = X[:, K_J] A[K_J, J], a
+// dense 81 x |K_J| by |K_J| x 8 product whose B fragments (A's values) are
+// gathered once per trajectory and whose A fragments are X's columns K_J
+// read in place (each lane its own k). K_J is dealt into 4-tuples with
+// distinct residues mod 4 where it can be, which keeps the gathered fragment
+// loads free of bank conflicts (row stride 84 = 4 mod 16). Config 4: 11
+// groups, 72 k-steps, 720 DMMAs per product (dense: 2,000). Work items are
+// (group, half of the m-tiles): 5 DMMA chains per k-step sharing one B
+// fragment; row 80 is a DFMA dot product on the same fragments. The plan
+// depends only on the sparsity pattern of dt (C0, Cd, Cs); ptm_plan_kernel
+// builds it on the device once per call.
+constexpr int SP_C = 8;                          // columns per group (one n-tile)
+constexpr int SP_G = (N + SP_C - 1) / SP_C;      // 11 groups
+constexpr int SP_ITEMS = 2 * SP_G;               // (group, m-tile half)
+constexpr int SP_IW = 3;                         // items per warp (8 x 3 >= 22)
+constexpr int SP_MAXKS = 128;                    // capacity in k-steps (sum of ceil(|K_J| / 4))
+struct SparsePlan {
+  int use_sparse;
+  int total_ks;
+  int cols[SP_G][SP_C];              // -1 = padding column
+  int ks[SP_G], ksoff[SP_G];         // k-steps per group, offset
+  int kidx[SP_MAXKS * 4];            // row index k of A per (k-step, lane % 4); -1 = padding
+  int bcol[SP_MAXKS * SP_C];         // column of A per (k-step, lane / 4); -1 = padding
+  int wcount[EXPM_WARPS];
+  int witem[EXPM_WARPS][SP_IW];      // item = 2 * group + half
+};
+constexpr size_t kPlanBytes = (sizeof(SparsePlan) + 255) & ~size_t(255);
+
+// One warp: column masks of the union pattern of (dt C0, dt Cd, dt Cs),
+// greedy grouping, residue-dealt row lists, longest-first item assignment.
+// Deterministic (ties go to the lowest index).
+__global__ void __launch_bounds__(32) ptm_plan_kernel(const double* __restrict__ terms, int allow_sparse,
+                                                      SparsePlan* __restrict__ plan) {
+  __shared__ unsigned long long mlo[N], mhi[N];  // column j: bit k set if A[k][j] may be non-zero
+  __shared__ int assigned[N], nnz[N];
+  __shared__ int grp_cols[SP_G][SP_C];
+  const int lane = threadIdx.x;
+  for (int j = lane; j < N; j += 32) {
+    unsigned long long lo = 0, hi = 0;
+    for (int k = 0; k < N; ++k) {
+      const int e = k * RS + j;
+      if (terms[e] != 0.0 || terms[MAT + e] != 0.0 || terms[2 * MAT + e] != 0.0) {
+        if (k < 64) lo |= 1ull << k;
+        else hi |= 1ull << (k - 64);
+      }
+    }
+    mlo[j] = lo;
+    mhi[j] = hi;
+    nnz[j] = __popcll(lo) + __popcll(hi);
+    assigned[j] = 0;
+  }
+  __syncwarp();
+  constexpr long long kBig = 1ll << 40;
+  for (int g = 0; g < SP_G; ++g) {
+    unsigned long long ulo = 0, uhi = 0;
+    for (int c = 0; c < SP_C; ++c) {
+      long long best = kBig;
+      int bi = N;
+      for (int j = lane; j < N; j += 32) {
+        if (assigned[j]) continue;
+        const long long growth = __popcll(mlo[j] & ~ulo) + __popcll(mhi[j] & ~uhi);
+        const long long key = (c == 0 ? 0 : growth * 128) + (127 - nnz[j]);
+        if (key < best || (key == best && j < bi)) best = key, bi = j;
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const long long k2 = __shfl_xor_sync(0xffffffffu, best, o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (k2 < best || (k2 == best && i2 < bi)) best = k2, bi = i2;
+      }
+      if (bi < N) {
+        ulo |= mlo[bi];
+        uhi |= mhi[bi];
+      }
+      __syncwarp();
+      if (lane == 0) {
+        if (bi < N) assigned[bi] = 1;
+        grp_cols[g][c] = bi < N ? bi : -1;
+      }
+      __syncwarp();
+    }
+  }
+  if (lane != 0) return;
+  int off = 0;
+  bool fits = true;
+  for (int g = 0; g < SP_G; ++g) {
+    unsigned long long lo = 0, hi = 0;
+    for (int c = 0; c < SP_C; ++c) {
+      plan->cols[g][c] = grp_cols[g][c];
+      if (grp_cols[g][c] >= 0) lo |= mlo[grp_cols[g][c]], hi |= mhi[grp_cols[g][c]];
+    }
+    // bucket the union rows by residue mod 4, then deal 4-tuples largest buckets first
+    int bucket[4][24], bn[4] = {0, 0, 0, 0}, m = 0;
+    for (int k = 0; k < N; ++k)
+      if (k < 64 ? (lo >> k) & 1 : (hi >> (k - 64)) & 1) bucket[k & 3][bn[k & 3]++] = k, ++m;
+    const int ks = (m + 3) / 4;
+    plan->ks[g] = ks;
+    plan->ksoff[g] = off;
+    if (off + ks > SP_MAXKS) {
+      fits = false;
+      plan->ks[g] = 0;
+      continue;
+    }
+    int taken[4] = {0, 0, 0, 0};
+    for (int q = 0; q < ks; ++q) {
+      int tup[4] = {-1, -1, -1, -1}, used = 0;
+      bool have[4] = {false, false, false, false};
+      for (int pass = 0; pass < 2 && used < 4; ++pass)
+        for (int slot = 0; slot < 4 && used < 4; ++slot) {
+          int rb = -1;  // largest remaining bucket (distinct residues on pass 0)
+          for (int r = 0; r < 4; ++r)
+            if (taken[r] < bn[r] && (pass == 1 || !have[r]) && (rb < 0 || bn[r] - taken[r] > bn[rb] - taken[rb]))
+              rb = r;
+          if (rb < 0) break;
+          have[rb] = true;
+          tup[used++] = bucket[rb][taken[rb]++];
+        }
+      // lane t of the k-step reads row slotv[t]: each row at the slot of its residue when free
+      int slotv[4] = {-1, -1, -1, -1};
+      for (int i = 0; i < 4; ++i)
+        if (tup[i] >= 0 && slotv[tup[i] & 3] < 0) slotv[tup[i] & 3] = tup[i], tup[i] = -2;
+      for (int i = 0; i < 4; ++i)
+        if (tup[i] >= 0)
+          for (int t = 0; t < 4; ++t)
+            if (slotv[t] == -1) {
+              slotv[t] = tup[i];
+              break;
+            }
+      for (int t = 0; t < 4; ++t) plan->kidx[(off + q) * 4 + t] = slotv[t];
+      for (int c = 0; c < SP_C; ++c) plan->bcol[(off + q) * SP_C + c] = grp_cols[g][c];
+    }
+    off += ks;
+  }
+  plan->total_ks = off;
+  // longest-first assignment of the (group, half) items to the least loaded warp with a free slot
+  int load[EXPM_WARPS], cnt[EXPM_WARPS], done[SP_ITEMS];
+  for (int w = 0; w < EXPM_WARPS; ++w) load[w] = cnt[w] = 0;
+  for (int i = 0; i < SP_ITEMS; ++i) done[i] = 0;
+  for (int it = 0; it < SP_ITEMS; ++it) {
+    int best = -1;
+    for (int i = 0; i < SP_ITEMS; ++i)
+      if (!done[i] && (best < 0 || plan->ks[i >> 1] > plan->ks[best >> 1])) best = i;
+    done[best] = 1;
+    int w = -1;
+    for (int v = 0; v < EXPM_WARPS; ++v)
+      if (cnt[v] < SP_IW && (w < 0 || load[v] < load[w])) w = v;
+    plan->witem[w][cnt[w]++] = best;
+    load[w] += plan->ks[best >> 1] * 5 + ((best & 1) ? 0 : plan->ks[best >> 1]);  // + the row-80 dot
+  }
+  for (int w = 0; w < EXPM_WARPS; ++w) {
+    plan->wcount[w] = cnt[w];
+    for (int i = cnt[w]; i < SP_IW; ++i) plan->witem[w][i] = 0;
+  }
+  plan->use_sparse = allow_sparse && fits;
+}
+
+// Per-warp view of the plan (registers).
+struct WarpItems {
+  int cnt;
+  int g[SP_IW], half[SP_IW], ks[SP_IW], ksoff[SP_IW];
+};
+
+// One work item of Y = X A: group g's 8 columns for m-tiles 5 h .. 5 h + 4
+// (and row 80 when h == 0). BB = gathered B fragments [k-step][lane], KO = row
+// index per (k-step, lane % 4). acc[m] = the C fragment of m-tile 5 h + m;
+// f80 = the row-80 dot for column lane / 4 (reduced over the 4 lanes of the
+// column).
+__device__ __forceinline__ void sparse_item(const double* __restrict__ X, const double* __restrict__ bb,
+                                            const int* __restrict__ ko, int ks, int ksoff, int h, int lane,
+                                            double (&acc)[5][2], double& f80) {
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int m = 0; m < 5; ++m) acc[m][0] = acc[m][1] = 0.0;
+  double fa = 0.0, fb = 0.0;
+  const double* xa = X + (h * 40 + g) * RS;
+  const double* bq = bb + ksoff * 32 + lane;
+  const int* kq = ko + ksoff * 4 + t;
+#pragma unroll 2
+  for (int q = 0; q < ks; ++q) {
+    const double b = bq[q * 32];
+    const int kc = kq[q * 4];
+    double a[5];
+#pragma unroll
+    for (int m = 0; m < 5; ++m) a[m] = xa[m * 8 * RS + kc];
+#pragma unroll
+    for (int m = 0; m < 5; ++m) dmma(acc[m], a[m], b);
+    if (h == 0) {
+      const double x80 = X[80 * RS + kc];
+      if (q & 1)
+        fb = fma(x80, b, fb);
+      else
+        fa = fma(x80, b, fa);
+    }
+  }
+  double f = fa + fb;
+  f += __shfl_xor_sync(0xffffffffu, f, 1);
+  f += __shfl_xor_sync(0xffffffffu, f, 2);
+  f80 = f;
+}
+
+// K4-S body: A (scaled) dense in SA; SB, SC scratch; BB / KO the gathered
+// fragments. Leaves P's own entries (DMMA ownership) in B.acc / B.f, then
+// squarings and the global store as the dense body.
+template <int NB>
+__device__ __forceinline__ void expm_sparse_body(double* SA, double* SB, double* SC, const double* bb,
+                                                 const int* ko, const SparsePlan* __restrict__ plan,
+                                                 const WarpItems& wi, const Fringe& fr, int sq,
+                                                 double* __restrict__ out, int w, int lane) {
+  const double* cf = c_taylor.v;
+  const int g = lane >> 2, t = lane & 3;
+  int col[SP_IW][2], c80[SP_IW];  // output columns of the item (-1: none)
+#pragma unroll
+  for (int i = 0; i < SP_IW; ++i) {
+    const bool ok = i < wi.cnt;
+    col[i][0] = ok ? plan->cols[wi.g[i]][2 * t] : -1;
+    col[i][1] = ok ? plan->cols[wi.g[i]][2 * t + 1] : -1;
+    c80[i] = ok && wi.half[i] == 0 && t == 0 ? plan->cols[wi.g[i]][g] : -1;
+  }
+  // B0 = c0 I + c1 A, B1 = c6 I + c7 A at the sparse-product ownership
+  double b0[SP_IW][5][2], b1[SP_IW][5][2], f0[SP_IW], f1[SP_IW];
+#pragma unroll
+  for (int i = 0; i < SP_IW; ++i) {
+#pragma unroll
+    for (int m = 0; m < 5; ++m)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int r = wi.half[i] * 40 + m * 8 + g, cc = col[i][c];
+        const double a = cc >= 0 ? SA[r * RS + cc] : 0.0;
+        const double dg = r == cc ? 1.0 : 0.0;
+        b0[i][m][c] = fma(cf[1], a, cf[0] * dg);
+        b1[i][m][c] = fma(cf[7], a, cf[6] * dg);
+      }
+    const double a = c80[i] >= 0 ? SA[80 * RS + c80[i]] : 0.0;
+    const double dg = c80[i] == 80 ? 1.0 : 0.0;
+    f0[i] = fma(cf[1], a, cf[0] * dg);
+    f1[i] = fma(cf[7], a, cf[6] * dg);
+  }
+  const double* cur = SA;
+  double* nxt = SB;
+#pragma unroll 1
+  for (int p = 1; p <= 5; ++p) {  // X_{p+1} = X_p A; p = 5: X6 -> nxt, T1 = B1 + c12 X6 -> SC
+#pragma unroll
+    for (int i = 0; i < SP_IW; ++i) {
+      if (i >= wi.cnt) continue;
+      double acc[5][2], f80;
+      sparse_item(cur, bb, ko, wi.ks[i], wi.ksoff[i], wi.half[i], lane, acc, f80);
+#pragma unroll
+      for (int m = 0; m < 5; ++m)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int r = wi.half[i] * 40 + m * 8 + g, cc = col[i][c];
+          if (cc >= 0) {
+            const double x = acc[m][c];
+            nxt[r * RS + cc] = x;
+            if (p < 5) {
+              b0[i][m][c] = fma(cf[p + 1], x, b0[i][m][c]);
+              b1[i][m][c] = fma(cf[p + 7], x, b1[i][m][c]);
+            } else {
+              SC[r * RS + cc] = fma(cf[12], x, b1[i][m][c]);
+            }
+          }
+        }
+      if (c80[i] >= 0) {
+        nxt[80 * RS + c80[i]] = f80;
+        if (p < 5) {
+          f0[i] = fma(cf[p + 1], f80, f0[i]);
+          f1[i] = fma(cf[p + 7], f80, f1[i]);
+        } else {
+          SC[80 * RS + c80[i]] = fma(cf[12], f80, f1[i]);
+        }
+      }
+    }
+    bar_all();
+    cur = nxt;
+    nxt = cur == SA ? SB : SA;
+  }
+  // cur = X6, nxt = the X5 buffer (free): B0 there
+  double* sb0 = nxt;
+#pragma unroll
+  for (int i = 0; i < SP_IW; ++i) {
+    if (i >= wi.cnt) continue;
+#pragma unroll
+    for (int m = 0; m < 5; ++m)
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+        if (col[i][c] >= 0) sb0[(wi.half[i] * 40 + m * 8 + g) * RS + col[i][c]] = b0[i][m][c];
+    if (c80[i] >= 0) sb0[80 * RS + c80[i]] = f0[i];
+  }
+  bar_all();
+  Blk<NB> B;
+  mm<NB>(cur, SC, B, fr, w, lane);  // X6 (B1 + c12 X6)
+  {
+    const int n0 = blk_n0(w), m0 = blk_m0(w);
+#pragma unroll
+    for (int m = 0; m < EMT; ++m)
+#pragma unroll
+      for (int n = 0; n < NB; ++n) {
+        const double2 v = *reinterpret_cast<const double2*>(sb0 + ((m0 + m) * 8 + g) * RS + (n0 + n) * 8 + 2 * t);
+        B.acc[m][n][0] += v.x;
+        B.acc[m][n][1] += v.y;
+      }
+#pragma unroll
+    for (int i = 0; i < Blk<NB>::FR; ++i) B.f[i] += sb0[fr.r[i] * RS + fr.c[i]];
+  }
+  if (sq > 0) {
+    bar_all();  // everyone done reading X6, T1, B0
+    double* tcur = SA;
+    double* tnxt = SB;
+    store<NB>(tcur, B, fr, w, lane);
+    bar_all();
+    for (int i = 0; i < sq; ++i) {
+      mm<NB>(tcur, tcur, B, fr, w, lane);
+      if (i + 1 < sq) {
+        store<NB>(tnxt, B, fr, w, lane);
+        bar_all();
+        double* tt = tcur;
+        tcur = tnxt;
+        tnxt = tt;
+      }
+    }
+  }
+  const int n0 = blk_n0(w), m0 = blk_m0(w);
+#pragma unroll
+  for (int m = 0; m < EMT; ++m)
+#pragma unroll
+    for (int n = 0; n < NB; ++n) {
+      double* o = out + ((m0 + m) * 8 + g) * N + (n0 + n) * 8 + 2 * t;
+      o[0] = B.acc[m][n][0];
+      o[1] = B.acc[m][n][1];
+    }
+#pragma unroll
+  for (int i = 0; i < Blk<NB>::FR; ++i)
+    if (fr.own[i]) out[fr.r[i] * N + fr.c[i]] = B.f[i];
+}
+
 __global__ void __launch_bounds__(EXPM_THREADS, 1)
     ptm_expm_kernel(const double* __restrict__ terms, const double2* __restrict__ sp_val,
                     const int* __restrict__ sp_idx, const int* __restrict__ sp_count,
                     const double* __restrict__ delta, const double* __restrict__ scale,
-                    double* __restrict__ p_out) {
+                    const SparsePlan* __restrict__ plan, double* __restrict__ p_out) {
   extern __shared__ __align__(16) double sm[];
   double* SA = sm;
   double* SA2 = sm + MAT;
   double* SA3 = sm + 2 * MAT;
+  double* BB = sm + 3 * MAT;                                   // sparse path: SP_MAXKS x 32
+  int* KO = reinterpret_cast<int*>(BB + SP_MAXKS * 32);        // sparse path: SP_MAXKS x 4
   __shared__ double colpart[3][RS];
   __shared__ int s_sq, s_deg12;
+  const bool sparse = plan->use_sparse;
   __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int b = blockIdx.x;
@@ -433,7 +789,10 @@ __global__ void __launch_bounds__(EXPM_THREADS, 1)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) nrm = fmax(nrm, __shfl_xor_sync(0xffffffffu, nrm, o));
     if (lane == 0) {
-      s_sq = nrm > kTheta14 ? int(ceil(log2(nrm / kTheta14))) : 0;
+      if (sparse)  // degree 12 always (s = 6 form), squarings above 0.36
+        s_sq = nrm > kTheta12 ? int(ceil(log2(nrm / kTheta12))) : 0;
+      else
+        s_sq = nrm > kTheta14 ? int(ceil(log2(nrm / kTheta14))) : 0;
       s_deg12 = nrm <= kTheta12;
     }
   }
@@ -449,6 +808,32 @@ __global__ void __launch_bounds__(EXPM_THREADS, 1)
     __syncthreads();
   }
   double* out = p_out + size_t(b) * N * N;
+  if (sparse) {
+    // gathered B fragments of (scaled) A: BB[k-step][lane] = A[k(k-step, lane % 4)][col(group, lane / 4)]
+    const int tks = plan->total_ks;
+    for (int e = tid; e < tks * 32; e += EXPM_THREADS) {
+      const int q = e >> 5, l = e & 31;
+      const int k = plan->kidx[q * 4 + (l & 3)], c = plan->bcol[q * SP_C + (l >> 2)];
+      BB[e] = (k >= 0 && c >= 0) ? SA[k * RS + c] : 0.0;
+      if (l < 4) KO[q * 4 + l] = k >= 0 ? k : 0;
+    }
+    WarpItems wi;
+    wi.cnt = plan->wcount[w];
+#pragma unroll
+    for (int i = 0; i < SP_IW; ++i) {
+      const int it = plan->witem[w][i], gg = it >> 1;
+      wi.g[i] = gg;
+      wi.half[i] = it & 1;
+      wi.ks[i] = plan->ks[gg];
+      wi.ksoff[i] = plan->ksoff[gg];
+    }
+    __syncthreads();
+    if (w < 4)
+      expm_sparse_body<3>(SA, SA2, SA3, BB, KO, plan, wi, fr, sq, out, w, lane);
+    else
+      expm_sparse_body<2>(SA, SA2, SA3, BB, KO, plan, wi, fr, sq, out, w, lane);
+    return;
+  }
   if (w < 4)
     expm_body<3>(SA, SA2, SA3, fr, sq, deg12, out, w, lane);
   else
@@ -640,6 +1025,13 @@ __global__ void x_to_rho_kernel(const double* __restrict__ x, double2* __restric
     rho[p] = make_double2(x[j * D + i], -x[p]);
 }
 
+SparsePlan* plan_of(double* terms) {
+  return reinterpret_cast<SparsePlan*>(reinterpret_cast<char*>(terms) + ((kTermsBytes + 255) & ~size_t(255)));
+}
+constexpr size_t kTermsRegion = ((kTermsBytes + 255) & ~size_t(255)) + kPlanBytes;
+
+// dt C0 / dt Cd / dt Cs, their compacted sparse part, and the sparse-build plan
+// (LBG_PTM_DENSE=1 forces the dense s = 3 build; measurement / A-B only).
 void launch_terms(const double2* dis, const double* h0, const double* hd, const double* hs, double dt,
                   double* terms, cudaStream_t s) {
   ptm_terms_kernel<<<(MAT + 255) / 256, 256, 0, s>>>(dis, reinterpret_cast<const double2*>(h0),
@@ -649,13 +1041,17 @@ void launch_terms(const double2* dis, const double* h0, const double* hd, const 
   check_cuda(cudaMemsetAsync(sparse_terms(terms).count, 0, sizeof(int), s), "memset");
   ptm_sparse_kernel<<<(MAT + 255) / 256, 256, 0, s>>>(terms);
   LBG_CHECK_LAUNCH("ptm_sparse_kernel");
+  const char* dense = std::getenv("LBG_PTM_DENSE");
+  ptm_plan_kernel<<<1, 32, 0, s>>>(terms, !(dense && dense[0] == '1'), plan_of(terms));
+  LBG_CHECK_LAUNCH("ptm_plan_kernel");
 }
 void launch_expm(const double* terms, const double* delta, const double* scale, double* pr, int count,
                  cudaStream_t s) {
-  const size_t smem = size_t(3) * MAT * 8;
+  const size_t smem = size_t(3) * MAT * 8 + size_t(SP_MAXKS) * (32 * 8 + 4 * 4);
   ensure_max_dyn_smem((const void*)ptm_expm_kernel, int(smem));
   const SparseTerms sp = sparse_terms(const_cast<double*>(terms));
-  ptm_expm_kernel<<<count, EXPM_THREADS, smem, s>>>(terms, sp.val, sp.idx, sp.count, delta, scale, pr);
+  ptm_expm_kernel<<<count, EXPM_THREADS, smem, s>>>(terms, sp.val, sp.idx, sp.count, delta, scale,
+                                                    plan_of(const_cast<double*>(terms)), pr);
   LBG_CHECK_LAUNCH("ptm_expm_kernel");
 }
 
@@ -667,7 +1063,7 @@ constexpr int64_t kChunk = 16384;
 size_t ptm_sweep_workspace(int64_t batch) {
   const size_t chunk = size_t(std::min<int64_t>(std::max<int64_t>(batch, 1), kChunk));
   return align_up(chunk * N * N * 8) + align_up(size_t(N) * N * 16) + align_up(2 * N * 8) +
-         align_up(kTermsBytes) + 256;
+         kTermsRegion + 256;
 }
 
 bool ptm_sweep_supported(size_t d) { return d == size_t(D); }
@@ -707,7 +1103,7 @@ void launch_ptm_sweep(size_t d, const double* h0, const double* hd, const double
 bool ptm_grape_supported(size_t d) { return d == size_t(D); }
 
 size_t ptm_grape_workspace(int64_t segments) {
-  return align_up(size_t(segments) * N * N * 8) + align_up(size_t(N) * N * 16) + align_up(kTermsBytes) +
+  return align_up(size_t(segments) * N * N * 8) + align_up(size_t(N) * N * 16) + kTermsRegion +
          align_up(size_t(segments) * 8) + 256;
 }
 
@@ -723,7 +1119,7 @@ void launch_ptm_grape(const double* h0, const double* hc, const double* zero_h, 
   double* pr = reinterpret_cast<double*>(w);
   double2* dis = reinterpret_cast<double2*>(w + align_up(size_t(segments) * N * N * 8));
   double* terms = reinterpret_cast<double*>(reinterpret_cast<char*>(dis) + align_up(size_t(N) * N * 16));
-  double* zeros = reinterpret_cast<double*>(reinterpret_cast<char*>(terms) + align_up(kTermsBytes));
+  double* zeros = reinterpret_cast<double*>(reinterpret_cast<char*>(terms) + kTermsRegion);
   check_cuda(cudaMemsetAsync(zeros, 0, size_t(segments) * 8, s), "memset");
   launch_build_lindbladian(size_t(D), zero_h, n_ops, ops, reinterpret_cast<double*>(dis), s);
   launch_terms(dis, h0, hc, zero_h, dt, terms, s);

@@ -408,6 +408,73 @@ def test_sweep_real_expm_branches(lbg, torch, dt):
     assert tr <= TOL_INV and herm <= TOL_INV
 
 
+def _sweep_real(lbg, torch, h0, hd, hs, ops, delta, scale, dt, rho0, S, dense_build):
+    import os
+    dev = torch.device("cuda")
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    B = len(delta)
+    pops = torch.zeros(B, 9, dtype=torch.float64, device=dev)
+    ens = torch.zeros(9, 9, dtype=torch.complex128, device=dev)
+    work = torch.empty(lbg.sweep_workspace(9, B), dtype=torch.uint8, device=dev)
+    if dense_build:
+        os.environ["LBG_PTM_DENSE"] = "1"
+    try:
+        lbg.evolve_sweep_dev(T(h0), T(hd), T(hs), T(ops), T(delta), T(scale), dt, T(rho0), S, pops, ens, work,
+                             mode="real")
+        torch.cuda.synchronize()
+    finally:
+        os.environ.pop("LBG_PTM_DENSE", None)
+    return pops.cpu().numpy(), ens.cpu().numpy()
+
+
+@pytest.mark.parametrize("dt", [0.1, 0.12, 0.6])
+def test_sweep_sparse_build_matches_dense_build(lbg, torch, dt):
+    """K4-S (sparse generator: five column-grouped DMMA products A^k A and one
+    dense product, Paterson-Stockmeyer s = 6) against the dense s = 3 build:
+    ||A||_1 ~ 0.33 (no squaring), 0.41 (one squaring in the sparse form, degree
+    14 in the dense one) and 2.0 (squarings in both); ragged batch, Hermitian
+    rho0 with every entry populated."""
+    B, S = 301, 40
+    h0, hd, hs = lbg.config_sweep_terms()
+    _, ops = lbg.config_model(4)
+    delta, scale = lbg.sweep_params(11, B)
+    rng = np.random.default_rng(9)
+    g = rng.normal(size=(9, 9)) + 1j * rng.normal(size=(9, 9))
+    rho0 = g @ g.conj().T
+    rho0 = 0.5 * (rho0 + rho0.conj().T) / np.trace(rho0).real
+    ps, es = _sweep_real(lbg, torch, h0, hd, hs, ops, delta, scale, dt, rho0, S, False)
+    pd, ed = _sweep_real(lbg, torch, h0, hd, hs, ops, delta, scale, dt, rho0, S, True)
+    assert np.abs(ps - pd).max() <= 1e-12
+    assert np.abs(es - ed).max() <= 1e-12 * B
+    assert (ps != pd).any()  # different rounding: the sparse path did run
+
+
+def test_sweep_dense_generator_falls_back_to_dense_build(lbg, torch):
+    """A generator with no sparsity (dense random Hermitian h0) overflows the
+    sparse plan's k-step capacity; the build must take the dense path on the
+    device and still match the reference-form complex path."""
+    dev = torch.device("cuda")
+    B, S = 37, 25
+    rng = np.random.default_rng(3)
+    a = rng.normal(size=(9, 9)) + 1j * rng.normal(size=(9, 9))
+    h0 = 0.05 * (a + a.conj().T)
+    _, hd, hs = lbg.config_sweep_terms()
+    _, ops = lbg.config_model(4)
+    delta, scale = lbg.sweep_params(0, B)
+    rho0 = np.zeros((9, 9), complex)
+    rho0[0, 0] = 1.0
+    pr, er = _sweep_real(lbg, torch, h0, hd, hs, ops, delta, scale, 0.1, rho0, S, False)
+    T = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev)  # noqa: E731
+    pops = torch.zeros(B, 9, dtype=torch.float64, device=dev)
+    ens = torch.zeros(9, 9, dtype=torch.complex128, device=dev)
+    work = torch.empty(lbg.sweep_workspace(9, B), dtype=torch.uint8, device=dev)
+    lbg.evolve_sweep_dev(T(h0), T(hd), T(hs), T(ops), T(delta), T(scale), 0.1, T(rho0), S, pops, ens, work,
+                         mode="complex")
+    torch.cuda.synchronize()
+    assert np.abs(pr - pops.cpu().numpy()).max() <= TOL_RHO
+    assert np.abs(er - ens.cpu().numpy()).max() <= TOL_RHO * B
+
+
 def test_sweep_real_mode_rejects_non_hermitian(lbg, torch):
     dev = torch.device("cuda")
     h0, hd, hs = lbg.config_sweep_terms()
