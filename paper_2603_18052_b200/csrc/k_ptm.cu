@@ -418,80 +418,88 @@ struct SparsePlan {
 };
 constexpr size_t kPlanBytes = (sizeof(SparsePlan) + 255) & ~size_t(255);
 
-// One warp: column masks of the union pattern of (dt C0, dt Cd, dt Cs),
-// greedy grouping, residue-dealt row lists, longest-first item assignment.
+// Four warps build the column masks of the union pattern of (dt C0, dt Cd,
+// dt Cs) with ballots; warp 0 then does the greedy grouping, the
+// residue-dealt row lists and the longest-first item assignment.
 // Deterministic (ties go to the lowest index).
-__global__ void __launch_bounds__(32) ptm_plan_kernel(const double* __restrict__ terms, int allow_sparse,
-                                                      SparsePlan* __restrict__ plan) {
+constexpr int PLAN_THREADS = 128;
+__global__ void __launch_bounds__(PLAN_THREADS) ptm_plan_kernel(const double* __restrict__ terms, int allow_sparse,
+                                                                SparsePlan* __restrict__ plan) {
   __shared__ unsigned long long mlo[N], mhi[N];  // column j: bit k set if A[k][j] may be non-zero
-  __shared__ int assigned[N], nnz[N];
+  __shared__ int nnz[N];
   __shared__ int grp_cols[SP_G][SP_C];
-  const int lane = threadIdx.x;
-  for (int j = lane; j < N; j += 32) {
-    unsigned long long lo = 0, hi = 0;
-    for (int k = 0; k < N; ++k) {
-      const int e = k * RS + j;
-      if (terms[e] != 0.0 || terms[MAT + e] != 0.0 || terms[2 * MAT + e] != 0.0) {
-        if (k < 64) lo |= 1ull << k;
-        else hi |= 1ull << (k - 64);
-      }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int j = wid; j < N; j += PLAN_THREADS / 32) {
+    double v[3][3];  // all nine loads in flight, no short-circuit chains
+#pragma unroll
+    for (int h = 0; h < 3; ++h) {
+      const int e = min(lane + 32 * h, N - 1) * RS + j;
+      v[h][0] = terms[e];
+      v[h][1] = terms[MAT + e];
+      v[h][2] = terms[2 * MAT + e];
     }
-    mlo[j] = lo;
-    mhi[j] = hi;
-    nnz[j] = __popcll(lo) + __popcll(hi);
-    assigned[j] = 0;
+    unsigned bits[3];
+#pragma unroll
+    for (int h = 0; h < 3; ++h)
+      bits[h] = __ballot_sync(0xffffffffu, lane + 32 * h < N && ((v[h][0] != 0.0) | (v[h][1] != 0.0) | (v[h][2] != 0.0)));
+    if (lane == 0) {
+      mlo[j] = bits[0] | (static_cast<unsigned long long>(bits[1]) << 32);
+      mhi[j] = bits[2];
+      nnz[j] = __popc(bits[0]) + __popc(bits[1]) + __popc(bits[2]);
+    }
   }
-  __syncwarp();
-  constexpr long long kBig = 1ll << 40;
+  __syncthreads();
+  if (wid != 0) return;
+  // the lane's three candidate columns in registers; one packed 32-bit key per pick
+  // (union growth, then most non-zeros, then lowest index) reduced by redux.sync.min
+  unsigned long long clo[3], chi[3];
+  int cnz[3];
+  bool free_[3];
+#pragma unroll
+  for (int h = 0; h < 3; ++h) {
+    const int j = lane + 32 * h;
+    free_[h] = j < N;
+    clo[h] = j < N ? mlo[j] : 0;
+    chi[h] = j < N ? mhi[j] : 0;
+    cnz[h] = j < N ? nnz[j] : 0;
+  }
   for (int g = 0; g < SP_G; ++g) {
     unsigned long long ulo = 0, uhi = 0;
     for (int c = 0; c < SP_C; ++c) {
-      long long best = kBig;
-      int bi = N;
-      for (int j = lane; j < N; j += 32) {
-        if (assigned[j]) continue;
-        const long long growth = __popcll(mlo[j] & ~ulo) + __popcll(mhi[j] & ~uhi);
-        const long long key = (c == 0 ? 0 : growth * 128) + (127 - nnz[j]);
-        if (key < best || (key == best && j < bi)) best = key, bi = j;
-      }
-      for (int o = 16; o > 0; o >>= 1) {
-        const long long k2 = __shfl_xor_sync(0xffffffffu, best, o);
-        const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (k2 < best || (k2 == best && i2 < bi)) best = k2, bi = i2;
-      }
-      if (bi < N) {
+      unsigned key = 0xffffffffu;
+#pragma unroll
+      for (int h = 0; h < 3; ++h)
+        if (free_[h]) {
+          const unsigned growth = c == 0 ? 0u : unsigned(__popcll(clo[h] & ~ulo) + __popcll(chi[h] & ~uhi));
+          key = min(key, ((growth * 128u + unsigned(127 - cnz[h])) << 7) | unsigned(lane + 32 * h));
+        }
+      key = __reduce_min_sync(0xffffffffu, key);
+      const int bi = key == 0xffffffffu ? -1 : int(key & 127u);
+      if (bi >= 0) {
         ulo |= mlo[bi];
         uhi |= mhi[bi];
+#pragma unroll
+        for (int h = 0; h < 3; ++h)
+          if (lane + 32 * h == bi) free_[h] = false;
       }
-      __syncwarp();
-      if (lane == 0) {
-        if (bi < N) assigned[bi] = 1;
-        grp_cols[g][c] = bi < N ? bi : -1;
-      }
-      __syncwarp();
+      if (lane == 0) grp_cols[g][c] = bi;
     }
   }
-  if (lane != 0) return;
-  int off = 0;
-  bool fits = true;
-  for (int g = 0; g < SP_G; ++g) {
+  __syncwarp();
+  // lane g < SP_G: its group's union rows, dealt into 4-tuples (largest residue buckets first)
+  __shared__ int s_ks[SP_G], s_off[SP_G], s_tup[SP_G][24][4], s_bucket[SP_G][4][24];
+  __shared__ int s_fits;
+  if (lane < SP_G) {
+    const int g = lane;
     unsigned long long lo = 0, hi = 0;
-    for (int c = 0; c < SP_C; ++c) {
-      plan->cols[g][c] = grp_cols[g][c];
+    for (int c = 0; c < SP_C; ++c)
       if (grp_cols[g][c] >= 0) lo |= mlo[grp_cols[g][c]], hi |= mhi[grp_cols[g][c]];
-    }
-    // bucket the union rows by residue mod 4, then deal 4-tuples largest buckets first
-    int bucket[4][24], bn[4] = {0, 0, 0, 0}, m = 0;
+    int(*bucket)[24] = s_bucket[g];
+    int bn[4] = {0, 0, 0, 0}, m = 0;
     for (int k = 0; k < N; ++k)
       if (k < 64 ? (lo >> k) & 1 : (hi >> (k - 64)) & 1) bucket[k & 3][bn[k & 3]++] = k, ++m;
-    const int ks = (m + 3) / 4;
-    plan->ks[g] = ks;
-    plan->ksoff[g] = off;
-    if (off + ks > SP_MAXKS) {
-      fits = false;
-      plan->ks[g] = 0;
-      continue;
-    }
+    const int ks = (m + 3) / 4;  // <= 21
+    s_ks[g] = ks;
     int taken[4] = {0, 0, 0, 0};
     for (int q = 0; q < ks; ++q) {
       int tup[4] = {-1, -1, -1, -1}, used = 0;
@@ -517,32 +525,61 @@ __global__ void __launch_bounds__(32) ptm_plan_kernel(const double* __restrict__
               slotv[t] = tup[i];
               break;
             }
-      for (int t = 0; t < 4; ++t) plan->kidx[(off + q) * 4 + t] = slotv[t];
-      for (int c = 0; c < SP_C; ++c) plan->bcol[(off + q) * SP_C + c] = grp_cols[g][c];
+      for (int t = 0; t < 4; ++t) s_tup[g][q][t] = slotv[t];
     }
-    off += ks;
   }
-  plan->total_ks = off;
-  // longest-first assignment of the (group, half) items to the least loaded warp with a free slot
-  int load[EXPM_WARPS], cnt[EXPM_WARPS], done[SP_ITEMS];
-  for (int w = 0; w < EXPM_WARPS; ++w) load[w] = cnt[w] = 0;
-  for (int i = 0; i < SP_ITEMS; ++i) done[i] = 0;
-  for (int it = 0; it < SP_ITEMS; ++it) {
-    int best = -1;
-    for (int i = 0; i < SP_ITEMS; ++i)
-      if (!done[i] && (best < 0 || plan->ks[i >> 1] > plan->ks[best >> 1])) best = i;
-    done[best] = 1;
-    int w = -1;
-    for (int v = 0; v < EXPM_WARPS; ++v)
-      if (cnt[v] < SP_IW && (w < 0 || load[v] < load[w])) w = v;
-    plan->witem[w][cnt[w]++] = best;
-    load[w] += plan->ks[best >> 1] * 5 + ((best & 1) ? 0 : plan->ks[best >> 1]);  // + the row-80 dot
+  __syncwarp();
+  if (lane == 0) {
+    int off = 0;
+    for (int g = 0; g < SP_G; ++g) {
+      s_off[g] = off;
+      off += s_ks[g];
+    }
+    s_fits = off <= SP_MAXKS;
+    plan->total_ks = s_fits ? off : 0;
+    // longest-first assignment of the (group, half) items to the least loaded warp with a
+    // free slot (register arrays: every index below is an unrolled loop variable)
+    int load[EXPM_WARPS], cnt[EXPM_WARPS];
+#pragma unroll
+    for (int w = 0; w < EXPM_WARPS; ++w) load[w] = cnt[w] = 0;
+    unsigned done = 0;
+    for (int it = 0; it < SP_ITEMS; ++it) {
+      int best = -1, bk = -1;
+#pragma unroll
+      for (int i = 0; i < SP_ITEMS; ++i) {
+        const int k = s_ks[i >> 1];
+        if (!((done >> i) & 1) && k > bk) best = i, bk = k;
+      }
+      done |= 1u << best;
+      int w = -1, wl = 0;
+#pragma unroll
+      for (int v = 0; v < EXPM_WARPS; ++v)
+        if (cnt[v] < SP_IW && (w < 0 || load[v] < wl)) w = v, wl = load[v];
+      const int add = bk * 5 + ((best & 1) ? 0 : bk);  // + the row-80 dot
+#pragma unroll
+      for (int v = 0; v < EXPM_WARPS; ++v)
+        if (v == w) {
+          plan->witem[v][cnt[v]] = best;
+          load[v] += add;
+          ++cnt[v];
+        }
+    }
+#pragma unroll
+    for (int w = 0; w < EXPM_WARPS; ++w) {
+      plan->wcount[w] = cnt[w];
+      for (int i = cnt[w]; i < SP_IW; ++i) plan->witem[w][i] = 0;
+    }
+    plan->use_sparse = allow_sparse && s_fits;
   }
-  for (int w = 0; w < EXPM_WARPS; ++w) {
-    plan->wcount[w] = cnt[w];
-    for (int i = cnt[w]; i < SP_IW; ++i) plan->witem[w][i] = 0;
+  __syncwarp();
+  if (!s_fits) return;
+  for (int g = 0; g < SP_G; ++g) {  // the lists, written by the whole warp
+    const int ks = s_ks[g], off = s_off[g];
+    if (lane < SP_C) plan->cols[g][lane] = grp_cols[g][lane];
+    if (lane == 0) plan->ks[g] = ks, plan->ksoff[g] = off;
+    for (int e = lane; e < ks * 4; e += 32) plan->kidx[off * 4 + e] = s_tup[g][e >> 2][e & 3];
+    for (int e = lane; e < ks * SP_C; e += 32) plan->bcol[off * SP_C + e] = grp_cols[g][e % SP_C];
   }
-  plan->use_sparse = allow_sparse && fits;
 }
 
 // Per-warp view of the plan (registers).
@@ -1029,11 +1066,12 @@ SparsePlan* plan_of(double* terms) {
   return reinterpret_cast<SparsePlan*>(reinterpret_cast<char*>(terms) + ((kTermsBytes + 255) & ~size_t(255)));
 }
 constexpr size_t kTermsRegion = ((kTermsBytes + 255) & ~size_t(255)) + kPlanBytes;
+constexpr int64_t kPlanMinBatch = 1024;
 
 // dt C0 / dt Cd / dt Cs, their compacted sparse part, and the sparse-build plan
 // (LBG_PTM_DENSE=1 forces the dense s = 3 build; measurement / A-B only).
 void launch_terms(const double2* dis, const double* h0, const double* hd, const double* hs, double dt,
-                  double* terms, cudaStream_t s) {
+                  double* terms, int64_t count, cudaStream_t s) {
   ptm_terms_kernel<<<(MAT + 255) / 256, 256, 0, s>>>(dis, reinterpret_cast<const double2*>(h0),
                                                      reinterpret_cast<const double2*>(hd),
                                                      reinterpret_cast<const double2*>(hs), dt, terms);
@@ -1041,9 +1079,15 @@ void launch_terms(const double2* dis, const double* h0, const double* hd, const 
   check_cuda(cudaMemsetAsync(sparse_terms(terms).count, 0, sizeof(int), s), "memset");
   ptm_sparse_kernel<<<(MAT + 255) / 256, 256, 0, s>>>(terms);
   LBG_CHECK_LAUNCH("ptm_sparse_kernel");
+  // The plan (~0.1 ms, one CTA) pays off over thousands of propagators; short
+  // batches (GRAPE segments, small sweeps) take the dense build.
   const char* dense = std::getenv("LBG_PTM_DENSE");
-  ptm_plan_kernel<<<1, 32, 0, s>>>(terms, !(dense && dense[0] == '1'), plan_of(terms));
-  LBG_CHECK_LAUNCH("ptm_plan_kernel");
+  if (count >= kPlanMinBatch && !(dense && dense[0] == '1')) {
+    ptm_plan_kernel<<<1, PLAN_THREADS, 0, s>>>(terms, 1, plan_of(terms));
+    LBG_CHECK_LAUNCH("ptm_plan_kernel");
+  } else {
+    check_cuda(cudaMemsetAsync(plan_of(terms), 0, sizeof(int), s), "memset");  // use_sparse = 0
+  }
 }
 void launch_expm(const double* terms, const double* delta, const double* scale, double* pr, int count,
                  cudaStream_t s) {
@@ -1086,7 +1130,7 @@ void launch_ptm_sweep(size_t d, const double* h0, const double* hd, const double
   check_cuda(cudaMemsetAsync(ens_x, 0, N * 8, s), "memset");
   check_cuda(cudaMemsetAsync(pr, 0, d * d * 16, s), "memset");
   launch_build_lindbladian(d, pr, n_ops, ops, reinterpret_cast<double*>(dis), s);
-  launch_terms(dis, h0, hd, hs, dt, terms, s);
+  launch_terms(dis, h0, hd, hs, dt, terms, batch, s);
   rho_to_x_kernel<<<1, 96, 0, s>>>(reinterpret_cast<const double2*>(rho0), x0);
   LBG_CHECK_LAUNCH("rho_to_x_kernel");
   for (int64_t c0 = 0; c0 < batch; c0 += int64_t(chunk)) {
@@ -1122,7 +1166,7 @@ void launch_ptm_grape(const double* h0, const double* hc, const double* zero_h, 
   double* zeros = reinterpret_cast<double*>(reinterpret_cast<char*>(terms) + kTermsRegion);
   check_cuda(cudaMemsetAsync(zeros, 0, size_t(segments) * 8, s), "memset");
   launch_build_lindbladian(size_t(D), zero_h, n_ops, ops, reinterpret_cast<double*>(dis), s);
-  launch_terms(dis, h0, hc, zero_h, dt, terms, s);
+  launch_terms(dis, h0, hc, zero_h, dt, terms, segments, s);
   launch_expm(terms, amps, zeros, pr, int(segments), s);
   if (ev_build_end) check_cuda(cudaEventRecord(ev_build_end, s), "event");
   ptm_chain_kernel<<<1, CH_THREADS, 0, s>>>(pr, segments, sps, reinterpret_cast<double2*>(rho));

@@ -433,8 +433,9 @@ def test_sweep_sparse_build_matches_dense_build(lbg, torch, dt):
     dense product, Paterson-Stockmeyer s = 6) against the dense s = 3 build:
     ||A||_1 ~ 0.33 (no squaring), 0.41 (one squaring in the sparse form, degree
     14 in the dense one) and 2.0 (squarings in both); ragged batch, Hermitian
-    rho0 with every entry populated."""
-    B, S = 301, 40
+    rho0 with every entry populated. The batch is past the plan threshold
+    (1,024) and not a multiple of the 3 trajectories per step CTA."""
+    B, S = 1100, 40
     h0, hd, hs = lbg.config_sweep_terms()
     _, ops = lbg.config_model(4)
     delta, scale = lbg.sweep_params(11, B)
@@ -454,7 +455,7 @@ def test_sweep_dense_generator_falls_back_to_dense_build(lbg, torch):
     sparse plan's k-step capacity; the build must take the dense path on the
     device and still match the reference-form complex path."""
     dev = torch.device("cuda")
-    B, S = 37, 25
+    B, S = 1030, 25
     rng = np.random.default_rng(3)
     a = rng.normal(size=(9, 9)) + 1j * rng.normal(size=(9, 9))
     h0 = 0.05 * (a + a.conj().T)
