@@ -413,6 +413,7 @@ struct SparsePlan {
   int ks[SP_G], ksoff[SP_G];         // k-steps per group, offset
   int kidx[SP_MAXKS * 4];            // row index k of A per (k-step, lane % 4); -1 = padding
   int bcol[SP_MAXKS * SP_C];         // column of A per (k-step, lane / 4); -1 = padding
+  int boff[SP_MAXKS * 32];           // shared-memory offset k * RS + col of each B-fragment value; -1 = zero
   int wcount[EXPM_WARPS];
   int witem[EXPM_WARPS][SP_IW];      // item = 2 * group + half
 };
@@ -579,6 +580,10 @@ __global__ void __launch_bounds__(PLAN_THREADS) ptm_plan_kernel(const double* __
     if (lane == 0) plan->ks[g] = ks, plan->ksoff[g] = off;
     for (int e = lane; e < ks * 4; e += 32) plan->kidx[off * 4 + e] = s_tup[g][e >> 2][e & 3];
     for (int e = lane; e < ks * SP_C; e += 32) plan->bcol[off * SP_C + e] = grp_cols[g][e % SP_C];
+    for (int e = lane; e < ks * 32; e += 32) {  // e = k-step * 32 + fragment lane
+      const int k = s_tup[g][e >> 5][e & 3], c = grp_cols[g][(e & 31) >> 2];
+      plan->boff[off * 32 + e] = (k >= 0 && c >= 0) ? k * RS + c : -1;
+    }
   }
 }
 
@@ -672,6 +677,30 @@ __device__ __forceinline__ void expm_sparse_body(double* SA, double* SB, double*
       if (i >= wi.cnt) continue;
       double acc[5][2], f80;
       sparse_item(cur, bb, ko, wi.ks[i], wi.ksoff[i], wi.half[i], lane, acc, f80);
+      if (i == 0 && p >= 2) {
+        // B0 += c_p X_p, B1 += c_{p+6} X_p from this product's INPUT (complete since the
+        // barrier): independent of the DMMAs in flight, so it fills their latency instead of
+        // waiting on their results in the epilogue
+        const double ca = cf[p], cb = cf[p + 6];
+#pragma unroll
+        for (int j = 0; j < SP_IW; ++j) {
+          if (j >= wi.cnt) continue;
+#pragma unroll
+          for (int m = 0; m < 5; ++m)
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+              if (col[j][c] >= 0) {
+                const double x = cur[(wi.half[j] * 40 + m * 8 + g) * RS + col[j][c]];
+                b0[j][m][c] = fma(ca, x, b0[j][m][c]);
+                b1[j][m][c] = fma(cb, x, b1[j][m][c]);
+              }
+          if (c80[j] >= 0) {
+            const double x = cur[80 * RS + c80[j]];
+            f0[j] = fma(ca, x, f0[j]);
+            f1[j] = fma(cb, x, f1[j]);
+          }
+        }
+      }
 #pragma unroll
       for (int m = 0; m < 5; ++m)
 #pragma unroll
@@ -680,22 +709,12 @@ __device__ __forceinline__ void expm_sparse_body(double* SA, double* SB, double*
           if (cc >= 0) {
             const double x = acc[m][c];
             nxt[r * RS + cc] = x;
-            if (p < 5) {
-              b0[i][m][c] = fma(cf[p + 1], x, b0[i][m][c]);
-              b1[i][m][c] = fma(cf[p + 7], x, b1[i][m][c]);
-            } else {
-              SC[r * RS + cc] = fma(cf[12], x, b1[i][m][c]);
-            }
+            if (p == 5) SC[r * RS + cc] = fma(cf[12], x, b1[i][m][c]);
           }
         }
       if (c80[i] >= 0) {
         nxt[80 * RS + c80[i]] = f80;
-        if (p < 5) {
-          f0[i] = fma(cf[p + 1], f80, f0[i]);
-          f1[i] = fma(cf[p + 7], f80, f1[i]);
-        } else {
-          SC[80 * RS + c80[i]] = fma(cf[12], f80, f1[i]);
-        }
+        if (p == 5) SC[80 * RS + c80[i]] = fma(cf[12], f80, f1[i]);
       }
     }
     bar_all();
@@ -849,11 +868,10 @@ __global__ void __launch_bounds__(EXPM_THREADS, 1)
     // gathered B fragments of (scaled) A: BB[k-step][lane] = A[k(k-step, lane % 4)][col(group, lane / 4)]
     const int tks = plan->total_ks;
     for (int e = tid; e < tks * 32; e += EXPM_THREADS) {
-      const int q = e >> 5, l = e & 31;
-      const int k = plan->kidx[q * 4 + (l & 3)], c = plan->bcol[q * SP_C + (l >> 2)];
-      BB[e] = (k >= 0 && c >= 0) ? SA[k * RS + c] : 0.0;
-      if (l < 4) KO[q * 4 + l] = k >= 0 ? k : 0;
+      const int o = plan->boff[e];
+      BB[e] = o >= 0 ? SA[o] : 0.0;
     }
+    for (int e = tid; e < tks * 4; e += EXPM_THREADS) KO[e] = max(plan->kidx[e], 0);
     WarpItems wi;
     wi.cnt = plan->wcount[w];
 #pragma unroll
