@@ -538,37 +538,55 @@ __global__ void __launch_bounds__(PLAN_THREADS) ptm_plan_kernel(const double* __
     }
     s_fits = off <= SP_MAXKS;
     plan->total_ks = s_fits ? off : 0;
-    // longest-first assignment of the (group, half) items to the least loaded warp with a
-    // free slot (register arrays: every index below is an unrolled loop variable)
-    int load[EXPM_WARPS], cnt[EXPM_WARPS];
+    // Longest-first assignment of the (group, half) items, first to the SM sub-partitions
+    // (warps q and q + 4 share sub-partition q and its FP64 pipe; <= 2 SP_IW items each),
+    // then within a sub-partition to its two warps (<= SP_IW each). Cost in half-DMMAs:
+    // 10 per k-step, + 1 per k-step for the row-80 DFMA dot of the upper half.
+    // (Balancing the 8 warps directly left the sub-partitions 1.09 apart at config 4.)
+    int sload[4], scnt[4], sit[4][2 * SP_IW];
 #pragma unroll
-    for (int w = 0; w < EXPM_WARPS; ++w) load[w] = cnt[w] = 0;
+    for (int q = 0; q < 4; ++q) sload[q] = scnt[q] = 0;
     unsigned done = 0;
     for (int it = 0; it < SP_ITEMS; ++it) {
-      int best = -1, bk = -1;
+      int best = -1, bc = -1;
 #pragma unroll
       for (int i = 0; i < SP_ITEMS; ++i) {
-        const int k = s_ks[i >> 1];
-        if (!((done >> i) & 1) && k > bk) best = i, bk = k;
+        const int c = s_ks[i >> 1] * 10 + ((i & 1) ? 0 : s_ks[i >> 1]);
+        if (!((done >> i) & 1) && c > bc) best = i, bc = c;
       }
       done |= 1u << best;
-      int w = -1, wl = 0;
+      int qq = -1, ql = 0;
 #pragma unroll
-      for (int v = 0; v < EXPM_WARPS; ++v)
-        if (cnt[v] < SP_IW && (w < 0 || load[v] < wl)) w = v, wl = load[v];
-      const int add = bk * 5 + ((best & 1) ? 0 : bk);  // + the row-80 dot
+      for (int q = 0; q < 4; ++q)
+        if (scnt[q] < 2 * SP_IW && (qq < 0 || sload[q] < ql)) qq = q, ql = sload[q];
 #pragma unroll
-      for (int v = 0; v < EXPM_WARPS; ++v)
-        if (v == w) {
-          plan->witem[v][cnt[v]] = best;
-          load[v] += add;
-          ++cnt[v];
+      for (int q = 0; q < 4; ++q)
+        if (q == qq) {
+#pragma unroll
+          for (int j = 0; j < 2 * SP_IW; ++j)
+            if (j == scnt[q]) sit[q][j] = best;
+          sload[q] += bc;
+          ++scnt[q];
         }
     }
 #pragma unroll
-    for (int w = 0; w < EXPM_WARPS; ++w) {
-      plan->wcount[w] = cnt[w];
-      for (int i = cnt[w]; i < SP_IW; ++i) plan->witem[w][i] = 0;
+    for (int q = 0; q < 4; ++q) {  // items arrive longest first: LPT onto warps q, q + 4
+      int wl[2] = {0, 0}, wc[2] = {0, 0};
+#pragma unroll
+      for (int j = 0; j < 2 * SP_IW; ++j) {
+        if (j >= scnt[q]) continue;
+        const int i = sit[q][j];
+        const int c = s_ks[i >> 1] * 10 + ((i & 1) ? 0 : s_ks[i >> 1]);
+        const int v = (wc[0] < SP_IW && (wc[1] >= SP_IW || wl[0] <= wl[1])) ? 0 : 1;
+        plan->witem[q + 4 * v][wc[v]] = i;
+        wl[v] += c;
+        ++wc[v];
+      }
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        plan->wcount[q + 4 * v] = wc[v];
+        for (int i = wc[v]; i < SP_IW; ++i) plan->witem[q + 4 * v][i] = 0;
+      }
     }
     plan->use_sparse = allow_sparse && s_fits;
   }
