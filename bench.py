@@ -466,19 +466,19 @@ def run_ours(args):
         torch.cuda.synchronize(dev)
         want = xr.cpu().numpy().reshape(b, d, d)
         with Clocks(local) as eclk:  # clocks during the host-buffer calls too
-            med, calls, h2d, d2h, diff = host_call_e2e(torch, lbg, P, rho0, S, want, True, 21)
-        med_pg, calls_pg, _, _, diff_pg = host_call_e2e(torch, lbg, P, rho0, S, want, False, 5)
+            med, calls, h2d, d2h, diff = host_call_e2e(torch, lbg, P, rho0, S, want, True, 41)
+        med_pg, calls_pg, _, _, diff_pg = host_call_e2e(torch, lbg, P, rho0, S, want, False, 11)
         e2e_s = max_over_ranks(torch, med)
         e2e_pg = max_over_ranks(torch, med_pg)
         e2e = {"value": gb * S / e2e_s, "unit": "traj-steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_call": e2e_s * 1e3, "ms_per_call_all": [round(c * 1e3, 3) for c in calls],
-               "call": "lbg_evolve_shared_p (pinned host buffers, synchronous); median of 21 (the shared box throws occasional 35-100 ms calls)",
+               "call": "lbg_evolve_shared_p (pinned host buffers, synchronous); median of 41 (the box throws bursts of 35-125 ms calls, with or without the nvidia-smi sampler: tools/e2e_bursts.py measured 1-5 per 40 calls either way)",
                "max_abs_diff_vs_device": diff, "clocks": eclk.summary(),
                "pageable": {"value": gb * S / e2e_pg, "ms_per_call": e2e_pg * 1e3,
                             "ms_per_call_all": [round(c * 1e3, 3) for c in calls_pg],
                             "max_abs_diff_vs_device": diff_pg,
                             "call": "lbg_evolve_shared_p from pageable buffers (lb::MatrixAoS storage): "
-                                    "staged through the pool's pinned buffers; median of 5"}}
+                                    "staged through the pool's pinned buffers; median of 11"}}
     else:
         e2e = sweep.e2e(reps=2)
         e2e["value"] = gb * S / max_over_ranks(torch, e2e["ms_per_call"] * 1e-3)
