@@ -598,19 +598,26 @@ int lbg_evolve_sweep_dev(size_t d, const double* h0, const double* hd, const dou
     if (!work) throw invalid_argument("sweep: workspace required");
     cudaStream_t s = as_stream(stream);
     if (batch == 0) return;
+    bool real = false;
+    if (mode != LBG_SWEEP_REAL && mode != LBG_SWEEP_AUTO && mode != LBG_SWEEP_COMPLEX)
+      throw invalid_argument("sweep: unknown mode");
     {  // propagate.cpp:79-80: lb::evolve validates rho0 before any work (K6), and
        // lb::expm rejects a non-finite generator (expm.cpp:110-112): the model
-       // terms and every (delta, s) are checked for NaN / Inf; one 32-byte D2H
+       // terms and every (delta, s) are checked for NaN / Inf; the real form also
+       // needs an exactly Hermitian rho0. One 32-byte D2H and one sync for all of it.
       double* dchk = nullptr;
       check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&dchk), 4 * sizeof(double), s), "malloc check");
-      unsigned* flag = reinterpret_cast<unsigned*>(dchk + 3);
-      check_cuda(cudaMemsetAsync(flag, 0, sizeof(unsigned), s), "memset");
+      unsigned* flag = reinterpret_cast<unsigned*>(dchk + 3);  // [0] non-finite, [1] not Hermitian
+      check_cuda(cudaMemsetAsync(flag, 0, 2 * sizeof(unsigned), s), "memset");
       launch_check_state(rho0, d, 1, dchk, s);
       const long long dd = (long long)(2 * d * d);
       for (const double* m : {h0, hd, hs}) launch_flag_nonfinite(m, dd, flag, s);
       launch_flag_nonfinite(ops, dd * (long long)n_ops, flag, s);
       launch_flag_nonfinite(delta, batch, flag, s);
       launch_flag_nonfinite(scale, batch, flag, s);
+      const bool want_real = (mode == LBG_SWEEP_REAL || mode == LBG_SWEEP_AUTO) &&
+                             (ptm_sweep_supported(d) || ptm_small_supported(d));
+      if (want_real) launch_flag_nonhermitian(rho0, (long long)d, flag + 1, s);
       double chk[4];
       const cudaError_t e1 = cudaMemcpyAsync(chk, dchk, sizeof chk, cudaMemcpyDeviceToHost, s);
       const cudaError_t e2 = cudaFreeAsync(dchk, s);
@@ -619,28 +626,13 @@ int lbg_evolve_sweep_dev(size_t d, const double* h0, const double* hd, const dou
       check_cuda(cudaStreamSynchronize(s), "sync check");
       if (!(chk[0] <= 1e-8 && chk[1] <= 1e-8 && chk[2] >= -1e-8))
         throw invalid_argument("evolve: initial state fails physical-state checks");
-      unsigned bad;
-      std::memcpy(&bad, &chk[3], sizeof bad);
-      if (bad) throw invalid_argument("sweep: non-finite entries in the model terms or sweep parameters");
-    }
-    bool real = false;
-    if (mode == LBG_SWEEP_REAL || mode == LBG_SWEEP_AUTO) {
-      bool herm = false;
-      if (ptm_sweep_supported(d) || ptm_small_supported(d)) {  // the real form needs an exactly Hermitian rho0
-        std::vector<double> r(2 * d * d);
-        check_cuda(cudaMemcpyAsync(r.data(), rho0, r.size() * 8, cudaMemcpyDeviceToHost, s), "D2H rho0");
-        check_cuda(cudaStreamSynchronize(s), "sync");
-        herm = true;
-        for (size_t i = 0; i < d; ++i)
-          for (size_t j = 0; j < d; ++j)
-            herm = herm && r[2 * (i * d + j)] == r[2 * (j * d + i)] &&
-                   r[2 * (i * d + j) + 1] == -r[2 * (j * d + i) + 1];
-      }
+      unsigned flags[2];
+      std::memcpy(flags, &chk[3], sizeof flags);
+      if (flags[0]) throw invalid_argument("sweep: non-finite entries in the model terms or sweep parameters");
+      const bool herm = want_real && flags[1] == 0;
       if (mode == LBG_SWEEP_REAL && !herm)
         throw invalid_argument("sweep: real mode needs d in {2, 3, 9} and an exactly Hermitian rho0");
-      real = herm;
-    } else if (mode != LBG_SWEEP_COMPLEX) {
-      throw invalid_argument("sweep: unknown mode");
+      real = herm && mode != LBG_SWEEP_COMPLEX;
     }
     if (real && ptm_small_supported(d))
       launch_ptm_sweep_small(d, h0, hd, hs, n_ops, ops, delta, scale, dt, rho0, batch, steps, pops, ens_sum, work, s);

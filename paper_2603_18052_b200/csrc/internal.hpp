@@ -110,6 +110,7 @@ constexpr std::size_t kExpmStreamN = 128;  // expm products on the stream-K engi
 std::size_t expm_workspace(std::size_t n);  // bytes (lbg_expm_workspace)
 // flag |= 1 when any of p[0 .. count) is not finite (k_validate.cu)
 void launch_flag_nonfinite(const double* p, long long count, unsigned* flag, cudaStream_t s);
+void launch_flag_nonhermitian(const double* m, long long d, unsigned* flag, cudaStream_t s);
 // batched building blocks (k_model.cu)
 void launch_build_lindbladian_batched(std::size_t d, const double* h, std::size_t n_ops, const double* ops,
                                       int64_t batch, double* out, cudaStream_t s);

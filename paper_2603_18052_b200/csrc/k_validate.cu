@@ -106,7 +106,24 @@ __global__ void flag_nonfinite_kernel(const double* __restrict__ p, long long co
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
 }
 
+// flag |= 1 when the d x d complex matrix is not EXACTLY Hermitian (bitwise)
+__global__ void flag_nonhermitian_kernel(const double2* __restrict__ m, long long d, unsigned* __restrict__ flag) {
+  bool bad = false;
+  for (long long e = threadIdx.x; e < d * d; e += blockDim.x) {
+    const long long i = e / d, j = e - i * d;
+    const double2 a = m[i * d + j], b = m[j * d + i];
+    bad = bad || a.x != b.x || a.y != -b.y;
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+}
+
 }  // namespace
+
+void launch_flag_nonhermitian(const double* m, long long d, unsigned* flag, cudaStream_t s) {
+  if (d <= 0) return;
+  flag_nonhermitian_kernel<<<1, 256, 0, s>>>(reinterpret_cast<const double2*>(m), d, flag);
+  LBG_CHECK_LAUNCH("flag_nonhermitian_kernel");
+}
 
 // flag |= 1 when any of p[0 .. count) is NaN or infinite (stream-ordered)
 void launch_flag_nonfinite(const double* p, long long count, unsigned* flag, cudaStream_t s) {
