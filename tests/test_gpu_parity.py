@@ -450,6 +450,37 @@ def test_sweep_sparse_build_matches_dense_build(lbg, torch, dt):
     assert (ps != pd).any()  # different rounding: the sparse path did run
 
 
+def test_sweep_sparse_build_edge_patterns(lbg, torch):
+    """K4-S plans on patterns other than config 4's: (a) the zero generator (every
+    column group empty, P = I: populations of rho0 unchanged, bitwise); (b) a
+    random sparse Hamiltonian with a single collapse operator (ragged union
+    sizes, groups with empty columns) against the dense build."""
+    B, S = 1040, 30
+    z = np.zeros((9, 9), complex)
+    delta, scale = lbg.sweep_params(3, B)
+    rng = np.random.default_rng(21)
+    g = rng.normal(size=(9, 9)) + 1j * rng.normal(size=(9, 9))
+    rho0 = g @ g.conj().T
+    rho0 = 0.5 * (rho0 + rho0.conj().T) / np.trace(rho0).real
+    pz, _ = _sweep_real(lbg, torch, z, z, z, np.zeros((1, 9, 9), complex), delta, scale, 0.1, rho0, S, False)
+    assert np.array_equal(pz, np.tile(np.diag(rho0).real, (B, 1)))
+    h = np.zeros((9, 9), complex)
+    for _ in range(6):
+        i, j = rng.integers(0, 9, 2)
+        v = rng.normal() + 1j * rng.normal()
+        h[i, j] += v
+        h[j, i] += np.conj(v)
+    hd = np.diag(rng.normal(size=9)).astype(complex)
+    hs = np.zeros((9, 9), complex)
+    hs[0, 3] = hs[3, 0] = 0.4
+    op = np.zeros((1, 9, 9), complex)
+    op[0, 2, 5] = 0.3
+    ps, es = _sweep_real(lbg, torch, h, hd, hs, op, delta, scale, 0.1, rho0, S, False)
+    pd, ed = _sweep_real(lbg, torch, h, hd, hs, op, delta, scale, 0.1, rho0, S, True)
+    assert np.abs(ps - pd).max() <= 1e-12
+    assert np.abs(es - ed).max() <= 1e-12 * B
+
+
 def test_sweep_dense_generator_falls_back_to_dense_build(lbg, torch):
     """A generator with no sparsity (dense random Hermitian h0) overflows the
     sparse plan's k-step capacity; the build must take the dense path on the
