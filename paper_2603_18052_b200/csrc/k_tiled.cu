@@ -43,9 +43,8 @@ namespace lbg {
 namespace {
 
 constexpr int BM = 32, BK = 32, STAGES = 2;  // default ring depth
-constexpr int CWARPS = 8, THREADS = 32 * (CWARPS + 1);  // defaults (Geo<..., CW_>)
+constexpr int CWARPS = 8;  // default consumer warps (Geo<..., CW_>)
 constexpr int SA = BK + 2;  // complex stride of A rows: 2 (mod 8), see header
-constexpr int A_ELEMS = BM * SA;
 
 // Tile geometry by tile width BN (complex columns): 32 for the expm GEMM, 16 for
 // the stepper (twice the tiles per step -> half the step-tail granularity).
@@ -55,22 +54,29 @@ constexpr int A_ELEMS = BM * SA;
 // x BN tiles, K chunk 32, A stride 36 = 4 (mod 16) and B stride BN + 8 =
 // 8 (mod 16) doubles (conflict-free m8n8k4 fragments), the same byte size per
 // stage as the complex geometry.
-template <int BN_, bool REAL_ = false, int BK_ = BK, int ST_ = STAGES, int CW_ = CWARPS>
+template <int BN_, bool REAL_ = false, int BK_ = BK, int ST_ = STAGES, int CW_ = CWARPS, int BMC_ = BM,
+          bool KS_ = false, int NI_ = 2>
 struct Geo {
   static constexpr int ST = ST_;  // ring stages
   static constexpr int CW = CW_, NT = 32 * (CW_ + 1);  // consumer warps, threads (+ producer warp)
   static constexpr bool REAL = REAL_;
+  // KS: warps w and w + CW / 2 compute the same output block over the even / odd
+  // k-steps of every chunk and add at the end of the tile (exact-fit geometry)
+  static constexpr bool KS = KS_;
+  static constexpr int CWE = KS ? CW / 2 : CW;     // warps of the output grid
   static constexpr int CPX = REAL ? 1 : 2;         // doubles per element
-  static constexpr int BMg = REAL ? 64 : BM;       // rows per tile
+  static constexpr int BMg = REAL ? 64 : BMC_;     // rows per tile
   static constexpr int BKg = BK_;                  // K chunk (elements)
   static constexpr int SAg = REAL ? BKg + 4 : SA;  // A row stride (elements)
-  static constexpr int BN = BN_, NI = 2, WN = BN_ / (8 * NI), WM = CW / WN;
+  static constexpr int BN = BN_, NI = NI_, WN = BN_ / (8 * NI), WM = CWE / WN;
   static constexpr int MI = (REAL ? BMg / 8 : BMg / 4) / WM;
   static constexpr int SB = REAL ? BN_ + 8 : BN_ + 4;  // B row stride (elements)
   static constexpr int A_ELEMS = BMg * SAg * CPX / 2, B_ELEMS = BKg * SB * CPX / 2;  // double2 units
   static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
-  static constexpr size_t kSmemBytes = size_t(ST) * STAGE_ELEMS * sizeof(double2) + 256;
-  static_assert(WN * WM == CW && MI * WM * (REAL ? 8 : 4) == BMg, "tile geometry");
+  static constexpr size_t XCH_ELEMS = KS ? size_t(CWE) * 32 * MI * NI : 0;  // k-parity handoff (double2)
+  static constexpr size_t kSmemBytes = size_t(ST) * STAGE_ELEMS * sizeof(double2) + 256 + XCH_ELEMS * 16;
+  static_assert(WN * WM == CWE && MI * WM * (REAL ? 8 : 4) == BMg, "tile geometry");
+  static_assert(!KS || (!REAL && CW % 2 == 0), "k-parity split: complex tiles, warp pairs");
   static_assert(REAL || BK_ == BK, "complex tiles use the global K chunk (SA and the B box follow BK)");
 };
 
@@ -132,6 +138,7 @@ struct Ring {
   uint64_t* full;  // STAGES
   uint64_t* empty; // STAGES
   int* hdr;        // STAGES x 4: tile id (-1 = end of step), k chunk, segment [lo, hi] chunks
+  double2* xch;    // KS geometries: the odd-k warps' accumulators at the end of a tile
 };
 
 template <class G>
@@ -142,6 +149,7 @@ __device__ __forceinline__ Ring carve(unsigned char* smem) {
   r.full = reinterpret_cast<uint64_t*>(tail);
   r.empty = r.full + G::ST;
   r.hdr = reinterpret_cast<int*>(r.empty + G::ST);
+  r.xch = reinterpret_cast<double2*>(smem + size_t(G::ST) * G::STAGE_ELEMS * sizeof(double2) + 256);
   return r;
 }
 
@@ -236,7 +244,8 @@ __device__ __forceinline__ void consume(const Ring& r, const Problem& p, int til
   constexpr int BN = G::BN, SB = G::SB, STAGE_ELEMS = G::STAGE_ELEMS, MI = G::MI, NI = G::NI;
   constexpr int BK = G::BKg;
   const AFragLane af(lane);
-  const int wm = warp / G::WN, wn = warp % G::WN;
+  const int wsub = G::KS ? warp % G::CWE : warp, kpar = G::KS ? warp / G::CWE : 0;
+  const int wm = wsub / G::WN, wn = wsub % G::WN;
   const int nk = (p.K + BK - 1) / BK;
   const int gq = lane >> 2, tq = lane & 3;
   // fragment bases in doubles: complex real-form (common.cuh) or plain real
@@ -283,7 +292,8 @@ __device__ __forceinline__ void consume(const Ring& r, const Problem& p, int til
       }
     } else {
 #pragma unroll
-      for (int ks = 0; ks < BK / 2; ++ks) {
+      for (int k2 = 0; k2 < BK / (G::KS ? 4 : 2); ++k2) {
+        const int ks = G::KS ? 2 * k2 + kpar : k2;
         double a[MI], b[NI];
 #pragma unroll
         for (int mi = 0; mi < MI; ++mi) a[mi] = af.sign(ad[2 * (mi * 4 * SA) + 4 * ks]);
@@ -299,6 +309,28 @@ __device__ __forceinline__ void consume(const Ring& r, const Problem& p, int til
     if (lane == 0) mbar_arrive(&r.empty[stage]);
     advance<G::ST>(stage, phase);
     if (kc != hi) continue;
+    if constexpr (G::KS) {  // odd-k warps hand their accumulators to the even-k warps
+      double2* x = r.xch + (wsub * 32 + lane) * MI * NI;
+      if (kpar)
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < NI; ++ni) x[mi * NI + ni] = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+      consumer_bar<32 * G::CW>();
+      if (kpar) {
+        consumer_bar<32 * G::CW>();  // the xch slots are reused by the next tile
+        continue;  // (KS geometries run one whole tile per CTA: no stream-K parts)
+      }
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) {
+          const double2 v = x[mi * NI + ni];
+          acc[mi][ni][0] += v.x;
+          acc[mi][ni][1] += v.y;
+        }
+      consumer_bar<32 * G::CW>();
+    }
     constexpr int SLOT = G::CW * 32 * MI * NI;
     if (sk && lo > 0) {  // TAIL / MIDDLE part: publish the partial accumulators
       double2* dst = sk->part + (long long)blockIdx.x * SLOT;
@@ -444,6 +476,13 @@ __global__ void __launch_bounds__(G::NT) gemm_kernel(const double2* __restrict__
 // 32-wide tiles: 16-wide halves the step-tail granularity but doubles the
 // row copies per MMA and measured 2x slower at config 3 (copy-issue bound).
 using StepGeo = Geo<32>;
+// Exact-fit geometry for small batches: 20 complex rows (5 m-tiles) x 32
+// trajectories, warp pair (w, w + 4) on n-tile w splitting the k-steps by
+// parity, 4 stages (127 KB: one CTA per SM). At c3's 8-GPU share (n = 729,
+// 128 trajectories) that is 37 x 4 = 148 tiles: one whole tile per SM per step,
+// no stream-K parts and no fixups (the default 32 x 32 tiles: 92 tiles split
+// several ways over 148 CTAs, the HEADs waiting on their contributors).
+using StepGeoX = Geo<32, false, BK, 4, 8, 20, true, 1>;
 using StepGeoR = Geo<32, true, 64>;  // real arithmetic (density mode); measured: <64,true,32> 11.2, <64,true,64> 8.34, this 8.32 ms at c3
 struct StepCtl {
   unsigned int tile_ctr[2];
@@ -664,8 +703,16 @@ size_t workspace_of(size_t n, int64_t batch) {
   return 2 * align_up(vbytes) + aux_workspace_of<G>(n, batch);
 }
 
+// the exact-fit geometry when its tiles fill 90-100% of the SMs and the default
+// tiles would have to be split (fewer tiles than SMs)
+bool use_exact_fit(size_t n, int64_t batch) {
+  const long long sms = sm_count(), t = (long long)ntiles_of<StepGeoX>(n, batch);
+  return t <= sms && 10 * t >= 9 * sms && (long long)ntiles_of<StepGeo>(n, batch) < sms;
+}
+
 size_t tiled_workspace(size_t n, int64_t batch) {
-  return workspace_of<StepGeo>(n, batch);
+  return use_exact_fit(n, batch) ? std::max(workspace_of<StepGeo>(n, batch), workspace_of<StepGeoX>(n, batch))
+                                 : workspace_of<StepGeo>(n, batch);
 }
 size_t tiled_real_workspace(size_t n, int64_t batch) {
   return workspace_of<StepGeoR>(n, batch) + align_up(8 * n * even(n));  // + an even-stride copy of P_R
@@ -740,7 +787,7 @@ void run_tiled_ext(const double* p_dev, size_t ldp, size_t n, int64_t batch, int
     map_v0 = real_map(reinterpret_cast<const double*>(v0), n, size_t(batch), ldv, G::BKg, G::SB);
     map_v1 = real_map(reinterpret_cast<const double*>(v1), n, size_t(batch), ldv, G::BKg, G::SB);
   } else {
-    map_p = complex_map(p2, n, n, BM, SA);
+    map_p = complex_map(p2, n, n, G::BMg, SA);
     map_v0 = complex_map(v0, n, size_t(batch), BK, G::SB);
     map_v1 = complex_map(v1, n, size_t(batch), BK, G::SB);
   }
@@ -788,7 +835,11 @@ void launch_tiled_evolve(const double* p_dev, size_t n, double* x_re, double* x_
   double2* v1 = reinterpret_cast<double2*>(static_cast<char*>(work) + align_up(sizeof(double2) * n * size_t(batch)));
   const int ni = int(n), bi = int(batch);
   convert<true>(x_re, x_im, x_aos, v0, ni, bi, layout, s);
-  run_tiled<StepGeo>(p_dev, n, n, batch, steps, work, s);
+  static const bool no_fit = std::getenv("LBG_TILED_NO_EXACT_FIT") != nullptr;  // A/B only
+  if (!no_fit && use_exact_fit(n, batch))
+    run_tiled<StepGeoX>(p_dev, n, n, batch, steps, work, s);
+  else
+    run_tiled<StepGeo>(p_dev, n, n, batch, steps, work, s);
   convert<false>(x_re, x_im, x_aos, (steps & 1) ? v1 : v0, ni, bi, layout, s);
 }
 

@@ -671,12 +671,16 @@ def test_grape_real_squarings(lbg, dt):
     assert np.abs(got1 - lbg.evolve(P, rho0, 6)).max() <= TOL_RHO
 
 
-@pytest.mark.parametrize("n,B", [(17, 16), (33, 5), (81, 8), (97, 40), (130, 333), (729, 128), (729, 100), (500, 200)])
+@pytest.mark.parametrize("n,B", [(17, 16), (33, 5), (81, 8), (97, 40), (130, 333), (729, 128), (729, 100), (729, 97),
+                                 (729, 96), (500, 200)])
 def test_tiled_ragged_shapes_vs_torch(lbg, torch, n, B):
     """Regression: odd n (ragged last K chunk and last M tile) through the TMA /
     mbarrier tile engine, against torch fp64 matmuls (a plain fp64 reference).
-    (729, 128), (729, 100), (500, 200): fewer tiles than resident CTAs, so tiles
-    split several ways (stream-K HEAD + MIDDLE + TAIL parts)."""
+    (729, 128), (729, 100), (729, 97): the exact-fit geometry (37 x 4 = 148 tiles
+    of 20 rows x 32 trajectories, warp pairs splitting k by parity, ragged last
+    row tile and trajectory tile); (729, 96), (500, 200): fewer tiles than
+    resident CTAs on the default tiles, split several ways (stream-K HEAD +
+    MIDDLE + TAIL parts)."""
     dev = torch.device("cuda")
     g = torch.Generator(device="cpu").manual_seed(n)
     P = (torch.randn(n, n, dtype=torch.complex128, generator=g) / n).to(dev)
