@@ -163,16 +163,18 @@ int lbg_evolve_density(const double* p, size_t d, const double* rho0, int64_t ba
  * Per-trajectory propagators (config 4, "robustness atlas"): for trajectory b
  *   H_b = h0 + delta[b] * hd + scale[b] * hs,   L_k fixed,
  *   L_b = build_lindbladian(H_b, L_k),  P_b = exp(L_b dt),
- *   rho_b <- P_b^steps rho0      (fused on the GPU: assembly K5, expm K4,
- *                                  stepping K3; in the default REAL mode P_R (52 KB per
- *                                  trajectory) passes through HBM once between K4 and K3)
+ *   rho_b <- P_b^steps rho0      (on the GPU: assembly K5, expm K4, stepping K3; in the
+ *                                  default REAL mode the build exploits the sparse
+ *                                  generator (K4-S) and P_R (52 KB per trajectory)
+ *                                  passes through HBM once between K4 and K3)
  * Outputs: pops[b*d + i] = Re rho_b[i][i]; ens_sum (d*d AoS) += sum_b rho_b.
  * Replaces, per trajectory, the make_model + build_lindbladian + expm + step
  * sequence of lb::grape_chain (propagate.cpp:130-160). Device pointers.
  * mode: LBG_SWEEP_REAL propagates the real coordinates of the (Hermitian)
  * density matrix with the real d^2 x d^2 representation L_R = T L T^-1 of the
  * same generator (P_R = T P T^-1; 4x fewer flops; d == 9; rho0 must be exactly
- * Hermitian — checked, one 81-element D2H). LBG_SWEEP_COMPLEX uses the
+ * Hermitian — checked on the device with the other input checks, one 32-byte
+ * D2H per call). LBG_SWEEP_COMPLEX uses the
  * complex d^2 x d^2 matrices exactly as the reference does. AUTO = REAL when
  * it applies, else COMPLEX.
  * ------------------------------------------------------------------------ */
