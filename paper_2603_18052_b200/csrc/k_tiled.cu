@@ -217,6 +217,66 @@ __device__ __forceinline__ void produce_end(const Ring& r, int& stage, unsigned&
   advance<G::ST>(stage, phase);
 }
 
+// Producer for the exact-fit geometries (one whole tile per CTA and step, the
+// same chunk sequence every step): the A parts (P, never written) of the next
+// step's first chunks are issued as soon as their ring slots free up, BEFORE the
+// grid barrier; after it only their B parts (the new state) remain to be
+// issued. The slot's full barrier expects both (one expect_tx), so the
+// consumers see no difference. npre_in: chunks of this step whose A part is
+// already in flight (issued at the end of the previous step).
+template <class G>
+__device__ __forceinline__ int produce_tile_prefetch(const Ring& r, const Problem& p, const CUtensorMap* map_a,
+                                                     const CUtensorMap* map_b, int tiles_m, int tile, int npre_in,
+                                                     bool prefetch_next, int& stage, unsigned& phase,
+                                                     int& pre_stage, unsigned& pre_phase, int lane) {
+  constexpr int BN = G::BN, STAGE_ELEMS = G::STAGE_ELEMS, BK = G::BKg;
+  constexpr unsigned kBytes = unsigned(STAGE_ELEMS) * 16u;
+  const int nk = (p.K + BK - 1) / BK;
+  const int m0 = (tile % tiles_m) * G::BMg, n0 = (tile / tiles_m) * BN;
+  if (npre_in > 0) {  // back to the first slot that already holds this step's A part
+    stage = pre_stage;
+    phase = pre_phase;
+  }
+  for (int kc = 0; kc < nk; ++kc) {
+    double2* as = r.data + stage * STAGE_ELEMS;
+    if (kc >= npre_in) {
+      mbar_wait(&r.empty[stage], phase ^ 1u);
+      if (lane == 0) {
+        r.hdr[4 * stage] = tile;
+        r.hdr[4 * stage + 1] = kc;
+        r.hdr[4 * stage + 2] = 0;
+        r.hdr[4 * stage + 3] = nk - 1;
+        mbar_arrive_tx(&r.full[stage], kBytes);
+        tma_g2s_2d(as, map_a, G::CPX * kc * BK, m0, &r.full[stage]);
+      }
+    }
+    if (lane == 0) tma_g2s_2d(as + G::A_ELEMS, map_b, G::CPX * n0, kc * BK, &r.full[stage]);
+    __syncwarp();
+    advance<G::ST>(stage, phase);
+  }
+  produce_end<G>(r, stage, phase, lane);
+  if (!prefetch_next) return 0;
+  const int npre = nk < G::ST ? nk : G::ST;
+  pre_stage = stage;
+  pre_phase = phase;
+  for (int kc = 0; kc < npre; ++kc) {  // next step: header, expect_tx and the A part now
+    mbar_wait(&r.empty[stage], phase ^ 1u);
+    if (lane == 0) {
+      double2* as = r.data + stage * STAGE_ELEMS;
+      r.hdr[4 * stage] = tile;
+      r.hdr[4 * stage + 1] = kc;
+      r.hdr[4 * stage + 2] = 0;
+      r.hdr[4 * stage + 3] = nk - 1;
+      mbar_arrive_tx(&r.full[stage], kBytes);
+      tma_g2s_2d(as, map_a, G::CPX * kc * BK, m0, &r.full[stage]);
+    }
+    __syncwarp();
+    advance<G::ST>(stage, phase);
+  }
+  return npre;
+}
+
+
 // Consumer warps: run tiles until the end-of-step sentinel.
 // Split tiles (stream-K): a tile cut between CTAs' ranges has a HEAD part
 // (chunks from 0), possibly MIDDLE parts (a CTA whose whole range lies inside
@@ -527,14 +587,22 @@ __global__ void __launch_bounds__(G::NT) tiled_evolve_kernel(const double2* __re
       trace[((size_t)s * gridDim.x + blockIdx.x) * (G::CW + 2) + slot] = t;
     }
   };
+  int npre = 0;  // exact-fit producer: chunks of the step whose A part is already in flight,
+  int pre_stage = 0;  // starting at this ring slot / phase
+  unsigned pre_phase = 0;
   for (int64_t s = 0; s < steps; ++s) {
     const Problem p{P, n, cur, ldv, nxt, ldv, n, batch, n};
     if (warp == 0) stamp(s, 0);
     if (warp == G::CW) {
       // generic-proxy stores of the previous step -> async-proxy (bulk copy) reads
       asm volatile("fence.proxy.async.global;\n" ::: "memory");
-      produce_range_tma<G>(r, p, &map_p, (s & 1) ? &map_v1 : &map_v0, tiles_m, it0, it1, stage, phase, lane);
-      produce_end<G>(r, stage, phase, lane);
+      if constexpr (G::KS) {  // exact fit: it0 / it1 cover exactly the tile blockIdx.x
+        npre = produce_tile_prefetch<G>(r, p, &map_p, (s & 1) ? &map_v1 : &map_v0, tiles_m, int(blockIdx.x), npre,
+                                        s + 1 < steps, stage, phase, pre_stage, pre_phase, lane);
+      } else {
+        produce_range_tma<G>(r, p, &map_p, (s & 1) ? &map_v1 : &map_v0, tiles_m, it0, it1, stage, phase, lane);
+        produce_end<G>(r, stage, phase, lane);
+      }
       stamp(s, G::CW + 1);
     } else {
       const SplitK sk{part, flags, unsigned(s + 1), work};
@@ -680,6 +748,7 @@ int tiled_grid_of(size_t n, int64_t batch) {
   check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, G::NT, G::kSmemBytes), "occupancy");
   const int sms = sm_count(), slots = std::max(1, occ * sms);
   const long long nt = (long long)ntiles_of<G>(n, batch), nk = ((long long)n + G::BKg - 1) / G::BKg;
+  if constexpr (G::KS) return int(nt);  // exact fit: one whole tile per CTA (use_exact_fit: nt <= SMs)
   constexpr long long kMinItersPerCta = 3;
   int grid;
   if (nt >= slots) {

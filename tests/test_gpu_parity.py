@@ -672,11 +672,12 @@ def test_grape_real_squarings(lbg, dt):
 
 
 @pytest.mark.parametrize("n,B", [(17, 16), (33, 5), (81, 8), (97, 40), (130, 333), (729, 128), (729, 100), (729, 97),
-                                 (729, 96), (500, 200)])
+                                 (700, 128), (729, 96), (500, 200)])
 def test_tiled_ragged_shapes_vs_torch(lbg, torch, n, B):
     """Regression: odd n (ragged last K chunk and last M tile) through the TMA /
     mbarrier tile engine, against torch fp64 matmuls (a plain fp64 reference).
-    (729, 128), (729, 100), (729, 97): the exact-fit geometry (37 x 4 = 148 tiles
+    (729, 128), (729, 100), (729, 97), (700, 128): the exact-fit geometry (37 x 4 = 148 tiles,
+    35 x 4 = 140 at n = 700
     of 20 rows x 32 trajectories, warp pairs splitting k by parity, ragged last
     row tile and trajectory tile); (729, 96), (500, 200): fewer tiles than
     resident CTAs on the default tiles, split several ways (stream-K HEAD +
