@@ -197,6 +197,23 @@ void launch_scale(double* x, size_t n, double s, cudaStream_t st) {
   LBG_CHECK_LAUNCH("scale_kernel");
 }
 
+void sync_event_spin(cudaEvent_t e, const char* what) {
+  cudaError_t rc;
+  while ((rc = cudaEventQuery(e)) == cudaErrorNotReady) {
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+  }
+  check_cuda(rc, what);
+}
+void sync_stream_spin(cudaStream_t s, const char* what) {
+  thread_local std::map<int, cudaEvent_t>* evs = new std::map<int, cudaEvent_t>;  // per thread and device
+  cudaEvent_t& e = (*evs)[current_device()];
+  if (!e) check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  check_cuda(cudaEventRecord(e, s), what);
+  sync_event_spin(e, what);
+}
+
 int current_device() {
   int dev = 0;
   check_cuda(cudaGetDevice(&dev), "get device");
@@ -623,7 +640,7 @@ int lbg_evolve_sweep_dev(size_t d, const double* h0, const double* hd, const dou
       const cudaError_t e2 = cudaFreeAsync(dchk, s);
       check_cuda(e1, "D2H check");
       check_cuda(e2, "free check");
-      check_cuda(cudaStreamSynchronize(s), "sync check");
+      sync_stream_spin(s, "sync check");
       if (!(chk[0] <= 1e-8 && chk[1] <= 1e-8 && chk[2] >= -1e-8))
         throw invalid_argument("evolve: initial state fails physical-state checks");
       unsigned flags[2];

@@ -282,7 +282,7 @@ void host_evolve(const double* p, size_t d, const double* rho0, int64_t batch, d
       check_cuda(cudaEventRecord(pool.ev_c[c], sc), "event");
     }
     check_cuda(cudaEventRecord(pool.ev_chk, sk), "event");
-    check_cuda(cudaEventSynchronize(pool.ev_chk), "sync check");
+    sync_event_spin(pool.ev_chk, "sync check");
     for (int c = 0; c < nchunks; ++c)
       if (!(hchk[3 * c] <= 1e-8 && hchk[3 * c + 1] <= 1e-8 && hchk[3 * c + 2] >= -1e-8))
         throw invalid_argument("evolve: initial state fails physical-state checks");
@@ -298,10 +298,10 @@ void host_evolve(const double* p, size_t d, const double* rho0, int64_t batch, d
     if (!out_pinned)
       for (int c = 0; c < nchunks; ++c) {  // copy each chunk out as soon as it has landed
         const size_t off = size_t(bounds[c]) * n * 16, bytes = size_t(bounds[c + 1] - bounds[c]) * n * 16;
-        check_cuda(cudaEventSynchronize(pool.ev_d[c]), "sync D2H");
+        sync_event_spin(pool.ev_d[c], "sync D2H");
         cp.copy(reinterpret_cast<char*>(out) + off, pin_out + off, bytes);
       }
-    check_cuda(cudaStreamSynchronize(sd), "sync");
+    sync_stream_spin(sd, "sync");
     if (timing) {
       for (int c = 0; c < nchunks; ++c) {
         float t[4];

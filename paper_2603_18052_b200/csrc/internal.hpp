@@ -183,5 +183,11 @@ int sm_count();       // of the current device
 int current_device();
 // cudaFuncAttributeMaxDynamicSharedMemorySize, set once per (kernel, device)
 void ensure_max_dyn_smem(const void* fn, int bytes);
+// Wait for an event / a stream by polling (cudaEventQuery) instead of the
+// runtime's blocking wait: a blocking cudaStreamSynchronize returned ~0.25-0.3 ms
+// after the work completed on the GPU box (thread wake-up), which left the GPU
+// idle mid-call (config-4 validation round trip) and padded every host-buffer call.
+void sync_event_spin(cudaEvent_t e, const char* what);
+void sync_stream_spin(cudaStream_t s, const char* what);
 
 }  // namespace lbg

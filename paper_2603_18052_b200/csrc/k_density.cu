@@ -431,7 +431,7 @@ void launch_density(const double* p, size_t d, double* rho, int64_t batch, int64
     if (tiled_auto) {  // read the flag (one 4-byte sync): the tile engine takes its vector count from the host
       int h = 0;
       check_cuda(cudaMemcpyAsync(&h, live, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H flag");
-      check_cuda(cudaStreamSynchronize(s), "sync flag");
+      sync_stream_spin(s, "sync flag");
       gen = h != 0;
     }
     void* inner = w + align_up(n * n * 8) + align_up(2 * size_t(batch) * n * 8) + 256;

@@ -428,7 +428,7 @@ void expm_dev(const double* a, size_t n, double dt, double* out, double* work, c
   LBG_CHECK_LAUNCH("colsum_kernel");
   std::vector<double> cs(n);
   check_cuda(cudaMemcpyAsync(cs.data(), colsum, sizeof(double) * n, cudaMemcpyDeviceToHost, s), "D2H norm");
-  check_cuda(cudaStreamSynchronize(s), "sync norm");
+  sync_stream_spin(s, "sync norm");
   double nrm = 0.0;
   for (double v : cs) nrm = (std::isnan(v) || v > nrm) ? v : nrm;  // a NaN column must not be dropped
   nrm *= std::fabs(dt);
@@ -509,7 +509,7 @@ void expm_batched_dev(const double* a, size_t n, int64_t batch, double dt, doubl
     LBG_CHECK_LAUNCH("small_expm_batched_kernel");
     unsigned hbad = 0;
     check_cuda(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, s), "D2H");
-    check_cuda(cudaStreamSynchronize(s), "sync");
+    sync_stream_spin(s, "sync");
     if (hbad & 1u) throw invalid_argument("expm: non-finite entries in input");
     if (hbad & 2u) throw runtime_error("expm: norm of a*dt requires more than 64 squarings");
     return;
@@ -524,7 +524,7 @@ void expm_batched_dev(const double* a, size_t n, int64_t batch, double dt, doubl
   LBG_CHECK_LAUNCH("norm_batched_kernel");
   unsigned long long bits = 0;
   check_cuda(cudaMemcpyAsync(&bits, nmax, 8, cudaMemcpyDeviceToHost, s), "D2H norm");
-  check_cuda(cudaStreamSynchronize(s), "sync norm");
+  sync_stream_spin(s, "sync norm");
   double nrm;
   std::memcpy(&nrm, &bits, 8);
   nrm *= std::fabs(dt);

@@ -262,7 +262,7 @@ void propagators_complex(size_t d, const double* h0, const double* hd, const dou
   }
   unsigned long long bits = 0;
   check_cuda(cudaMemcpyAsync(&bits, nmax, 8, cudaMemcpyDeviceToHost, s), "D2H");
-  check_cuda(cudaStreamSynchronize(s), "sync");
+  sync_stream_spin(s, "sync");
   double nrm;
   std::memcpy(&nrm, &bits, 8);
   if (!std::isfinite(nrm)) throw invalid_argument("sweep: non-finite generator");

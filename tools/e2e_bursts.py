@@ -1,5 +1,5 @@
-"""e2e call-time bursts with and without an nvidia-smi -lms 50 sampler (measurement tooling):
-python tools/e2e_bursts.py"""
+"""e2e call times of lbg_evolve_shared_p with and without an nvidia-smi -lms 50 sampler
+(measurement tooling): python tools/e2e_bursts.py"""
 import os, sys, time, subprocess
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch
