@@ -472,7 +472,7 @@ def run_ours(args):
         e2e_pg = max_over_ranks(torch, med_pg)
         e2e = {"value": gb * S / e2e_s, "unit": "traj-steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_call": e2e_s * 1e3, "ms_per_call_all": [round(c * 1e3, 3) for c in calls],
-               "call": "lbg_evolve_shared_p (pinned host buffers, synchronous); median of 41 (the box throws bursts of 35-125 ms calls, with or without the nvidia-smi sampler: tools/e2e_bursts.py measured 1-5 per 40 calls either way)",
+               "call": "lbg_evolve_shared_p (pinned host buffers, synchronous); median of 41 (the 35-125 ms call bursts seen before came from the runtime's blocking stream sync; the engine now spin-waits its host round trips: tools/e2e_bursts.py)",
                "max_abs_diff_vs_device": diff, "clocks": eclk.summary(),
                "pageable": {"value": gb * S / e2e_pg, "ms_per_call": e2e_pg * 1e3,
                             "ms_per_call_all": [round(c * 1e3, 3) for c in calls_pg],
