@@ -32,7 +32,7 @@ for e in evs:
     if last_end is not None and e.time_range.start > last_end:
         gap = (e.time_range.start - last_end) / 1e3
         gaps += gap
-        if gap > 0.02:
+        if gap > 0.005:
             print(f"gap {gap:.3f} ms before {e.name[:50]}")
     last_end = max(last_end or 0, e.time_range.end)
 span = (evs[-1].time_range.end - evs[0].time_range.start) / 1e3
