@@ -1,9 +1,9 @@
 // k_probe.cu — FP64 roofline denominators measured live on the current GPU.
 // MEASURED_PEAKS.json carries HBM and bf16 peaks only, so bench.py calls
 // lbg_fp64_peak() right before its timed region: a register-only DMMA loop
-// (mma.sync m8n8k4 f64 -> SASS DMMA.8x8x4) and a register-only DFMA loop, both
-// over 148 x 8 CTAs, best of 3 by CUDA events. profiles/r01_fp64_peaks.json has
-// the first measurement (DMMA 37.0, DFMA 34.1 TF/s at 1965 MHz).
+// (mma.sync m8n8k4 f64 -> SASS DMMA.8x8x4) and a DFMA loop (occupancy sweep),
+// best of 3 by CUDA events. r02: DMMA 37.1, DFMA 36.8 TF/s at 1965 MHz; DMMA and
+// DFMA share one FP64 pipe (tools/fp64_mixed.cu: any mix tops out at 36.9).
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
@@ -31,21 +31,24 @@ __global__ void probe_dmma(double* out, int iters) {
   if (s == 1234.5678) out[threadIdx.x] = s;
 }
 
-// 16 independent chains x 16 unrolled FMAs per loop trip: the loop overhead
-// is < 2% of the issue slots (r01's 8 x 8 body read 34.1 TF/s, below the 35.2
-// the dfma9 stepper reaches)
-__global__ void probe_dfma(double* out, int iters, double a, double b) {
-  double acc[16];
+// 8 independent chains x 8 unrolled FMAs per loop trip with compile-time
+// coefficients, so ptxas feeds the multiplier from a uniform register (DFMA R,
+// R, UR, R) as the dfma9 stepper does: r02 measured 36.5-36.8 TF/s that way at
+// one 512-thread CTA per SM (tools/fp64_mixed.cu), against 33.4-34.1 when all
+// three operands come from the register file (runtime a, b).
+__global__ void probe_dfma(double* out, int iters, double, double) {
+  constexpr double a = 0.999, b = 1e-3;
+  double acc[8];
 #pragma unroll
-  for (int c = 0; c < 16; ++c) acc[c] = threadIdx.x * 1e-3 + c;
-  for (int it = 0; it < iters / 2; ++it)
+  for (int c = 0; c < 8; ++c) acc[c] = threadIdx.x * 1e-3 + c;
+  for (int it = 0; it < iters; ++it)
 #pragma unroll
     for (int u = 0; u < 8; ++u)
 #pragma unroll
-      for (int c = 0; c < 16; ++c) acc[c] = fma(acc[c], a, b);
+      for (int c = 0; c < 8; ++c) acc[c] = fma(acc[c], a, b);
   double s = 0;
 #pragma unroll
-  for (int c = 0; c < 16; ++c) s += acc[c];
+  for (int c = 0; c < 8; ++c) s += acc[c];
   if (s == 1234.5678) out[threadIdx.x] = s;
 }
 
@@ -200,8 +203,15 @@ extern "C" int lbg_fp64_peak(double* dmma_tflops, double* dfma_tflops) {
     };
     *dmma_tflops = best_of([&] { probe_dmma<<<blocks, threads>>>(out, iters); },
                            2.0 * 256 * 16.0 * iters * blocks * (threads / 32));
-    *dfma_tflops = best_of([&] { probe_dfma<<<blocks, threads>>>(out, iters, 0.999, 1e-3); },
-                           2.0 * 64 * double(iters) * blocks * threads);
+    // occupancy sweep (r02: 4 x 256 threads per SM read 33.4-34.1 TF/s, below the 35.2 the
+    // dfma9 stepper reaches; one 512-thread CTA per SM reads ~36.8, tools/fp64_mixed.cu)
+    double best = 0.0;
+    for (const int bpsm : {1, 2, 4}) {
+      const int tb = bpsm == 1 ? 512 : 256, nb = sm_count() * bpsm;
+      best = std::max(best, best_of([&] { probe_dfma<<<nb, tb>>>(out, iters, 0.999, 1e-3); },
+                                    2.0 * 64 * double(iters) * nb * tb));
+    }
+    *dfma_tflops = best;
     check_cuda(cudaGetLastError(), "probe");
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
