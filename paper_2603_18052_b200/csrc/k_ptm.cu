@@ -29,7 +29,7 @@
 //   and row / column 80), 8 warps in 5x3 / 5x2 tile blocks, A and A^2 kept at
 //   the lanes' own entries. Writes P_R (n x n) to global memory.
 // K3 (ptm_step_kernel): three trajectories per CTA; P_R register resident
-//   (a 4 x 21 block per thread), x in shared memory; per step 84 FMAs in 12
+//   (a 4 x 21 block per thread), x in shared memory; per step 84 FMAs in 4
 //   chains, a 4-lane shuffle reduce-scatter, one barrier. The SM register file
 //   (P_R = 13k registers per trajectory) caps residency at 3 trajectories per
 //   SM. Epilogue: populations + ensemble sum.
@@ -922,8 +922,11 @@ __global__ void __launch_bounds__(EXPM_THREADS, 1)
 // 40%, profiles/r01_ncu_ptm_step_rowthread.json), then a 2-round butterfly
 // reduce-scatter over the 4 lanes leaves each lane one finished row, one store
 // and one barrier.
-// DFMA latency is 23 cycles on B200 (profiles/r01_latency_probe.json): the 4
-// row sums run as 12 independent chains of depth 7.
+// One accumulator per row (4 chains of 21 FMAs per lane): r02 measured 6.06 ms
+// per 16,384-trajectory launch against 6.26 with two per row and 6.63 / 7.10
+// with three / four — with two 224-register warps per sub-partition the step
+// is not bound by the 23-cycle DFMA latency, and the extra accumulators and
+// their DADD combine cost registers and issue slots.
 // Three trajectories per CTA: 63 groups of 4 lanes = 252 of 256 threads, two
 // 224-register warps per sub-partition — all its 16K registers can carry.
 // x lives in shared memory padded per column block (stride 22: 16-byte aligned
@@ -1067,7 +1070,7 @@ __global__ void __maxnreg__(224)
   int cur = 0;
 #pragma unroll 1
   for (int64_t s = 0; s < steps; ++s) {
-    const double kk = block_row_step<2>(p, xs[cur][tt] + cb * XB, hi2, hi1);
+    const double kk = block_row_step<1>(p, xs[cur][tt] + cb * XB, hi2, hi1);
     if (writer) xs[cur ^ 1][tt][slot] = kk;
     __syncthreads();
     cur ^= 1;
