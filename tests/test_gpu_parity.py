@@ -696,7 +696,7 @@ def test_tiled_ragged_shapes_vs_torch(lbg, torch, n, B):
     assert (x - want).abs().max().item() <= 1e-13 * want.abs().max().item()
 
 
-@pytest.mark.parametrize("n,B", [(9, 3000), (81, 70), (81, 5), (729, 3)])
+@pytest.mark.parametrize("n,B", [(9, 3000), (81, 70), (81, 5), (729, 3), (729, 100)])
 def test_all_soa_planes_entry_point(lbg, torch, n, B):
     """lbg_evolve_shared_p_planes_dev (P and the states as re / im planes, the
     reference's Variant::soa) equals the AoS path"""
