@@ -667,29 +667,33 @@ __device__ __forceinline__ void expm_sparse_body(double* SA, double* SB, double*
     col[i][1] = ok ? plan->cols[wi.g[i]][2 * t + 1] : -1;
     c80[i] = ok && wi.half[i] == 0 && t == 0 ? plan->cols[wi.g[i]][g] : -1;
   }
-  // B0 = c0 I + c1 A, B1 = c6 I + c7 A at the sparse-product ownership
-  double b0[SP_IW][5][2], b1[SP_IW][5][2], f0[SP_IW], f1[SP_IW];
+  // B0 = c0 I + c1 A, B1 = c6 I + c7 A at the dense product's ownership (the warp's
+  // 5 x NB tile block and its fringe dots), so B0 is added to that product in registers
+  const int n0 = blk_n0(w), m0 = blk_m0(w);
+  constexpr int FRD = Blk<NB>::FRA;
+  double b0[EMT][NB][2], b1[EMT][NB][2], f0[FRD], f1[FRD];
+  auto dent = [&](int m, int n) { return ((m0 + m) * 8 + g) * RS + (n0 + n) * 8 + 2 * t; };
 #pragma unroll
-  for (int i = 0; i < SP_IW; ++i) {
+  for (int m = 0; m < EMT; ++m)
 #pragma unroll
-    for (int m = 0; m < 5; ++m)
+    for (int n = 0; n < NB; ++n) {
+      const double2 a = *reinterpret_cast<const double2*>(SA + dent(m, n));
+      const int r = (m0 + m) * 8 + g, c = (n0 + n) * 8 + 2 * t;
+      b0[m][n][0] = fma(cf[1], a.x, r == c ? cf[0] : 0.0);
+      b0[m][n][1] = fma(cf[1], a.y, r == c + 1 ? cf[0] : 0.0);
+      b1[m][n][0] = fma(cf[7], a.x, r == c ? cf[6] : 0.0);
+      b1[m][n][1] = fma(cf[7], a.y, r == c + 1 ? cf[6] : 0.0);
+    }
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const int r = wi.half[i] * 40 + m * 8 + g, cc = col[i][c];
-        const double a = cc >= 0 ? SA[r * RS + cc] : 0.0;
-        const double dg = r == cc ? 1.0 : 0.0;
-        b0[i][m][c] = fma(cf[1], a, cf[0] * dg);
-        b1[i][m][c] = fma(cf[7], a, cf[6] * dg);
-      }
-    const double a = c80[i] >= 0 ? SA[80 * RS + c80[i]] : 0.0;
-    const double dg = c80[i] == 80 ? 1.0 : 0.0;
-    f0[i] = fma(cf[1], a, cf[0] * dg);
-    f1[i] = fma(cf[7], a, cf[6] * dg);
+  for (int i = 0; i < Blk<NB>::FR; ++i) {
+    const double a = SA[fr.r[i] * RS + fr.c[i]];
+    f0[i] = fma(cf[1], a, fr.r[i] == fr.c[i] ? cf[0] : 0.0);
+    f1[i] = fma(cf[7], a, fr.r[i] == fr.c[i] ? cf[6] : 0.0);
   }
   const double* cur = SA;
   double* nxt = SB;
 #pragma unroll 1
-  for (int p = 1; p <= 5; ++p) {  // X_{p+1} = X_p A; p = 5: X6 -> nxt, T1 = B1 + c12 X6 -> SC
+  for (int p = 1; p <= 5; ++p) {  // X_{p+1} = X_p A
 #pragma unroll
     for (int i = 0; i < SP_IW; ++i) {
       if (i >= wi.cnt) continue;
@@ -697,76 +701,62 @@ __device__ __forceinline__ void expm_sparse_body(double* SA, double* SB, double*
       sparse_item(cur, bb, ko, wi.ks[i], wi.ksoff[i], wi.half[i], lane, acc, f80);
       if (i == 0 && p >= 2) {
         // B0 += c_p X_p, B1 += c_{p+6} X_p from this product's INPUT (complete since the
-        // barrier): independent of the DMMAs in flight, so it fills their latency instead of
-        // waiting on their results in the epilogue
+        // barrier): independent of the DMMAs in flight, so it fills their latency
         const double ca = cf[p], cb = cf[p + 6];
 #pragma unroll
-        for (int j = 0; j < SP_IW; ++j) {
-          if (j >= wi.cnt) continue;
+        for (int m = 0; m < EMT; ++m)
 #pragma unroll
-          for (int m = 0; m < 5; ++m)
-#pragma unroll
-            for (int c = 0; c < 2; ++c)
-              if (col[j][c] >= 0) {
-                const double x = cur[(wi.half[j] * 40 + m * 8 + g) * RS + col[j][c]];
-                b0[j][m][c] = fma(ca, x, b0[j][m][c]);
-                b1[j][m][c] = fma(cb, x, b1[j][m][c]);
-              }
-          if (c80[j] >= 0) {
-            const double x = cur[80 * RS + c80[j]];
-            f0[j] = fma(ca, x, f0[j]);
-            f1[j] = fma(cb, x, f1[j]);
+          for (int n = 0; n < NB; ++n) {
+            const double2 x = *reinterpret_cast<const double2*>(cur + dent(m, n));
+            b0[m][n][0] = fma(ca, x.x, b0[m][n][0]);
+            b0[m][n][1] = fma(ca, x.y, b0[m][n][1]);
+            b1[m][n][0] = fma(cb, x.x, b1[m][n][0]);
+            b1[m][n][1] = fma(cb, x.y, b1[m][n][1]);
           }
+#pragma unroll
+        for (int j = 0; j < Blk<NB>::FR; ++j) {
+          const double x = cur[fr.r[j] * RS + fr.c[j]];
+          f0[j] = fma(ca, x, f0[j]);
+          f1[j] = fma(cb, x, f1[j]);
         }
       }
 #pragma unroll
       for (int m = 0; m < 5; ++m)
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-          const int r = wi.half[i] * 40 + m * 8 + g, cc = col[i][c];
-          if (cc >= 0) {
-            const double x = acc[m][c];
-            nxt[r * RS + cc] = x;
-            if (p == 5) SC[r * RS + cc] = fma(cf[12], x, b1[i][m][c]);
-          }
+          const int cc = col[i][c];
+          if (cc >= 0) nxt[(wi.half[i] * 40 + m * 8 + g) * RS + cc] = acc[m][c];
         }
-      if (c80[i] >= 0) {
-        nxt[80 * RS + c80[i]] = f80;
-        if (p == 5) SC[80 * RS + c80[i]] = fma(cf[12], f80, f1[i]);
-      }
+      if (c80[i] >= 0) nxt[80 * RS + c80[i]] = f80;
     }
     bar_all();
     cur = nxt;
     nxt = cur == SA ? SB : SA;
   }
-  // cur = X6, nxt = the X5 buffer (free): B0 there
-  double* sb0 = nxt;
+  // cur = X6: T1 = B1 + c12 X6 into SC at the dense product's ownership
 #pragma unroll
-  for (int i = 0; i < SP_IW; ++i) {
-    if (i >= wi.cnt) continue;
+  for (int m = 0; m < EMT; ++m)
 #pragma unroll
-    for (int m = 0; m < 5; ++m)
+    for (int n = 0; n < NB; ++n) {
+      const double2 x = *reinterpret_cast<const double2*>(cur + dent(m, n));
+      *reinterpret_cast<double2*>(SC + dent(m, n)) =
+          make_double2(fma(cf[12], x.x, b1[m][n][0]), fma(cf[12], x.y, b1[m][n][1]));
+    }
 #pragma unroll
-      for (int c = 0; c < 2; ++c)
-        if (col[i][c] >= 0) sb0[(wi.half[i] * 40 + m * 8 + g) * RS + col[i][c]] = b0[i][m][c];
-    if (c80[i] >= 0) sb0[80 * RS + c80[i]] = f0[i];
-  }
+  for (int i = 0; i < Blk<NB>::FR; ++i)
+    if (fr.own[i]) SC[fr.r[i] * RS + fr.c[i]] = fma(cf[12], cur[fr.r[i] * RS + fr.c[i]], f1[i]);
   bar_all();
   Blk<NB> B;
   mm<NB>(cur, SC, B, fr, w, lane);  // X6 (B1 + c12 X6)
-  {
-    const int n0 = blk_n0(w), m0 = blk_m0(w);
 #pragma unroll
-    for (int m = 0; m < EMT; ++m)
+  for (int m = 0; m < EMT; ++m)
 #pragma unroll
-      for (int n = 0; n < NB; ++n) {
-        const double2 v = *reinterpret_cast<const double2*>(sb0 + ((m0 + m) * 8 + g) * RS + (n0 + n) * 8 + 2 * t);
-        B.acc[m][n][0] += v.x;
-        B.acc[m][n][1] += v.y;
-      }
+    for (int n = 0; n < NB; ++n) {
+      B.acc[m][n][0] += b0[m][n][0];
+      B.acc[m][n][1] += b0[m][n][1];
+    }
 #pragma unroll
-    for (int i = 0; i < Blk<NB>::FR; ++i) B.f[i] += sb0[fr.r[i] * RS + fr.c[i]];
-  }
+  for (int i = 0; i < Blk<NB>::FR; ++i) B.f[i] += f0[i];
   if (sq > 0) {
     bar_all();  // everyone done reading X6, T1, B0
     double* tcur = SA;
@@ -784,7 +774,6 @@ __device__ __forceinline__ void expm_sparse_body(double* SA, double* SB, double*
       }
     }
   }
-  const int n0 = blk_n0(w), m0 = blk_m0(w);
 #pragma unroll
   for (int m = 0; m < EMT; ++m)
 #pragma unroll
