@@ -398,7 +398,7 @@ __device__ __forceinline__ void expm_body(double* SA, double* SA2, double* SA3, 
 // loads free of bank conflicts (row stride 84 = 4 mod 16). Config 4: 11
 // groups, 72 k-steps, 720 DMMAs per product (dense: 2,000). Work items are
 // (group, half of the m-tiles): 5 DMMA chains per k-step sharing one B
-// fragment; row 80 is a DFMA dot product on the same fragments. The plan
+// fragment, 6 for the upper half (a sixth m-tile on rows 80..87 carries row 80). The plan
 // depends only on the sparsity pattern of dt (C0, Cd, Cs); ptm_plan_kernel
 // builds it on the device once per call.
 constexpr int SP_C = 8;                          // columns per group (one n-tile)
@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) ptm_plan_kernel(const double* __
     // Longest-first assignment of the (group, half) items, first to the SM sub-partitions
     // (warps q and q + 4 share sub-partition q and its FP64 pipe; <= 2 SP_IW items each),
     // then within a sub-partition to its two warps (<= SP_IW each). Cost in half-DMMAs:
-    // 10 per k-step, + 1 per k-step for the row-80 DFMA dot of the upper half.
+    // 10 per k-step, 12 for the upper half (its sixth m-tile carries row 80).
     // (Balancing the 8 warps directly left the sub-partitions 1.09 apart at config 4.)
     int sload[4], scnt[4], sit[4][2 * SP_IW];
 #pragma unroll
@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) ptm_plan_kernel(const double* __
       int best = -1, bc = -1;
 #pragma unroll
       for (int i = 0; i < SP_ITEMS; ++i) {
-        const int c = s_ks[i >> 1] * 10 + ((i & 1) ? 0 : s_ks[i >> 1]);
+        const int c = s_ks[i >> 1] * ((i & 1) ? 10 : 12);
         if (!((done >> i) & 1) && c > bc) best = i, bc = c;
       }
       done |= 1u << best;
@@ -576,7 +576,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) ptm_plan_kernel(const double* __
       for (int j = 0; j < 2 * SP_IW; ++j) {
         if (j >= scnt[q]) continue;
         const int i = sit[q][j];
-        const int c = s_ks[i >> 1] * 10 + ((i & 1) ? 0 : s_ks[i >> 1]);
+        const int c = s_ks[i >> 1] * ((i & 1) ? 10 : 12);
         const int v = (wc[0] < SP_IW && (wc[1] >= SP_IW || wl[0] <= wl[1])) ? 0 : 1;
         plan->witem[q + 4 * v][wc[v]] = i;
         wl[v] += c;
@@ -611,42 +611,32 @@ struct WarpItems {
   int g[SP_IW], half[SP_IW], ks[SP_IW], ksoff[SP_IW];
 };
 
-// One work item of Y = X A: group g's 8 columns for m-tiles 5 h .. 5 h + 4
-// (and row 80 when h == 0). BB = gathered B fragments [k-step][lane], KO = row
-// index per (k-step, lane % 4). acc[m] = the C fragment of m-tile 5 h + m;
-// f80 = the row-80 dot for column lane / 4 (reduced over the 4 lanes of the
-// column).
+// One work item of Y = X A: group g's 8 columns for m-tiles 5 h .. 5 h + 4, and
+// for the upper half (MT = 6) a sixth m-tile on rows 80..87 carrying row 80 (its
+// other rows read past the matrix into the next buffer and are never stored:
+// one DMMA per k-step instead of a DFMA dot that waits on the shared FP64 pipe).
+// BB = gathered B fragments [k-step][lane], KO = row index per (k-step, lane % 4).
+template <int MT>
 __device__ __forceinline__ void sparse_item(const double* __restrict__ X, const double* __restrict__ bb,
                                             const int* __restrict__ ko, int ks, int ksoff, int h, int lane,
-                                            double (&acc)[5][2], double& f80) {
+                                            double (&acc)[MT][2]) {
   const int g = lane >> 2, t = lane & 3;
 #pragma unroll
-  for (int m = 0; m < 5; ++m) acc[m][0] = acc[m][1] = 0.0;
-  double fa = 0.0, fb = 0.0;
+  for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = 0.0;
   const double* xa = X + (h * 40 + g) * RS;
+  const double* x80 = X + (80 + g) * RS;
   const double* bq = bb + ksoff * 32 + lane;
   const int* kq = ko + ksoff * 4 + t;
 #pragma unroll 2
   for (int q = 0; q < ks; ++q) {
     const double b = bq[q * 32];
     const int kc = kq[q * 4];
-    double a[5];
+    double a[MT];
 #pragma unroll
-    for (int m = 0; m < 5; ++m) a[m] = xa[m * 8 * RS + kc];
+    for (int m = 0; m < MT; ++m) a[m] = m < 5 ? xa[m * 8 * RS + kc] : x80[kc];
 #pragma unroll
-    for (int m = 0; m < 5; ++m) dmma(acc[m], a[m], b);
-    if (h == 0) {
-      const double x80 = X[80 * RS + kc];
-      if (q & 1)
-        fb = fma(x80, b, fb);
-      else
-        fa = fma(x80, b, fa);
-    }
+    for (int m = 0; m < MT; ++m) dmma(acc[m], a[m], b);
   }
-  double f = fa + fb;
-  f += __shfl_xor_sync(0xffffffffu, f, 1);
-  f += __shfl_xor_sync(0xffffffffu, f, 2);
-  f80 = f;
 }
 
 // K4-S body: A (scaled) dense in SA; SB, SC scratch; BB / KO the gathered
@@ -659,13 +649,12 @@ __device__ __forceinline__ void expm_sparse_body(double* SA, double* SB, double*
                                                  double* __restrict__ out, int w, int lane) {
   const double* cf = c_taylor.v;
   const int g = lane >> 2, t = lane & 3;
-  int col[SP_IW][2], c80[SP_IW];  // output columns of the item (-1: none)
+  int col[SP_IW][2];  // output columns of the item (-1: none)
 #pragma unroll
   for (int i = 0; i < SP_IW; ++i) {
     const bool ok = i < wi.cnt;
     col[i][0] = ok ? plan->cols[wi.g[i]][2 * t] : -1;
     col[i][1] = ok ? plan->cols[wi.g[i]][2 * t + 1] : -1;
-    c80[i] = ok && wi.half[i] == 0 && t == 0 ? plan->cols[wi.g[i]][g] : -1;
   }
   // B0 = c0 I + c1 A, B1 = c6 I + c7 A at the dense product's ownership (the warp's
   // 5 x NB tile block and its fringe dots), so B0 is added to that product in registers
@@ -697,8 +686,15 @@ __device__ __forceinline__ void expm_sparse_body(double* SA, double* SB, double*
 #pragma unroll
     for (int i = 0; i < SP_IW; ++i) {
       if (i >= wi.cnt) continue;
-      double acc[5][2], f80;
-      sparse_item(cur, bb, ko, wi.ks[i], wi.ksoff[i], wi.half[i], lane, acc, f80);
+      double acc[6][2];
+      if (wi.half[i] == 0) {
+        sparse_item<6>(cur, bb, ko, wi.ks[i], wi.ksoff[i], 0, lane, acc);
+      } else {
+        double a5[5][2];
+        sparse_item<5>(cur, bb, ko, wi.ks[i], wi.ksoff[i], 1, lane, a5);
+#pragma unroll
+        for (int m = 0; m < 5; ++m) acc[m][0] = a5[m][0], acc[m][1] = a5[m][1];
+      }
       if (i == 0 && p >= 2) {
         // B0 += c_p X_p, B1 += c_{p+6} X_p from this product's INPUT (complete since the
         // barrier): independent of the DMMAs in flight, so it fills their latency
@@ -727,7 +723,11 @@ __device__ __forceinline__ void expm_sparse_body(double* SA, double* SB, double*
           const int cc = col[i][c];
           if (cc >= 0) nxt[(wi.half[i] * 40 + m * 8 + g) * RS + cc] = acc[m][c];
         }
-      if (c80[i] >= 0) nxt[80 * RS + c80[i]] = f80;
+      if (wi.half[i] == 0 && g == 0) {  // row 80 from the sixth m-tile
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          if (col[i][c] >= 0) nxt[80 * RS + col[i][c]] = acc[5][c];
+      }
     }
     bar_all();
     cur = nxt;
