@@ -593,15 +593,15 @@ def extra_configs(torch, lbg, R, peak):
                 # the real form executes 2 d^4 flops per traj-step (+ the build), so
                 # the reference-form 8 d^4 count would put frac above 1: the
                 # roofline is the EXECUTED rate over the whole pass
-                # K4-S issues 5,600 DMMA.8x8x4 per trajectory (five column-grouped sparse
-                # products A^k A at 720 each + one dense 81 x 81 product at 2,000; 512 flop
-                # each, zeros inside the tiles included) plus ~0.03 M flop of DFMA fringe
-                # (ncu count: profiles/r02_ncu_k4s.txt); the dense s = 3 build issued 5 x 2 x 81^3
+                # K4-S issues 5,960 DMMA.8x8x4 per trajectory (five column-grouped sparse
+                # products A^k A at 792 each + one dense 81 x 81 product at 2,000; 512 flop
+                # each, zeros inside the tiles included) plus ~0.03 M flop of DFMA fringe;
+                # the dense s = 3 build issued 5 x 2 x 81^3
                 build_flops = B * (K4S_DMMAS * 512 + 2 * 81 * 161 + 2 * 80 * 80)
                 exec_tf = (build_flops + B * S * 2 * 81 ** 2) / (ms * 1e-3) / 1e12
                 entry["roofline"] = {"bound": "fp64", "achieved": exec_tf, "peak": peak, "unit": "TFLOP/s",
                                      "frac": exec_tf / peak,
-                                     "counted": "issued FP64 work: build 5,600 DMMA.8x8x4 (512 flop each) + DFMA "
+                                     "counted": "issued FP64 work: build 5,960 DMMA.8x8x4 (512 flop each) + DFMA "
                                                 "fringe per trajectory (sparse-generator build, K4-S) + steps "
                                                 "2 x 81^2 per traj-step",
                                      "reference_form_8d4_frac": tf / peak}
@@ -633,7 +633,7 @@ def extra_configs(torch, lbg, R, peak):
     return out
 
 
-K4S_DMMAS = 5 * 720 + 2000  # per trajectory at config 4 (ncu, profiles/r02_ncu_k4s.txt)
+K4S_DMMAS = 5 * 792 + 2000  # per trajectory at config 4: 72 k-steps x (5 + 6 m-tiles) per sparse product
 EXTRA_REF_SAMPLE = {0: 1, 2: 4096, 3: 256, 4: 2048}  # ~1 s of host work each
 
 
