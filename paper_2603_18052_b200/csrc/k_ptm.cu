@@ -1071,10 +1071,17 @@ __global__ void __maxnreg__(224)
     __syncthreads();
     cur ^= 1;
   }
-  if (writer && live) {
-    const double v = xs[cur][tt][slot];
-    if (row % (D + 1) == 0) pops[size_t(b) * D + row / (D + 1)] = v;
-    atomicAdd(&ens_x[row], v);
+  if (writer && live && row % (D + 1) == 0) pops[size_t(b) * D + row / (D + 1)] = xs[cur][tt][slot];
+  // ensemble sum: the CTA's trajectories combined first, one atomic per coordinate
+  // per CTA (65,536 x 81 same-address atomics per c4 pass otherwise)
+  if (tid < N) {
+    const int64_t b0 = int64_t(blockIdx.x) * STEP_TRAJ;
+    const int q = xpos(tid);
+    double v = 0.0;
+#pragma unroll
+    for (int t = 0; t < STEP_TRAJ; ++t)
+      if (b0 + t < count) v += xs[cur][t][q];
+    atomicAdd(&ens_x[tid], v);
   }
 }
 
