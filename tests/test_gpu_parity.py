@@ -376,6 +376,36 @@ def test_sweep_modes_agree_at_full_size(lbg, torch):
     assert np.abs(er - ec).max() <= TOL_RHO
 
 
+@pytest.mark.parametrize("B", [1, 2, 4, 1100, 16385])
+def test_sweep_ensemble_sum_ragged_batches(lbg, torch, B):
+    """The real path's ensemble sum is combined per CTA of 3 trajectories before
+    its atomics: batches that leave a partial CTA (B % 3 != 0) or a 1-trajectory
+    last chunk (16,385) must still sum every trajectory exactly once — against
+    the complex path (one CTA per trajectory) and the populations."""
+    dev = torch.device("cuda")
+    h0, hd, hs = lbg.config_sweep_terms()
+    _, ops = lbg.config_model(4)
+    delta, scale = lbg.sweep_params(0, B)
+    rho0 = np.zeros((9, 9), complex)
+    rho0[0, 0] = 1.0
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    work = torch.empty(lbg.sweep_workspace(9, B), dtype=torch.uint8, device=dev)
+    out = {}
+    for mode in ("real", "complex"):
+        pops = torch.zeros(B, 9, dtype=torch.float64, device=dev)
+        ens = torch.full((9, 9), float("nan"), dtype=torch.complex128, device=dev)
+        lbg.evolve_sweep_dev(T(h0), T(hd), T(hs), T(ops), T(delta), T(scale), 0.1, T(rho0), 60, pops, ens, work,
+                             mode=mode)
+        torch.cuda.synchronize()
+        out[mode] = pops.cpu().numpy(), ens.cpu().numpy()
+    (pr, er), (pc, ec) = out["real"], out["complex"]
+    assert np.isfinite(er).all()
+    assert np.abs(pr - pc).max() <= TOL_RHO
+    assert np.abs(er - ec).max() <= TOL_RHO * B
+    assert np.abs(np.diag(er).real - pr.sum(axis=0)).max() <= 1e-12 * B
+    assert abs(np.trace(er).real - B) <= 1e-11 * B
+
+
 @pytest.mark.parametrize("dt", [0.07, 0.12, 0.6])
 def test_sweep_real_expm_branches(lbg, torch, dt):
     """k_ptm.cu expm branches: ||A||_1 ~ 0.23 / 0.41 / 2.0 take Taylor degree 12,
