@@ -930,16 +930,18 @@ __device__ __forceinline__ int xpos(int c) { return (c / SC) * XB + c % SC; }
 // sums over its column block x[0..20] (NA accumulators per row), then a
 // butterfly reduce-scatter over the 4 column-block lanes (lane cb keeps the
 // total of row cb of its group).
-template <int NA, bool Perm = false>
-__device__ __forceinline__ double block_row_step(const double (&p)[SR][SC], const double* __restrict__ x, bool hi2,
-                                                 bool hi1) {
+// (C columns per block; init0 seeds the first accumulator of row slot 0.)
+template <int NA, bool Perm = false, int C = SC>
+__device__ __forceinline__ double block_row_step(const double (&p)[SR][C], const double* __restrict__ x, bool hi2,
+                                                 bool hi1, double init0 = 0.0) {
   double acc[SR][NA];
 #pragma unroll
   for (int i = 0; i < SR; ++i)
 #pragma unroll
     for (int a = 0; a < NA; ++a) acc[i][a] = 0.0;
+  acc[0][0] = init0;
 #pragma unroll
-  for (int k = 0; k + 1 < SC; k += 2) {
+  for (int k = 0; k + 1 < C; k += 2) {
     if (k % 10 == 0) asm volatile("" ::: "memory");  // bound how far loads are hoisted
     const double2 v = *reinterpret_cast<const double2*>(x + k);
 #pragma unroll
@@ -948,10 +950,10 @@ __device__ __forceinline__ double block_row_step(const double (&p)[SR][SC], cons
       acc[i][(k + 1) % NA] = fma(p[i][k + 1], v.y, acc[i][(k + 1) % NA]);
     }
   }
-  {
-    const double v = x[SC - 1];
+  if constexpr (C % 2 == 1) {
+    const double v = x[C - 1];
 #pragma unroll
-    for (int i = 0; i < SR; ++i) acc[i][(SC - 1) % NA] = fma(p[i][SC - 1], v, acc[i][(SC - 1) % NA]);
+    for (int i = 0; i < SR; ++i) acc[i][(C - 1) % NA] = fma(p[i][C - 1], v, acc[i][(C - 1) % NA]);
   }
   double r4[SR];
 #pragma unroll
@@ -1085,6 +1087,87 @@ __global__ void __maxnreg__(224)
   }
 }
 
+// K3-T: K3 on the trace-reduced coordinates. P_R maps rho's real coordinates
+// x[0..80] and preserves the trace t = sum_i x[i (D+1)], so x[80] = rho_88 =
+// t - sum_{i<8} x[i (D+1)] and the step is the affine map on x[0..79]
+//   y_r = sum_{c<80} (P_rc - P_r,80 [c = i (D+1)]) x_c + P_r,80 t,   r < 80,
+// with rho_88 recovered once at the end. 80 = 4 x 20 exactly: 4-row x
+// 20-column blocks (80 FMAs and 10 paired loads per lane and step, against 84
+// and 11 for the 84-padded 81 x 81 blocks), 20 row groups per trajectory (240
+// of 256 lanes for 3 trajectories), the offset P_r,80 t seeded into the first
+// accumulator of the lane that finishes row r. The folded entries cost one
+// rounding each; t is exact, so the trace is preserved exactly, where the
+// 81 x 81 map drifts by P_R's own trace error per step (~1e-16).
+constexpr int TC = 20, TGROUPS = 20, TXS = 4 * XB + 2;  // rho_88 parked at 4 * XB for the epilogue
+__device__ __forceinline__ int tpos(int c) { return c < N - 1 ? (c / TC) * XB + c % TC : 4 * XB; }
+
+__global__ void __maxnreg__(224)
+    ptm_step_trace_kernel(const double* __restrict__ p_r, const double* __restrict__ x0, int64_t count,
+                          int64_t steps, double* __restrict__ pops, double* __restrict__ ens_x) {
+  __shared__ __align__(16) double xs[2][STEP_TRAJ][TXS];
+  const int tid = threadIdx.x;
+  const int grp = tid >> 2, cb = tid & 3;
+  const bool active = grp < STEP_TRAJ * TGROUPS;  // the 16 spare lanes shadow the last group
+  const int tt = active ? grp / TGROUPS : STEP_TRAJ - 1;
+  const int rg = active ? grp - tt * TGROUPS : TGROUPS - 1;
+  const int64_t b = int64_t(blockIdx.x) * STEP_TRAJ + tt;
+  const bool live = b < count;
+  const double* pb = p_r + size_t(live ? b : 0) * N * N;
+  double tr = 0.0;
+#pragma unroll
+  for (int i = 0; i < D; ++i) tr += x0[i * (D + 1)];
+  double p[SR][TC];
+  double off = 0.0;
+#pragma unroll
+  for (int i = 0; i < SR; ++i) {
+    const int r = rg * SR + (i ^ cb);  // butterfly order: slot 0 is the lane's own row
+    const double pl = pb[r * N + N - 1];
+#pragma unroll
+    for (int k = 0; k < TC; ++k) {
+      const int c = cb * TC + k;
+      const double v = pb[r * N + c];
+      p[i][k] = c % (D + 1) == 0 ? v - pl : v;
+    }
+    if (i == 0) off = pl * tr;
+  }
+  for (int e = tid; e < STEP_TRAJ * TXS; e += STEP_THREADS) {
+    const int t = e / TXS, q = e - t * TXS, c = (q / XB) * TC + q % XB;
+    xs[0][t][q] = (q < 4 * XB && q % XB < TC) ? x0[c] : 0.0;
+    xs[1][t][q] = 0.0;
+  }
+  __syncthreads();
+  const int row = rg * SR + cb;  // the row this lane finishes (< 80)
+  const int slot = tpos(row);
+  const bool hi2 = cb & 2, hi1 = cb & 1;
+  int cur = 0;
+#pragma unroll 1
+  for (int64_t s = 0; s < steps; ++s) {
+    const double kk = block_row_step<1, true, TC>(p, xs[cur][tt] + cb * XB, hi2, hi1, off);
+    if (active) xs[cur ^ 1][tt][slot] = kk;
+    __syncthreads();
+    cur ^= 1;
+  }
+  if (tid < STEP_TRAJ) {  // rho_88 = t - the other populations (rho0's own at zero steps)
+    double v = tr;
+#pragma unroll
+    for (int i = 0; i < D - 1; ++i) v -= xs[cur][tid][tpos(i * (D + 1))];
+    xs[cur][tid][4 * XB] = steps > 0 ? v : x0[N - 1];
+  }
+  __syncthreads();
+  if (active && live && row % (D + 1) == 0) pops[size_t(b) * D + row / (D + 1)] = xs[cur][tt][slot];
+  if (tid < STEP_TRAJ && int64_t(blockIdx.x) * STEP_TRAJ + tid < count)
+    pops[size_t(int64_t(blockIdx.x) * STEP_TRAJ + tid) * D + D - 1] = xs[cur][tid][4 * XB];
+  if (tid < N) {  // ensemble sum, combined over the CTA's trajectories first
+    const int64_t b0 = int64_t(blockIdx.x) * STEP_TRAJ;
+    const int q = tpos(tid);
+    double v = 0.0;
+#pragma unroll
+    for (int t = 0; t < STEP_TRAJ; ++t)
+      if (b0 + t < count) v += xs[cur][t][q];
+    atomicAdd(&ens_x[tid], v);
+  }
+}
+
 // complex rho (d x d) <-> real coordinates
 __global__ void rho_to_x_kernel(const double2* __restrict__ rho, double* __restrict__ x) {
   const int p = threadIdx.x;
@@ -1175,11 +1258,18 @@ void launch_ptm_sweep(size_t d, const double* h0, const double* hd, const double
   launch_terms(dis, h0, hd, hs, dt, terms, batch, s);
   rho_to_x_kernel<<<1, 96, 0, s>>>(reinterpret_cast<const double2*>(rho0), x0);
   LBG_CHECK_LAUNCH("rho_to_x_kernel");
+  // LBG_PTM_STEP81=1: the 81 x 81 step kernel instead of the trace-reduced one (A/B only)
+  const char* s81 = std::getenv("LBG_PTM_STEP81");
+  const bool step81 = s81 && s81[0] == '1';
   for (int64_t c0 = 0; c0 < batch; c0 += int64_t(chunk)) {
     const int cb = int(std::min<int64_t>(int64_t(chunk), batch - c0));
     launch_expm(terms, delta + c0, scale + c0, pr, cb, s);
-    ptm_step_kernel<<<unsigned((cb + STEP_TRAJ - 1) / STEP_TRAJ), STEP_THREADS, 0, s>>>(
-        pr, x0, cb, steps, pops + c0 * int64_t(D), ens_x);
+    if (step81)
+      ptm_step_kernel<<<unsigned((cb + STEP_TRAJ - 1) / STEP_TRAJ), STEP_THREADS, 0, s>>>(
+          pr, x0, cb, steps, pops + c0 * int64_t(D), ens_x);
+    else
+      ptm_step_trace_kernel<<<unsigned((cb + STEP_TRAJ - 1) / STEP_TRAJ), STEP_THREADS, 0, s>>>(
+          pr, x0, cb, steps, pops + c0 * int64_t(D), ens_x);
     LBG_CHECK_LAUNCH("ptm_step_kernel");
   }
   x_to_rho_kernel<<<1, 96, 0, s>>>(ens_x, reinterpret_cast<double2*>(ens_sum));
