@@ -1099,18 +1099,20 @@ __global__ void __maxnreg__(224)
 // rounding each; t is exact, so the trace is preserved exactly, where the
 // 81 x 81 map drifts by P_R's own trace error per step (~1e-16).
 constexpr int TC = 20, TGROUPS = 20, TXS = 4 * XB + 2;  // rho_88 parked at 4 * XB for the epilogue
+constexpr int T_TRAJ = 3, T_THREADS = 256;
+#define LBG_K3T_MAXREG 224
 __device__ __forceinline__ int tpos(int c) { return c < N - 1 ? (c / TC) * XB + c % TC : 4 * XB; }
 
-__global__ void __maxnreg__(224)
+__global__ void __maxnreg__(LBG_K3T_MAXREG)
     ptm_step_trace_kernel(const double* __restrict__ p_r, const double* __restrict__ x0, int64_t count,
                           int64_t steps, double* __restrict__ pops, double* __restrict__ ens_x) {
-  __shared__ __align__(16) double xs[2][STEP_TRAJ][TXS];
+  __shared__ __align__(16) double xs[2][T_TRAJ][TXS];
   const int tid = threadIdx.x;
   const int grp = tid >> 2, cb = tid & 3;
-  const bool active = grp < STEP_TRAJ * TGROUPS;  // the 16 spare lanes shadow the last group
-  const int tt = active ? grp / TGROUPS : STEP_TRAJ - 1;
+  const bool active = grp < T_TRAJ * TGROUPS;  // the 16 spare lanes shadow the last group
+  const int tt = active ? grp / TGROUPS : T_TRAJ - 1;
   const int rg = active ? grp - tt * TGROUPS : TGROUPS - 1;
-  const int64_t b = int64_t(blockIdx.x) * STEP_TRAJ + tt;
+  const int64_t b = int64_t(blockIdx.x) * T_TRAJ + tt;
   const bool live = b < count;
   const double* pb = p_r + size_t(live ? b : 0) * N * N;
   double tr = 0.0;
@@ -1130,7 +1132,7 @@ __global__ void __maxnreg__(224)
     }
     if (i == 0) off = pl * tr;
   }
-  for (int e = tid; e < STEP_TRAJ * TXS; e += STEP_THREADS) {
+  for (int e = tid; e < T_TRAJ * TXS; e += T_THREADS) {
     const int t = e / TXS, q = e - t * TXS, c = (q / XB) * TC + q % XB;
     xs[0][t][q] = (q < 4 * XB && q % XB < TC) ? x0[c] : 0.0;
     xs[1][t][q] = 0.0;
@@ -1147,22 +1149,22 @@ __global__ void __maxnreg__(224)
     __syncthreads();
     cur ^= 1;
   }
-  if (tid < STEP_TRAJ) {  // rho_88 = t - the other populations (rho0's own at zero steps)
+  if (tid < T_TRAJ) {  // rho_88 = t - the other populations (steps > 0: the host sends 0 steps to K3)
     double v = tr;
 #pragma unroll
     for (int i = 0; i < D - 1; ++i) v -= xs[cur][tid][tpos(i * (D + 1))];
-    xs[cur][tid][4 * XB] = steps > 0 ? v : x0[N - 1];
+    xs[cur][tid][4 * XB] = v;
   }
   __syncthreads();
   if (active && live && row % (D + 1) == 0) pops[size_t(b) * D + row / (D + 1)] = xs[cur][tt][slot];
-  if (tid < STEP_TRAJ && int64_t(blockIdx.x) * STEP_TRAJ + tid < count)
-    pops[size_t(int64_t(blockIdx.x) * STEP_TRAJ + tid) * D + D - 1] = xs[cur][tid][4 * XB];
+  if (tid < T_TRAJ && int64_t(blockIdx.x) * T_TRAJ + tid < count)
+    pops[size_t(int64_t(blockIdx.x) * T_TRAJ + tid) * D + D - 1] = xs[cur][tid][4 * XB];
   if (tid < N) {  // ensemble sum, combined over the CTA's trajectories first
-    const int64_t b0 = int64_t(blockIdx.x) * STEP_TRAJ;
+    const int64_t b0 = int64_t(blockIdx.x) * T_TRAJ;
     const int q = tpos(tid);
     double v = 0.0;
 #pragma unroll
-    for (int t = 0; t < STEP_TRAJ; ++t)
+    for (int t = 0; t < T_TRAJ; ++t)
       if (b0 + t < count) v += xs[cur][t][q];
     atomicAdd(&ens_x[tid], v);
   }
@@ -1260,7 +1262,8 @@ void launch_ptm_sweep(size_t d, const double* h0, const double* hd, const double
   LBG_CHECK_LAUNCH("rho_to_x_kernel");
   // LBG_PTM_STEP81=1: the 81 x 81 step kernel instead of the trace-reduced one (A/B only)
   const char* s81 = std::getenv("LBG_PTM_STEP81");
-  const bool step81 = s81 && s81[0] == '1';
+  // zero steps also take K3, whose rho0 passes through bitwise (K3-T would recompute rho_88)
+  const bool step81 = (s81 && s81[0] == '1') || steps == 0;
   for (int64_t c0 = 0; c0 < batch; c0 += int64_t(chunk)) {
     const int cb = int(std::min<int64_t>(int64_t(chunk), batch - c0));
     launch_expm(terms, delta + c0, scale + c0, pr, cb, s);
@@ -1268,7 +1271,7 @@ void launch_ptm_sweep(size_t d, const double* h0, const double* hd, const double
       ptm_step_kernel<<<unsigned((cb + STEP_TRAJ - 1) / STEP_TRAJ), STEP_THREADS, 0, s>>>(
           pr, x0, cb, steps, pops + c0 * int64_t(D), ens_x);
     else
-      ptm_step_trace_kernel<<<unsigned((cb + STEP_TRAJ - 1) / STEP_TRAJ), STEP_THREADS, 0, s>>>(
+      ptm_step_trace_kernel<<<unsigned((cb + T_TRAJ - 1) / T_TRAJ), T_THREADS, 0, s>>>(
           pr, x0, cb, steps, pops + c0 * int64_t(D), ens_x);
     LBG_CHECK_LAUNCH("ptm_step_kernel");
   }
